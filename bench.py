@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the 3DPIFCM hot path on B200 (BASELINE.json metric:
+"voxel-iterations/s (x particles) and PSO-3DPIFCM wall time, 181x217x181").
+
+One step = one whole PSO-3DPIFCM segmentation (pifcm_segment: normalise ->
+GMM -> FCM start -> 30 generations x 32 particles of the fused IFCM step ->
+final IFCM until eps -> argmax) of the BrainWeb-shaped 181x217x181 synthetic
+phantom (9% noise, C=4), early stop disabled so the work is fixed.
+value = voxel x particle x iterations processed / second (all ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): particles are sharded over ranks (P/N each); the only
+collectives are an all-gather of the per-particle fitness every generation and
+a broadcast of the gbest state (paper_2002_01981_b200/dist.py).
+--impl reference times the fp64 CPU oracle (the paper has no released code):
+one step = one oracle IFCM step of one particle over the same volume.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = "C3: BrainWeb-shaped 181x217x181 synthetic phantom (CSF/GM/WM), 9% noise, C=4, 26-neighbour 3D IFCM, PSO 32 particles x 30 generations"
+METRIC = "voxel-iterations/s (x particles)"
+SHAPE = (181, 217, 181)  # (nz, ny, nx) with nx = 181, ny = 217, nz = 181
+C, P, GENS = 4, 32, 30
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "kstep_summary.json")
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _volume():
+    from inputs import config_volume
+    vol, _ = config_volume("C3")
+    return vol
+
+
+def cpu_baseline_measure(vol, budget_s=20.0):
+    """The oracle as it stands (fp64 C, OpenMP on all host cores) on a bounded
+    sample of the same workload: whole IFCM steps of single particles over the
+    full 181x217x181 volume, repeated until ~budget_s of CPU work."""
+    import numpy as np
+
+    import oracle
+    x = oracle.normalize_u8(vol)
+    c0 = oracle.gmm_init(oracle.histogram_u8(vol), C)
+    U, c, _ = oracle.fcm_run(x, c0, max_iter=1)
+    pos, _ = oracle.pso_init(P, 12345)
+    n_vox = vol.size
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        p = steps % P
+        oracle.ifcm_step(x, U, c, pos[p, 0], pos[p, 1], m=2.0)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or steps >= 64:
+            break
+    del np
+    return {"value": n_vox * steps / el, "unit": "voxel-iterations/s (x particles)",
+            "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{steps} oracle IFCM steps (one particle each, lambda/xi from the bench "
+                      f"swarm) over the full 181x217x181 C3 volume, {el:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle timed on host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    oracle.build_oracle()
+    vol = _volume()
+    x = oracle.normalize_u8(vol)
+    c0 = oracle.gmm_init(oracle.histogram_u8(vol), C)
+    U, c, _ = oracle.fcm_run(x, c0, max_iter=1)
+    pos, _ = oracle.pso_init(P, 12345)
+    for w in range(args.warmup):
+        oracle.ifcm_step(x, U, c, pos[w % P, 0], pos[w % P, 1])
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        oracle.ifcm_step(x, U, c, pos[s % P, 0], pos[s % P, 1])
+    el = time.perf_counter() - t0
+    value = vol.size * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "voxel-iterations/s (x particles)",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "reference_step": "one oracle IFCM step of one particle over the full volume"},
+        "cpu_baseline": {"value": value, "unit": "voxel-iterations/s (x particles)",
+                         "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": f"{args.steps} oracle IFCM steps of one particle each over the full volume"},
+        "e2e": {"value": value, "unit": "voxel-iterations/s (x particles)",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    from paper_2002_01981_b200 import Context, IfcmConfig, PsoConfig
+    from paper_2002_01981_b200 import build as pbuild
+
+    if rank == 0 or not os.path.exists(pbuild.LIB):
+        pbuild.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device(f"cuda:{local_rank}")
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=dev)
+        dist = tdist
+    ctx = Context(local_rank)
+    vol = _volume()
+    nz, ny, nx = vol.shape
+    cfg = IfcmConfig(C=C, m=2.0, q_mode=0, eps=1e-5, max_iter=100)
+    pso = PsoConfig(P=P, ring_k=1, max_gen=GENS, patience=0, seed=12345)
+    vol_d = torch.as_tensor(vol, device=dev)
+    vol_h = torch.as_tensor(vol).pin_memory()
+    lab_h = torch.empty(vol.shape, dtype=torch.uint8).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+
+    if world > 1:
+        from paper_2002_01981_b200.dist import ShardedSegmenter
+        seg = ShardedSegmenter(ctx, cfg, pso, (nz, ny, nx), dist)
+
+        def step():
+            return seg.segment(vol_d)
+
+        def step_host():
+            return seg.segment_host(vol_h, lab_h)
+    else:
+        ws = ctx.workspace(nx, ny, nz, cfg, pso)
+        lab_d = torch.empty(vol.shape, dtype=torch.uint8, device=dev)
+
+        def step():
+            return ctx.segment(vol_d, cfg, pso, ws=ws)[2]
+
+        def step_host():
+            return ctx.segment_host(vol_h, cfg, pso, ws, lab_h)
+
+    # ---- warm-up
+    rep = None
+    for _ in range(args.warmup):
+        rep = step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: device-resident input
+    ctx.timing_enable(True)
+    l0 = ctx.launch_count()
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    vp_total = 0.0
+    reps = []
+    for _ in range(args.steps):
+        rep = step()
+        reps.append(rep)
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop() if clocks else None
+    launches = ctx.launch_count() - l0
+    k_ms, k_n, k_bytes = ctx.timing_read()
+    ctx.timing_enable(False)
+    for r in reps:
+        vp = nx * ny * nz * (r["fcm_iters"] + P * r["generations"] + r["final_iters"])
+        vp_total += vp
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = vp_total / (ms_max * 1e-3)
+
+    # ---- e2e: host buffers through the public C-ABI call (H2D + D2H inside)
+    barrier()
+    h0 = torch.cuda.Event(enable_timing=True)
+    h1 = torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    vp_e2e = 0.0
+    for _ in range(args.steps):
+        r = step_host()
+        vp_e2e += nx * ny * nz * (r["fcm_iters"] + P * r["generations"] + r["final_iters"])
+    h1.record(stream)
+    barrier()
+    te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = vp_e2e / (float(te.item()) * 1e-3)
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    hbm, hbm_kind = _peaks()
+    achieved = (k_bytes / k_n) / ((k_ms / k_n) * 1e-3) / 1e9 if k_n else None
+    traffic = None
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_baseline_measure(vol, budget_s=args.cpu_budget)
+        except Exception as e:  # reported, never silently substituted
+            cpu = {"value": None, "error": str(e), "kind": "oracle"}
+    last = reps[-1]
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "voxel-iterations/s (x particles)",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {
+            "workload": WORKLOAD,
+            "volume": [nx, ny, nz], "C": C, "P": P, "generations": GENS, "m": 2.0,
+            "q_mode": "literal", "eps": 1e-5, "fitness": "chained",
+            "parallelism": f"particles/{world}",
+            "l2": "inputs larger than L2 (65 x 114 MB membership slots, every generation streams 7.3 GB)",
+            "pso_wall_ms": last["t_pso"] * 1e3, "segment_wall_ms": last["t_total"] * 1e3,
+            "fcm_iters": last["fcm_iters"], "final_iters": last["final_iters"],
+            "lambda_star": last["lambda"], "xi_star": last["xi"],
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "k_step_stencil (fused IFCM step, all particles of a generation per launch)",
+            "achieved": achieved,
+            "peak": hbm,
+            "peak_kind": hbm_kind,
+            "unit": "GB/s",
+            "frac": (achieved / hbm) if achieved else None,
+            "traffic": traffic,
+            "alg_bytes_per_launch": (k_bytes / k_n) if k_n else None,
+            "avg_launch_ms": (k_ms / k_n) if k_n else None,
+            "launches": k_n,
+            "share_of_step": (k_ms / ms) if ms else None,
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "voxel-iterations/s (x particles)",
+                "h2d_bytes_per_step": int(vol.size), "d2h_bytes_per_step": int(vol.size)},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

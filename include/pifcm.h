@@ -1,0 +1,293 @@
+/*
+ * pifcm.h -- C ABI of libpifcm.so, the B200 (sm_100a) hot path of 3DPIFCM
+ * (Agranonik, Herman, Last, "Parallel 3DPIFCM Algorithm for Noisy Brain MRI
+ * Images", arXiv 2002.01981).
+ *
+ * Citation shorthand: PAPER:N = line N of the paper text, with the
+ * equation / algorithm it falls in.  "Rk" names a reading of an ambiguous
+ * passage, listed in DESIGN.md §Readings.
+ *
+ * What the library computes ("the step function"):
+ *   one IFCM iteration per voxel i and cluster j, from the previous
+ *   memberships U (Jacobi, R7):
+ *     g_ik  = |x_i - x_k|                               Eq. 6
+ *     q_ik  = dX^2 + dY^2 + dZ^2, q2 per R1            Eq. 8
+ *     k in NB_i = 26-neighbourhood (v = 1)             Eq. 9, R2
+ *     H_ij  = sum_k u_kj g_ik / sum_k g_ik  (0 if 0/0) Eq. 5, R3
+ *     F_ij  = sum_k u_kj^2 q2_ik / sum_k q2_ik          Eq. 7
+ *     d2_ij = (x_i - c_j)^2 max(1 - lam H_ij - xi F_ij, 1e-9)   Eq. 4, R4
+ *     u_ij  = 1 / sum_k (d2_ij / d2_ik)^{1/(m-1)}      Eq. 2, R5
+ *     c_j   = sum_i u_ij^m x_i / sum_i u_ij^m          Eq. 3, R9
+ *     J     = sum_i sum_j u_ij^m d2_ij                 Eq. 1, R8
+ *   evaluated for every PSO particle's (lam, xi) (Alg. 1 steps 4-8,
+ *   PAPER:98-102), inside the whole pipeline of Alg. 1 / Alg. 2
+ *   (PAPER:91-106, 171-187).
+ *
+ * Conventions for every call:
+ *   - Ownership: every buffer is borrowed from the caller (device memory from
+ *     torch / cudaMalloc, or host memory where stated).  The library owns only
+ *     the opaque context (streams/events/host scratch).  Device scratch is the
+ *     caller's workspace `ws`, sized by pifcm_workspace_size(); the library
+ *     never calls cudaMalloc on the compute path.
+ *   - Errors: a negative pifcm_status; no exception crosses the ABI.  All
+ *     arguments are validated before any launch; on failure nothing is
+ *     launched and pifcm_last_error() describes the problem.  Asynchronous
+ *     CUDA errors surface at the next synchronous call as PIFCM_ECUDA.
+ *   - Asynchrony: calls marked "async" enqueue on `stream` and return; calls
+ *     marked "sync" synchronise `stream` before returning.
+ *   - Determinism: every reduction sums fixed-size per-block fp64 partials in
+ *     a fixed order, so results are bit-identical run to run.
+ *   - A context is single-threaded.
+ *
+ * Device layouts:
+ *   x        fp32 [nz][ny][pitch], pitch >= nx, pitch % 4 == 0 (16-byte rows);
+ *            normalised intensities in [0,1] (Alg. 2 step 1).
+ *   U        fp32 "AoS-C4" [P][nz][ny][nx][4]: one 16-byte row per voxel,
+ *            u_i0..u_i(C-1) then zeros.  Rows must sum to 1 (they do for any
+ *            U the library writes).
+ *   centers  fp32 [P][4] (c_0..c_{C-1}, rest ignored).
+ *   lam_xi   fp64 [P][2] (lambda, xi) in [0,1]^2.
+ *   labels   u8 [nz][ny][nx].
+ */
+#ifndef PIFCM_H
+#define PIFCM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the ABI is exported even under -fvisibility=hidden */
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *pifcm_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    PIFCM_OK = 0,
+    PIFCM_EINVAL = -1,   /* invalid argument (range, null pointer, C > 4 ...) */
+    PIFCM_EALIGN = -2,   /* pitch / pointer alignment violated (16-byte rows required) */
+    PIFCM_ENOMEM = -3,   /* workspace smaller than pifcm_workspace_size() */
+    PIFCM_ECUDA = -4,    /* a CUDA runtime error (launch or asynchronous) */
+    PIFCM_ENCCL = -5,    /* reserved: collectives are done by the caller (torch.distributed) */
+    PIFCM_ENUMERIC = -6, /* non-finite cost J */
+    PIFCM_ESTATE = -7    /* call order violated (e.g. pso_step before pso_init) */
+} pifcm_status;
+
+typedef enum { PIFCM_Q_LITERAL = 0, PIFCM_Q_SQEUCLID = 1 } pifcm_qmode; /* R1 */
+typedef enum { PIFCM_FIT_CHAINED = 0 } pifcm_fitness;                   /* R11 */
+typedef enum { PIFCM_U8 = 0, PIFCM_U16 = 1, PIFCM_F32 = 2 } pifcm_dtype;
+
+typedef struct pifcm_ctx pifcm_ctx;
+
+/* Volume extent.  Alg. 1 input "img3d - a 3D matrix of pixel intensities"
+ * (PAPER:93).  nz == 1 is the 2D case (8-neighbourhood). */
+typedef struct {
+    int32_t nx, ny, nz;
+    int32_t pitch; /* elements per x row of the intensity volume; >= nx, % 4 == 0 */
+} pifcm_grid;
+
+/* Method parameters.  Alg. 1 inputs c, v, h, m, epsilon. */
+typedef struct {
+    int32_t C;        /* clusters, 2..4 on the device path                      */
+    float m;          /* fuzzifier, m > 1 (Eq. 2); m == 2 takes a fast path     */
+    int32_t v;        /* shells (Eq. 10); only v == 1 on the device path (R2)   */
+    float h;          /* Eq. 10 decay (> 0); irrelevant at v == 1               */
+    int32_t q_mode;   /* pifcm_qmode (R1)                                       */
+    float eps;        /* stop when max|u_new - u_old| < eps (R14); <= 0: never   */
+    int32_t max_iter; /* iteration cap of the FCM start and final IFCM (R14)    */
+} pifcm_ifcm_cfg;
+
+/* PSO parameters (Alg. 1 steps 3-9; R12). */
+typedef struct {
+    int32_t P;          /* particles, 1..1024                                     */
+    int32_t ring_k;     /* lbest ring radius (>= 0)                               */
+    int32_t max_gen;    /* generation cap (>= 1)                                  */
+    int32_t patience;   /* stop after `patience` calm generations; <= 0: never    */
+    double tol;         /* calm: relative decrease of the gbest J < tol           */
+    double v0;          /* initial |velocity| bound                               */
+    double vmax;        /* velocity clamp                                         */
+    uint64_t seed;      /* Philox4x32-10 key                                      */
+    int32_t fitness_mode; /* pifcm_fitness; CHAINED only                          */
+    int32_t p_begin;    /* this process evaluates particles [p_begin, p_end)      */
+    int32_t p_end;      /*   (particle sharding; 0,0 means all P)                 */
+} pifcm_pso_cfg;
+
+/* Host-side summary of a PSO run (Alg. 1 step 10). */
+typedef struct {
+    double lambda, xi, J;     /* gbest position and fitness                       */
+    int32_t generations;      /* generations run                                  */
+    int32_t gbest_particle;   /* global particle index of the gbest               */
+    float centers[4];         /* gbest centres (the state its evaluation produced)*/
+} pifcm_pso_result;
+
+/* Host-side summary of a whole segmentation. */
+typedef struct {
+    pifcm_pso_result pso;
+    int32_t fcm_iters;        /* iterations of the FCM start (Alg. 1 step 2)      */
+    int32_t final_iters;      /* iterations of the final IFCM (Alg. 1 step 11)    */
+    float c_init[4];          /* GMM centres (R15)                                */
+    float centers[4];         /* final centres                                    */
+    double t_norm, t_init, t_pso, t_final, t_total; /* seconds (CUDA events)      */
+} pifcm_report;
+
+/* ---------------------------------------------------------------- context */
+/* Create a context bound to CUDA device `device`.  Returns PIFCM_OK or
+ * PIFCM_ECUDA / PIFCM_EINVAL.  *out receives the context. */
+int pifcm_ctx_create(int device, pifcm_ctx **out);
+void pifcm_ctx_destroy(pifcm_ctx *ctx);
+/* Message describing the last non-OK status returned with this ctx (never NULL). */
+const char *pifcm_last_error(const pifcm_ctx *ctx);
+/* Library version string. */
+const char *pifcm_version(void);
+
+/* --------------------------------------------------------------- workspace */
+/* Bytes of device workspace needed by pso_* / segment calls for this grid and
+ * configuration (pso may be NULL for pifcm_iterate-only use, in which case the
+ * size covers pifcm_iterate with P = 1).  PIFCM_EINVAL on invalid arguments. */
+int pifcm_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                         const pifcm_pso_cfg *pso, size_t *bytes);
+/* Bytes of device scratch pifcm_iterate needs for P states and `iters`
+ * iterations (0 when iters == 1). */
+int pifcm_iterate_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                                 int32_t P, int32_t iters, size_t *bytes);
+
+/* ------------------------------------------------------------------ iterate */
+/* `iters` Jacobi IFCM iterations (Alg. 2 steps 6-8,
+ * PAPER:179-181) for P independent states over one shared volume: state p
+ * uses (lam_xi[p], centers[p], U_in[p]).  Async.
+ *   x        dev fp32 [nz][ny][pitch]
+ *   U_in     dev fp32 [P][nz][ny][nx][4]   (read only)
+ *   U_out    dev fp32 [P][nz][ny][nx][4]   (result; must not alias U_in)
+ *   centers  dev fp32 [P][4]   in: c used by the first iteration; out: Eq. 3
+ *   lam_xi   dev fp64 [P][2]   lambda, xi in [0,1] (lambda = xi = 0: plain FCM)
+ *   stats    dev fp64 [P][4]   out, nullable: {J, max|du|, iterations, converged}
+ *            of the last iteration run for that state.  J follows R8.
+ *   ws       dev scratch of pifcm_iterate_workspace_size() bytes (NULL if 0).
+ * With cfg->eps > 0 a state stops once its max|du| < eps (its U_out then
+ * holds the converged U); otherwise exactly `iters` iterations run.
+ * Errors: PIFCM_EINVAL (dims, C, m, P < 1, iters < 1, lam/xi range is not
+ * checked on device data), PIFCM_EALIGN (pitch), PIFCM_ENOMEM (ws too small),
+ * PIFCM_ECUDA. */
+int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                  const float *x, const float *U_in, float *U_out, float *centers,
+                  const double *lam_xi, int32_t P, int32_t iters, double *stats,
+                  void *ws, size_t ws_bytes, pifcm_stream stream);
+
+/* --------------------------------------------------------------------- PSO */
+/* Initialise the swarm (Alg. 1 step 3; Alg. 2 step 3)
+ * in the workspace: positions ~ U[0,1]^2 and velocities ~ U[-v0,v0]^2 from
+ * Philox (R12), every particle's state := (U0, c0).  Async.
+ *   U0 dev fp32 [nz][ny][nx][4]; c0 dev fp32 [4].
+ * Errors: PIFCM_EINVAL, PIFCM_ENOMEM, PIFCM_ECUDA. */
+int pifcm_pso_init(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                   const pifcm_pso_cfg *pso, const float *U0, const float *c0,
+                   void *ws, size_t ws_bytes, pifcm_stream stream);
+
+/* Fitness evaluation of this process's particles [p_begin, p_end) for the
+ * current generation (Alg. 1 step 4; CHAINED fitness R11): one
+ * IFCM step of each particle's state at its (lambda, xi); the J values land in
+ * the fitness vector returned by pifcm_pso_fitness_ptr().  Async. */
+int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                   const pifcm_pso_cfg *pso, const float *x, void *ws, size_t ws_bytes,
+                   pifcm_stream stream);
+
+/* Device pointer to the fitness vector fp64 [P] inside `ws` (so that a
+ * multi-process caller can all-gather it between eval and update).  Entries
+ * outside [p_begin, p_end) must be filled by the caller before update. */
+int pifcm_pso_fitness_ptr(const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                          const pifcm_pso_cfg *pso, void *ws, double **fitness);
+
+/* PSO bookkeeping and move after all P fitnesses are known (Alg. 1 steps 5-8,
+ * PAPER:99-102): pbest (strict <), ring lbest, velocity, fly, gbest snapshot
+ * and the stop test of step 9 (R12).  Identical on every process.  Async. */
+int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                     const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, pifcm_stream stream);
+
+/* One generation on one process: pifcm_pso_eval + pifcm_pso_update.  Async. */
+int pifcm_pso_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                   const pifcm_pso_cfg *pso, const float *x, void *ws, size_t ws_bytes,
+                   pifcm_stream stream);
+
+/* Read the swarm summary (sync).  `stopped` (nullable) receives 1 once the
+ * step-9 stop rule fired. */
+int pifcm_pso_result_get(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                         const pifcm_pso_cfg *pso, void *ws, pifcm_pso_result *out,
+                         int32_t *stopped, pifcm_stream stream);
+
+/* Copy the gbest state (the U and centres its evaluation produced, Alg. 1
+ * step 10) to U_out [nz][ny][nx][4] / c_out [4] (device).  PIFCM_ESTATE when
+ * the gbest particle is not evaluated by this process.  Async. */
+int pifcm_pso_gbest_state(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                          const pifcm_pso_cfg *pso, void *ws, float *U_out, float *c_out,
+                          pifcm_stream stream);
+
+/* Whole PSO (Alg. 1 steps 3-10): init from (U0, c0), generations until the
+ * stop rule or max_gen, summary into *out.  Single process.  Sync. */
+int pifcm_pso_run(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                  const pifcm_pso_cfg *pso, const float *x, const float *U0, const float *c0,
+                  void *ws, size_t ws_bytes, pifcm_pso_result *out, pifcm_stream stream);
+
+/* ----------------------------------------------------------- pipeline parts */
+/* Alg. 2 step 1: global min-max normalisation of a device u8
+ * volume [nz][ny][nx] into x [nz][ny][pitch] (constant volume -> 0, R16) and
+ * the 256-bin histogram of R15 into hist (dev int64 [256], nullable).  Async. */
+int pifcm_normalize_u8(pifcm_ctx *ctx, const pifcm_grid *grid, const uint8_t *vol, float *x,
+                       int64_t *hist, void *ws, size_t ws_bytes, pifcm_stream stream);
+
+/* R15 "Modified_FCM with Gaussian mixture model": 1-D EM on
+ * the 256-bin histogram -> C initial centres (fp32 [4], device).  Async. */
+int pifcm_gmm_init(pifcm_ctx *ctx, int32_t C, const int64_t *hist, float *c0, void *ws,
+                   size_t ws_bytes, pifcm_stream stream);
+
+/* Defuzzification (R13): labels = argmax_j u_ij, ties to the
+ * lowest j.  U dev fp32 [nz][ny][nx][4], labels dev u8.  Async. */
+int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float *U,
+                 uint8_t *labels, pifcm_stream stream);
+
+/* --------------------------------------------------------------- pipeline */
+/* The whole method (Alg. 1 / Alg. 2): normalise,
+ * histogram + GMM, FCM start (lambda = xi = 0) until eps, PSO over
+ * (lambda, xi) with CHAINED fitness, final IFCM at the gbest from the gbest's
+ * (U, c) until eps, argmax.  Sync.
+ *   vol      dev u8 [nz][ny][nx] (dtype must be PIFCM_U8 in this version)
+ *   labels   dev u8 [nz][ny][nx]  out
+ *   U_out    dev fp32 [nz][ny][nx][4] out, nullable: final memberships
+ *   z_slice  -1: whole volume.  >= 0: the paper's `z` argument;
+ *            the whole volume is segmented in 3D (R10) and only plane z_slice
+ *            of `labels` is written (labels then points to [ny][nx]).
+ *   rep      host out, nullable.
+ * Errors: as above, plus PIFCM_ENUMERIC for a non-finite fitness. */
+int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, int32_t ny,
+                  int32_t nz, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                  int32_t z_slice, void *ws, size_t ws_bytes, uint8_t *labels, float *U_out,
+                  pifcm_report *rep, pifcm_stream stream);
+
+/* The same pipeline with HOST buffers (vol host u8, labels host u8): copies
+ * the volume in, runs pifcm_segment, copies the labels out.  Sync. */
+int pifcm_segment_host(pifcm_ctx *ctx, const uint8_t *vol_host, int32_t nx, int32_t ny,
+                       int32_t nz, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                       void *ws, size_t ws_bytes, uint8_t *labels_host, pifcm_report *rep,
+                       pifcm_stream stream);
+
+/* Number of kernels this context has launched so far (for the bench's
+ * gpu_launches count). */
+int64_t pifcm_launch_count(const pifcm_ctx *ctx);
+
+/* Device timing of the fused step kernel: when enabled (which resets the
+ * counters), every launch of the neighbourhood (stencil) step kernel is
+ * bracketed by CUDA events on its stream.  pifcm_timing_read synchronises
+ * those events and returns the summed kernel time in ms, the number of
+ * launches, and their algorithmic bytes (per launch: P * nvox * 32 bytes of
+ * AoS-C4 membership read + write, plus nvox * 4 bytes of intensities). */
+int pifcm_timing_enable(pifcm_ctx *ctx, int32_t on);
+int pifcm_timing_read(pifcm_ctx *ctx, double *ms_total, int64_t *launches, double *alg_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* PIFCM_H */

@@ -1,0 +1,306 @@
+"""Python binding of libpifcm.so: the same calls as include/pifcm.h, taking
+torch tensors (device memory) and doing argument marshalling only.  Every
+step of the method runs in the library's CUDA kernels; torch provides device
+memory and streams.
+
+Citations: PAPER:N = line N of the paper text; Rk = DESIGN.md reading k.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _abi
+
+__all__ = ["IfcmConfig", "PsoConfig", "PifcmError", "Context", "pitch_of", "to_pitched_x",
+           "to_aos", "from_aos"]
+
+
+class PifcmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_abi.STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+@dataclass
+class IfcmConfig:
+    """Alg. 1 inputs c, v, h, m, epsilon + reading R1 (q_mode)."""
+    C: int = 4
+    m: float = 2.0
+    v: int = 1
+    h: float = 1.0
+    q_mode: int = _abi.Q_LITERAL
+    eps: float = 1e-5
+    max_iter: int = 100
+
+    def c(self) -> _abi.IfcmCfg:
+        return _abi.IfcmCfg(self.C, self.m, self.v, self.h, self.q_mode, self.eps, self.max_iter)
+
+
+@dataclass
+class PsoConfig:
+    """Alg. 1 steps 3-9, reading R12."""
+    P: int = 32
+    ring_k: int = 1
+    max_gen: int = 30
+    patience: int = 3
+    tol: float = 1e-4
+    v0: float = 0.1
+    vmax: float = 0.5
+    seed: int = 12345
+    p_begin: int = 0
+    p_end: int = 0
+
+    def c(self) -> _abi.PsoCfg:
+        return _abi.PsoCfg(self.P, self.ring_k, self.max_gen, self.patience, self.tol, self.v0,
+                           self.vmax, self.seed, _abi.FIT_CHAINED, self.p_begin, self.p_end)
+
+
+def pitch_of(nx: int) -> int:
+    return (nx + 3) // 4 * 4
+
+
+def to_pitched_x(x, device) -> torch.Tensor:
+    """[nz, ny, nx] intensities -> device fp32 [nz, ny, pitch] (zero padded)."""
+    x = torch.as_tensor(x, dtype=torch.float32)
+    nz, ny, nx = x.shape
+    out = torch.zeros((nz, ny, pitch_of(nx)), dtype=torch.float32, device=device)
+    out[:, :, :nx] = x.to(device)
+    return out
+
+
+def to_aos(U, device) -> torch.Tensor:
+    """[..., N, C] memberships -> device fp32 [..., N, 4] (AoS-C4, zero padded)."""
+    U = torch.as_tensor(U, dtype=torch.float32)
+    shape = list(U.shape)
+    C = shape[-1]
+    shape[-1] = 4
+    out = torch.zeros(shape, dtype=torch.float32, device=device)
+    out[..., :C] = U.to(device)
+    return out
+
+
+def from_aos(U: torch.Tensor, C: int) -> torch.Tensor:
+    return U[..., :C]
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream or None
+
+
+def _grid(nx, ny, nz, pitch=None) -> _abi.Grid:
+    return _abi.Grid(nx, ny, nz, pitch if pitch is not None else pitch_of(nx))
+
+
+@dataclass
+class PsoSummary:
+    lam: float
+    xi: float
+    J: float
+    generations: int
+    gbest_particle: int
+    centers: list = field(default_factory=list)
+
+
+class Context:
+    """Owns a pifcm_ctx on one CUDA device."""
+
+    def __init__(self, device: int | torch.device | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("pifcm needs a CUDA device (no CPU fallback)")
+        if device is None:
+            device = torch.cuda.current_device()
+        if isinstance(device, torch.device):
+            device = device.index if device.index is not None else torch.cuda.current_device()
+        self.device = int(device)
+        self.lib = _abi.load()
+        h = ct.c_void_p()
+        torch.cuda.init()
+        with torch.cuda.device(self.device):
+            rc = self.lib.pifcm_ctx_create(self.device, ct.byref(h))
+        if rc != 0:
+            raise PifcmError(rc, "pifcm_ctx_create failed")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.pifcm_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, rc: int):
+        if rc != 0:
+            raise PifcmError(rc, self.lib.pifcm_last_error(self._h).decode())
+
+    def launch_count(self) -> int:
+        return int(self.lib.pifcm_launch_count(self._h))
+
+    def timing_enable(self, on: bool = True):
+        self._ck(self.lib.pifcm_timing_enable(self._h, 1 if on else 0))
+
+    def timing_read(self):
+        """-> (summed fused-step kernel ms, launches, algorithmic bytes)."""
+        ms, n, b = ct.c_double(), ct.c_int64(), ct.c_double()
+        self._ck(self.lib.pifcm_timing_read(self._h, ct.byref(ms), ct.byref(n), ct.byref(b)))
+        return ms.value, n.value, b.value
+
+    # ------------------------------------------------------------ workspace
+    def workspace_size(self, nx, ny, nz, cfg: IfcmConfig, pso: PsoConfig | None) -> int:
+        n = ct.c_size_t()
+        g = _grid(nx, ny, nz)
+        rc = self.lib.pifcm_workspace_size(ct.byref(g), ct.byref(cfg.c()),
+                                           ct.byref(pso.c()) if pso else None, ct.byref(n))
+        self._ck(rc)
+        return n.value
+
+    def workspace(self, nx, ny, nz, cfg: IfcmConfig, pso: PsoConfig | None) -> torch.Tensor:
+        return torch.empty(self.workspace_size(nx, ny, nz, cfg, pso), dtype=torch.uint8,
+                           device=f"cuda:{self.device}")
+
+    # ------------------------------------------------------------ iterate
+    def iterate(self, x: torch.Tensor, U_in: torch.Tensor, U_out: torch.Tensor,
+                centers: torch.Tensor, lam_xi: torch.Tensor, cfg: IfcmConfig, iters: int = 1,
+                stats: torch.Tensor | None = None, nx: int | None = None, stream=None):
+        """pifcm_iterate: x [nz,ny,pitch] f32; U_in/U_out [P,nz*ny*nx,4] f32;
+        centers [P,4] f32; lam_xi [P,2] f64; stats [P,4] f64 or None."""
+        nz, ny, pitch = x.shape
+        P = U_in.shape[0]
+        if nx is None:
+            nx = U_in.shape[1] // (ny * nz)
+        g = _grid(nx, ny, nz, pitch)
+        n = ct.c_size_t()
+        self._ck(self.lib.pifcm_iterate_workspace_size(ct.byref(g), ct.byref(cfg.c()), P, iters,
+                                                       ct.byref(n)))
+        ws = torch.empty(max(n.value, 1), dtype=torch.uint8, device=x.device)
+        rc = self.lib.pifcm_iterate(self._h, ct.byref(g), ct.byref(cfg.c()), _ptr(x), _ptr(U_in),
+                                    _ptr(U_out), _ptr(centers), _ptr(lam_xi), P, iters, _ptr(stats),
+                                    _ptr(ws), n.value, _stream(stream))
+        self._ck(rc)
+        return U_out
+
+    # ------------------------------------------------------------ PSO
+    def pso_init(self, grid, cfg, pso, U0, c0, ws, stream=None):
+        self._ck(self.lib.pifcm_pso_init(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                         _ptr(U0), _ptr(c0), _ptr(ws), ws.numel(), _stream(stream)))
+
+    def pso_eval(self, grid, cfg, pso, x, ws, stream=None):
+        self._ck(self.lib.pifcm_pso_eval(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                         _ptr(x), _ptr(ws), ws.numel(), _stream(stream)))
+
+    def pso_update(self, grid, cfg, pso, ws, stream=None):
+        self._ck(self.lib.pifcm_pso_update(self._h, ct.byref(grid), ct.byref(cfg.c()),
+                                           ct.byref(pso.c()), _ptr(ws), ws.numel(), _stream(stream)))
+
+    def pso_step(self, grid, cfg, pso, x, ws, stream=None):
+        self._ck(self.lib.pifcm_pso_step(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                         _ptr(x), _ptr(ws), ws.numel(), _stream(stream)))
+
+    def pso_fitness(self, grid, cfg, pso, ws) -> torch.Tensor:
+        """The fp64 [P] fitness vector inside ws, as a tensor view (for all-gather)."""
+        p = ct.c_void_p()
+        self._ck(self.lib.pifcm_pso_fitness_ptr(ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                                _ptr(ws), ct.byref(p)))
+        off = p.value - ws.data_ptr()
+        return ws[off: off + 8 * pso.P].view(torch.float64)
+
+    def pso_result(self, grid, cfg, pso, ws, stream=None):
+        r = _abi.PsoResult()
+        stopped = ct.c_int32()
+        self._ck(self.lib.pifcm_pso_result_get(self._h, ct.byref(grid), ct.byref(cfg.c()),
+                                               ct.byref(pso.c()), _ptr(ws), ct.byref(r),
+                                               ct.byref(stopped), _stream(stream)))
+        return PsoSummary(r.lambda_, r.xi, r.J, r.generations, r.gbest_particle,
+                          list(r.centers)[:cfg.C]), bool(stopped.value)
+
+    def pso_gbest_state(self, grid, cfg, pso, ws, U_out, c_out, stream=None):
+        self._ck(self.lib.pifcm_pso_gbest_state(self._h, ct.byref(grid), ct.byref(cfg.c()),
+                                                ct.byref(pso.c()), _ptr(ws), _ptr(U_out), _ptr(c_out),
+                                                _stream(stream)))
+
+    def pso_run(self, x, U0, c0, cfg, pso, nx, ws=None, stream=None) -> PsoSummary:
+        nz, ny, pitch = x.shape
+        g = _grid(nx, ny, nz, pitch)
+        if ws is None:
+            ws = self.workspace(nx, ny, nz, cfg, pso)
+        r = _abi.PsoResult()
+        self._ck(self.lib.pifcm_pso_run(self._h, ct.byref(g), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                        _ptr(x), _ptr(U0), _ptr(c0), _ptr(ws), ws.numel(), ct.byref(r),
+                                        _stream(stream)))
+        return PsoSummary(r.lambda_, r.xi, r.J, r.generations, r.gbest_particle,
+                          list(r.centers)[:cfg.C])
+
+    # ------------------------------------------------------------ pipeline parts
+    def normalize_u8(self, vol: torch.Tensor, want_hist=True, stream=None):
+        nz, ny, nx = vol.shape
+        g = _grid(nx, ny, nz)
+        x = torch.empty((nz, ny, g.pitch), dtype=torch.float32, device=vol.device)
+        hist = torch.empty(256, dtype=torch.int64, device=vol.device) if want_hist else None
+        ws = torch.empty(256, dtype=torch.uint8, device=vol.device)
+        self._ck(self.lib.pifcm_normalize_u8(self._h, ct.byref(g), _ptr(vol), _ptr(x), _ptr(hist),
+                                             _ptr(ws), 256, _stream(stream)))
+        return x, hist
+
+    def gmm_init(self, hist: torch.Tensor, C: int, stream=None) -> torch.Tensor:
+        c0 = torch.zeros(4, dtype=torch.float32, device=hist.device)
+        self._ck(self.lib.pifcm_gmm_init(self._h, C, _ptr(hist), _ptr(c0), None, 0, _stream(stream)))
+        return c0
+
+    def argmax(self, U: torch.Tensor, nx, ny, nz, C, stream=None) -> torch.Tensor:
+        labels = torch.empty((nz, ny, nx), dtype=torch.uint8, device=U.device)
+        g = _grid(nx, ny, nz)
+        self._ck(self.lib.pifcm_argmax(self._h, ct.byref(g), C, _ptr(U), _ptr(labels), _stream(stream)))
+        return labels
+
+    # ------------------------------------------------------------ pipeline
+    def segment(self, vol: torch.Tensor, cfg: IfcmConfig, pso: PsoConfig, ws=None, want_U=False,
+                z_slice: int = -1, stream=None):
+        """pifcm_segment on a device u8 volume [nz, ny, nx] -> (labels, U or None, report)."""
+        nz, ny, nx = vol.shape
+        if ws is None:
+            ws = self.workspace(nx, ny, nz, cfg, pso)
+        if z_slice < 0:
+            labels = torch.empty((nz, ny, nx), dtype=torch.uint8, device=vol.device)
+        else:
+            labels = torch.empty((ny, nx), dtype=torch.uint8, device=vol.device)
+        U = torch.empty((nz * ny * nx, 4), dtype=torch.float32, device=vol.device) if want_U else None
+        rep = _abi.Report()
+        self._ck(self.lib.pifcm_segment(self._h, _ptr(vol), _abi.U8, nx, ny, nz, ct.byref(cfg.c()),
+                                        ct.byref(pso.c()), z_slice, _ptr(ws), ws.numel(), _ptr(labels),
+                                        _ptr(U), ct.byref(rep), _stream(stream)))
+        return labels, U, report_dict(rep, cfg.C)
+
+    def segment_host(self, vol_host: torch.Tensor, cfg: IfcmConfig, pso: PsoConfig, ws,
+                     labels_host: torch.Tensor, stream=None):
+        """pifcm_segment_host: host (pinned) u8 volume in, host u8 labels out."""
+        nz, ny, nx = vol_host.shape
+        rep = _abi.Report()
+        self._ck(self.lib.pifcm_segment_host(self._h, _ptr(vol_host), nx, ny, nz, ct.byref(cfg.c()),
+                                             ct.byref(pso.c()), _ptr(ws), ws.numel(), _ptr(labels_host),
+                                             ct.byref(rep), _stream(stream)))
+        return report_dict(rep, cfg.C)
+
+
+def report_dict(rep: _abi.Report, C: int) -> dict:
+    return {
+        "lambda": rep.pso.lambda_, "xi": rep.pso.xi, "J": rep.pso.J,
+        "generations": rep.pso.generations, "gbest_particle": rep.pso.gbest_particle,
+        "fcm_iters": rep.fcm_iters, "final_iters": rep.final_iters,
+        "c_init": list(rep.c_init)[:C], "centers": list(rep.centers)[:C],
+        "t_norm": rep.t_norm, "t_init": rep.t_init, "t_pso": rep.t_pso, "t_final": rep.t_final,
+        "t_total": rep.t_total,
+    }

@@ -1,0 +1,510 @@
+// aux_kernels.cu -- everything on the path except the fused step: the Eq. 3 /
+// Eq. 1 finalisation, the device PSO (Alg. 1 steps 3-8), normalisation and
+// histogram (Alg. 2 step 1), the GMM start (R15), defuzzification.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "pifcm_internal.cuh"
+
+namespace pifcm {
+
+// ---------------------------------------------------------------- finalize
+// Fixed-order fp64 sum of the per-block partial records of state p, then
+// Eq. 3: c_j = sum u^m x / sum u^m (keep c_j if the sum < 1e-12,
+// R9) and Eq. 1: J = sum of the per-voxel costs.
+constexpr int kFinThreads = 256;
+
+__global__ void __launch_bounds__(kFinThreads) k_finalize(const FinalizeArgs a) {
+    __shared__ double red[kFinThreads][kNR];
+    const int p = blockIdx.x;
+    if (a.stop && *a.stop) return;
+    if (a.stats && a.stats[4 * p + 3] != 0.0) return;
+    const double *src = a.partials + (long long)p * a.nblk * kNR;
+    double v[kNR];
+#pragma unroll
+    for (int r = 0; r < kNR; ++r) v[r] = 0.0;
+    for (int b = threadIdx.x; b < a.nblk; b += kFinThreads) {
+#pragma unroll
+        for (int r = 0; r < kNR - 1; ++r) v[r] += src[(long long)b * kNR + r];
+        v[kNR - 1] = fmax(v[kNR - 1], src[(long long)b * kNR + kNR - 1]);
+    }
+#pragma unroll
+    for (int r = 0; r < kNR; ++r) red[threadIdx.x][r] = v[r];
+    __syncthreads();
+    for (int s = kFinThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+#pragma unroll
+            for (int r = 0; r < kNR - 1; ++r) red[threadIdx.x][r] += red[threadIdx.x + s][r];
+            red[threadIdx.x][kNR - 1] = fmax(red[threadIdx.x][kNR - 1], red[threadIdx.x + s][kNR - 1]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double J = red[0][2 * kMaxC], du = red[0][2 * kMaxC + 1];
+        for (int j = 0; j < a.C; ++j) {
+            const double num = red[0][j], den = red[0][kMaxC + j];
+            if (den >= kDenEps) a.centers[4 * p + j] = (float)(num / den);
+        }
+        if (a.fitness) a.fitness[p] = J;
+        if (a.stats) {
+            a.stats[4 * p + 0] = J;
+            a.stats[4 * p + 1] = du;
+            a.stats[4 * p + 2] += 1.0;
+            a.stats[4 * p + 3] = (a.eps > 0.f && du < (double)a.eps) ? 1.0 : 0.0;
+        }
+        if (!isfinite(J) && a.status) atomicExch(a.status, (int)PIFCM_ENUMERIC);
+    }
+}
+
+cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st) {
+    k_finalize<<<a.P, kFinThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// After an early-converged pifcm_iterate: the last U of state p was written
+// by iteration stats[p][2]; iterations t with (iters - t) odd wrote to the
+// scratch buffer, so those states are copied to U_out.
+__global__ void k_fixup_copy(const float4 *scratch, float4 *out, long long nvox, int iters,
+                             const double *stats) {
+    const int p = blockIdx.y;
+    const int done = (int)stats[4 * p + 2];
+    if (((iters - done) & 1) == 0) return;
+    const float4 *s = scratch + (long long)p * nvox;
+    float4 *o = out + (long long)p * nvox;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nvox;
+         i += (long long)gridDim.x * blockDim.x)
+        o[i] = s[i];
+}
+
+cudaError_t launch_fixup_copy(const float4 *scratch, float4 *out, long long nvox, int P,
+                              const double *stats, int iters, cudaStream_t st) {
+    dim3 grid(148 * 4, P);
+    k_fixup_copy<<<grid, 256, 0, st>>>(scratch, out, nvox, iters, stats);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- Philox
+// Philox4x32-10 (Salmon et al. SC'11), the counter-based generator shared by
+// specification (not code) with the oracle so both see the same draws (R12).
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint32_t lo0 = 0xD2511F53u * c[0];
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]);
+        const uint32_t lo1 = 0xCD9E8D57u * c[2];
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]);
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+// Two uniform doubles in [0,1) (53 bits each) for counter (c0, c1, c2, 0).
+__device__ __forceinline__ void draw2(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t k0,
+                                      uint32_t k1, double &a, double &b) {
+    uint32_t c[4] = {c0, c1, c2, 0u};
+    philox4x32_10(c, k0, k1);
+    const unsigned long long wa = ((unsigned long long)c[1] << 32) | c[0];
+    const unsigned long long wb = ((unsigned long long)c[3] << 32) | c[2];
+    a = (double)(wa >> 11) * (1.0 / 9007199254740992.0);
+    b = (double)(wb >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// ---------------------------------------------------------------- PSO init
+// Alg. 1 step 3: positions ~ U[0,1]^2 from counter
+// (0xFFFFFFFF, p, 1, 0), velocities ~ U[-v0, v0]^2 from (0xFFFFFFFF, p, 2, 0)
+// (R12).  Every local particle's state is slot 0 (the start state); the first
+// evaluation of local particle q writes slot 1 + q.
+__global__ void k_pso_init(SwarmDev s, int P, int Pl, int p0, double v0, uint32_t k0,
+                           uint32_t k1, const float *c0, int nslots) {
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+        double a, b;
+        draw2(0xFFFFFFFFu, (uint32_t)p, 1u, k0, k1, a, b);
+        s.pos[2 * p] = a;
+        s.pos[2 * p + 1] = b;
+        draw2(0xFFFFFFFFu, (uint32_t)p, 2u, k0, k1, a, b);
+        s.vel[2 * p] = (2.0 * a - 1.0) * v0;
+        s.vel[2 * p + 1] = (2.0 * b - 1.0) * v0;
+        s.pbf[p] = INFINITY;
+        s.pbx[2 * p] = s.pos[2 * p];
+        s.pbx[2 * p + 1] = s.pos[2 * p + 1];
+        s.fit[p] = INFINITY;
+    }
+    for (int q = threadIdx.x; q < Pl; q += blockDim.x) {
+        s.cur[q] = 0;
+        s.nxt[q] = 1 + q;
+        for (int j = 0; j < kMaxC; ++j) s.centers[4 * q + j] = c0[j];
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 16; ++i) s.hdr[i] = 0;
+        s.hdr[kHGbest] = -1;
+        s.hdr[kHGbestSlot] = -1;
+        s.hdr[kHInit] = 1;
+        s.dhdr[kDPrevGf] = INFINITY;
+        s.dhdr[kDGbestJ] = INFINITY;
+        s.dhdr[kDGbestL] = 0.0;
+        s.dhdr[kDGbestX] = 0.0;
+        for (int j = 0; j < kMaxC; ++j) s.gbest_c[j] = c0[j];
+    }
+    (void)nslots;
+}
+
+cudaError_t launch_pso_init(SwarmDev s, int P, int Pl, int p0, double v0, uint32_t k0,
+                            uint32_t k1, const float *c0, int nslots, cudaStream_t st) {
+    k_pso_init<<<1, 256, 0, st>>>(s, P, Pl, p0, v0, k0, k1, c0, nslots);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- PSO update
+// After the fitnesses f[P] of generation t (evaluated at s.pos) are known:
+//   step 5:  pbest, strict <
+//   gbest = argmin pbest (lowest index on ties); on a strict improvement the
+//           gbest snapshot (Alg. 1 step 10) = the state that
+//           particle's evaluation produced (its new slot), pinned
+//   step 6: lbest over the ring {p-k..p+k} mod P (R12)
+//   step 7: v += p1 (pbest - x) + p2 (lbest - x), |v| <= vmax, with
+//           (p1, p2) from Philox counter (t, p, 0, 0)
+//   step 8: x = clamp(x + v, 0, 1)
+//   step 9: calm generations counter and stop flag (R12)
+// Slots: each local particle's new state is in nxt[q] -> becomes cur[q]; the
+// next evaluation writes to the lowest-numbered slots that are neither a
+// current state nor the pinned gbest (2*Pl + 1 slots always suffice).
+constexpr int kPsoThreads = 256;
+
+__global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs a) {
+    SwarmDev s = a.s;
+    __shared__ int lb_sh[1024];
+    if (s.hdr[kHStop]) return;
+    const int t = s.hdr[kHGen];
+    // step 5 (and remember the evaluation positions)
+    for (int p = threadIdx.x; p < a.P; p += blockDim.x) {
+        s.evalpos[2 * p] = s.pos[2 * p];
+        s.evalpos[2 * p + 1] = s.pos[2 * p + 1];
+        const double f = s.fit[p];
+        if (f < s.pbf[p]) {
+            s.pbf[p] = f;
+            s.pbx[2 * p] = s.pos[2 * p];
+            s.pbx[2 * p + 1] = s.pos[2 * p + 1];
+        }
+    }
+    __syncthreads();
+    // step 6: ring lbest
+    for (int p = threadIdx.x; p < a.P; p += blockDim.x) {
+        int best = -1;
+        for (int d = -a.ring_k; d <= a.ring_k; ++d) {
+            const int q = ((p + d) % a.P + a.P) % a.P;
+            if (best < 0 || s.pbf[q] < s.pbf[best] || (s.pbf[q] == s.pbf[best] && q < best))
+                best = q;
+        }
+        lb_sh[p] = best;
+    }
+    if (threadIdx.x == 0) {
+        // gbest, snapshot, slots, stop rule
+        int g = 0;
+        for (int p = 1; p < a.P; ++p)
+            if (s.pbf[p] < s.pbf[g]) g = p;
+        const double gf_old = s.dhdr[kDGbestJ];
+        const int improved = (s.pbf[g] < gf_old) ? 1 : 0;
+        for (int q = 0; q < a.Pl; ++q) s.cur[q] = s.nxt[q];
+        if (improved) {
+            s.hdr[kHGbest] = g;
+            s.dhdr[kDGbestJ] = s.pbf[g];
+            s.dhdr[kDGbestL] = s.pos[2 * g];
+            s.dhdr[kDGbestX] = s.pos[2 * g + 1];
+            const int gl = g - a.p0;
+            if (gl >= 0 && gl < a.Pl) {
+                s.hdr[kHGbestSlot] = s.cur[gl];
+                for (int j = 0; j < kMaxC; ++j) s.gbest_c[j] = s.centers[4 * gl + j];
+            } else {
+                s.hdr[kHGbestSlot] = -1;
+            }
+        }
+        s.hdr[kHImproved] = improved;
+        // free-slot assignment for the next evaluation
+        unsigned int used[(2 * 1024 + 1 + 31) / 32];
+        const int nw = (a.nslots + 31) / 32;
+        for (int w = 0; w < nw; ++w) used[w] = 0u;
+        for (int q = 0; q < a.Pl; ++q) used[s.cur[q] >> 5] |= 1u << (s.cur[q] & 31);
+        const int gs = s.hdr[kHGbestSlot];
+        if (gs >= 0) used[gs >> 5] |= 1u << (gs & 31);
+        int next_free = 0;
+        for (int q = 0; q < a.Pl; ++q) {
+            while (used[next_free >> 5] & (1u << (next_free & 31))) ++next_free;
+            s.nxt[q] = next_free++;
+        }
+        // step 9 stop rule on the relative decrease of the gbest fitness
+        const double gf = s.pbf[g];
+        if (t > 0 && a.patience > 0) {
+            const double rel = (s.dhdr[kDPrevGf] - gf) / (gf > 0.0 ? gf : 1.0);
+            s.hdr[kHCalm] = (rel < a.tol) ? s.hdr[kHCalm] + 1 : 0;
+            if (s.hdr[kHCalm] >= a.patience) s.hdr[kHStop] = 1;
+        }
+        s.dhdr[kDPrevGf] = gf;
+        s.hdr[kHGen] = t + 1;
+    }
+    __syncthreads();
+    // steps 7-8
+    for (int p = threadIdx.x; p < a.P; p += blockDim.x) {
+        double p1, p2;
+        draw2((uint32_t)t, (uint32_t)p, 0u, a.key0, a.key1, p1, p2);
+        const int lb = lb_sh[p];
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            double v = s.vel[2 * p + d] + p1 * (s.pbx[2 * p + d] - s.pos[2 * p + d]) +
+                       p2 * (s.pbx[2 * lb + d] - s.pos[2 * p + d]);
+            v = fmin(fmax(v, -a.vmax), a.vmax);
+            s.vel[2 * p + d] = v;
+            s.pos[2 * p + d] = fmin(fmax(s.pos[2 * p + d] + v, 0.0), 1.0);
+        }
+    }
+}
+
+cudaError_t launch_pso_update(const PsoUpdateArgs &a, cudaStream_t st) {
+    k_pso_update<<<1, kPsoThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+// gbest (lambda*, xi*) -> a [1][2] lam_xi buffer for the final IFCM.
+__global__ void k_set_lamxi(double *dst, const double *dhdr) {
+    dst[0] = dhdr[kDGbestL];
+    dst[1] = dhdr[kDGbestX];
+}
+cudaError_t launch_set_lamxi(double *dst, const double *dhdr, cudaStream_t st) {
+    k_set_lamxi<<<1, 1, 0, st>>>(dst, dhdr);
+    return cudaGetLastError();
+}
+
+// Copy the pinned gbest slot to U_out and its centres to c_out.
+__global__ void k_gather_gbest(const float4 *slots, long long nvox, const int *hdr,
+                               const float *gbest_c, float4 *U_out, float *c_out) {
+    const int gs = hdr[kHGbestSlot];
+    if (gs < 0) return;
+    const float4 *src = slots + (long long)gs * nvox;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nvox;
+         i += (long long)gridDim.x * blockDim.x)
+        U_out[i] = src[i];
+    if (blockIdx.x == 0 && threadIdx.x < kMaxC && c_out) c_out[threadIdx.x] = gbest_c[threadIdx.x];
+}
+cudaError_t launch_gather_gbest(const float4 *slots, long long nvox, const int *hdr,
+                                const float *gbest_c, float4 *U_out, float *c_out,
+                                cudaStream_t st) {
+    k_gather_gbest<<<148 * 4, 256, 0, st>>>(slots, nvox, hdr, gbest_c, U_out, c_out);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- normalise
+// Alg. 2 step 1: global min / max of the u8 volume.
+__global__ void k_minmax_u8(const uint8_t *vol, long long n, unsigned int *mm) {
+    unsigned int lo = 255u, hi = 0u;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const unsigned int v = vol[i];
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+__global__ void k_mm_reset(unsigned int *mm) {
+    mm[0] = 255u;
+    mm[1] = 0u;
+}
+cudaError_t launch_minmax_u8(const uint8_t *vol, long long n, unsigned int *mm, cudaStream_t st) {
+    k_mm_reset<<<1, 1, 0, st>>>(mm);
+    long long b = (n + 256 * 16 - 1) / (256 * 16);
+    if (b > 148 * 8) b = 148 * 8;
+    if (b < 1) b = 1;
+    k_minmax_u8<<<(int)b, 256, 0, st>>>(vol, n, mm);
+    return cudaGetLastError();
+}
+
+// x = (v - min) / (max - min) in IEEE fp32 (constant volume -> 0, R16), pitched rows.
+__global__ void k_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int pitch,
+                               const unsigned int *mm, float *x) {
+    const int lo = (int)mm[0], hi = (int)mm[1];
+    const float rng = (float)(hi - lo);
+    const long long rows = (long long)ny * nz;
+    const long long n = rows * pitch;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long row = e / pitch;
+        const int X = (int)(e - row * pitch);
+        float v = 0.f;
+        if (X < nx && hi > lo) v = __fdiv_rn((float)((int)vol[row * nx + X] - lo), rng);
+        x[e] = v;
+    }
+}
+cudaError_t launch_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int pitch,
+                                const unsigned int *mm, float *x, cudaStream_t st) {
+    k_normalize_u8<<<148 * 8, 256, 0, st>>>(vol, nx, ny, nz, pitch, mm, x);
+    return cudaGetLastError();
+}
+
+// R15: 256-bin histogram in integers, bin = ((v-min)*255 + (max-min)/2) / (max-min).
+__global__ void k_hist_u8(const uint8_t *vol, long long n, const unsigned int *mm, int64_t *hist) {
+    __shared__ unsigned int h[256];
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0u;
+    __syncthreads();
+    const int lo = (int)mm[0], rng = (int)mm[1] - (int)mm[0];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        int b = 0;
+        if (rng > 0) b = (((int)vol[i] - lo) * 255 + rng / 2) / rng;
+        atomicAdd(&h[b], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x)
+        if (h[b]) atomicAdd((unsigned long long *)&hist[b], (unsigned long long)h[b]);
+}
+__global__ void k_zero_i64(int64_t *p, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
+}
+cudaError_t launch_hist_u8(const uint8_t *vol, long long n, const unsigned int *mm,
+                           int64_t *hist, cudaStream_t st) {
+    k_zero_i64<<<1, 256, 0, st>>>(hist, 256);
+    long long b = (n + 256 * 32 - 1) / (256 * 32);
+    if (b > 148 * 4) b = 148 * 4;
+    if (b < 1) b = 1;
+    k_hist_u8<<<(int)b, 256, 0, st>>>(vol, n, mm, hist);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- GMM start
+// R15 ("Modified_FCM with Gaussian mixture model"): 1-D EM of a
+// C-component mixture on the 256-bin histogram, bin b at level b/255; start
+// mu_j = (j+0.5)/C, sigma_j^2 = 1/(4C^2), w_j = 1/C; variance floor 1e-6;
+// stop when no mean moves by 1e-9 or after max_iter; means sorted ascending;
+// fewer than C occupied bins or coincident means -> c_j = j/(C-1).
+// One block, one thread per bin, fp64, fixed-order tree reductions.
+__device__ double block_sum256(double v, double *sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max_iter, float *c0) {
+    __shared__ double sh[256];
+    __shared__ double mu[kMaxC], s2[kMaxC], w[kMaxC];
+    __shared__ int flag;
+    const int b = threadIdx.x;
+    const double y = (double)b / 255.0;
+    const double n = (double)hist[b];
+    const double Ntot = block_sum256(n, sh);
+    const double occ = block_sum256(n > 0.0 ? 1.0 : 0.0, sh);
+    if (threadIdx.x == 0) {
+        flag = (Ntot <= 0.0 || occ < (double)C) ? 1 : 0;
+        for (int j = 0; j < C; ++j) {
+            mu[j] = ((double)j + 0.5) / (double)C;
+            s2[j] = 1.0 / (4.0 * (double)C * (double)C);
+            w[j] = 1.0 / (double)C;
+        }
+    }
+    __syncthreads();
+    if (flag) {
+        if (threadIdx.x < C) c0[threadIdx.x] = (float)((double)threadIdx.x / (double)(C - 1));
+        return;
+    }
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int it = 0; it < max_iter; ++it) {
+        // E step
+        double r[kMaxC];
+        double s = 0.0;
+        for (int j = 0; j < C; ++j) {
+            const double d = y - mu[j];
+            r[j] = w[j] * exp(-d * d / (2.0 * s2[j])) / sqrt(two_pi * s2[j]);
+            s += r[j];
+        }
+        if (!(s > 0.0)) {
+            int jb = 0;
+            for (int j = 1; j < C; ++j)
+                if (fabs(y - mu[j]) < fabs(y - mu[jb])) jb = j;
+            for (int j = 0; j < C; ++j) r[j] = (j == jb) ? 1.0 : 0.0;
+            s = 1.0;
+        }
+        double Nj[kMaxC], newmu[kMaxC];
+        for (int j = 0; j < C; ++j) {
+            const double rr = (n > 0.0) ? r[j] / s : 0.0;
+            Nj[j] = block_sum256(n * rr, sh);
+            const double Sy = block_sum256(n * rr * y, sh);
+            newmu[j] = (Nj[j] > 1e-12) ? Sy / Nj[j] : mu[j];
+        }
+        double Syy[kMaxC];
+        for (int j = 0; j < C; ++j) {
+            const double rr = (n > 0.0) ? r[j] / s : 0.0;
+            const double d = y - newmu[j];
+            Syy[j] = block_sum256(n * rr * d * d, sh);
+        }
+        if (threadIdx.x == 0) {
+            double shift = 0.0;
+            for (int j = 0; j < C; ++j) {
+                if (Nj[j] > 1e-12) {
+                    w[j] = Nj[j] / Ntot;
+                    s2[j] = fmax(Syy[j] / Nj[j], 1e-6);
+                }
+                shift = fmax(shift, fabs(newmu[j] - mu[j]));
+                mu[j] = newmu[j];
+            }
+            flag = (shift < 1e-9) ? 1 : 0;
+        }
+        __syncthreads();
+        if (flag) break;
+    }
+    if (threadIdx.x == 0) {
+        double m[kMaxC];
+        for (int j = 0; j < C; ++j) m[j] = mu[j];
+        for (int i = 1; i < C; ++i) {
+            const double t = m[i];
+            int k = i - 1;
+            while (k >= 0 && m[k] > t) { m[k + 1] = m[k]; --k; }
+            m[k + 1] = t;
+        }
+        bool degen = false;
+        for (int j = 1; j < C; ++j)
+            if (m[j] - m[j - 1] < 1e-6) degen = true;
+        for (int j = 0; j < kMaxC; ++j)
+            c0[j] = (j < C) ? (float)(degen ? (double)j / (double)(C - 1) : m[j]) : 0.f;
+    }
+}
+
+cudaError_t launch_gmm(const int64_t *hist, int C, int max_iter, float *c0, cudaStream_t st) {
+    k_gmm<<<1, 256, 0, st>>>(hist, C, max_iter, c0);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- argmax
+// Defuzzification (R13): strict > in cluster order, so ties go
+// to the lowest index.
+__global__ void k_argmax(const float4 *U, long long n, int C, uint8_t *labels) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float4 u = U[i];
+        const float v[4] = {u.x, u.y, u.z, u.w};
+        int best = 0;
+        for (int j = 1; j < C; ++j)
+            if (v[j] > v[best]) best = j;
+        labels[i] = (uint8_t)best;
+    }
+}
+cudaError_t launch_argmax(const float4 *U, long long n, int C, uint8_t *labels, cudaStream_t st) {
+    long long b = (n + 255) / 256;
+    if (b > 148 * 16) b = 148 * 16;
+    if (b < 1) b = 1;
+    k_argmax<<<(int)b, 256, 0, st>>>(U, n, C, labels);
+    return cudaGetLastError();
+}
+
+}  // namespace pifcm

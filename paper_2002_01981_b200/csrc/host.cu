@@ -1,0 +1,699 @@
+// host.cu -- the C ABI of libpifcm.so (include/pifcm.h): validation, workspace
+// layout and orchestration of the kernels in step.cu / aux_kernels.cu.
+// Everything on the path runs in those kernels; this file only launches.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "pifcm_internal.cuh"
+
+using namespace pifcm;
+
+struct pifcm_ctx {
+    int device = 0;
+    std::string err = "ok";
+    long long launches = 0;
+    cudaEvent_t ev[8];
+    // fused-step timing (pifcm_timing_*)
+    bool timing = false;
+    std::vector<cudaEvent_t> tev;   // pairs (start, stop)
+    size_t tused = 0;               // events in use
+    double t_ms = 0.0, t_bytes = 0.0, pend_bytes = 0.0;
+    long long t_launches = 0;
+};
+
+namespace {
+
+int fail(pifcm_ctx *ctx, int code, const char *fmt, ...) {
+    if (ctx) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        ctx->err = buf;
+    }
+    return code;
+}
+
+#define CK(ctx, expr)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail((ctx), PIFCM_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                              \
+    } while (0)
+
+#define LAUNCH(ctx, n, expr)       \
+    do {                           \
+        CK(ctx, expr);             \
+        (ctx)->launches += (n);    \
+    } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int check_grid(pifcm_ctx *ctx, const pifcm_grid *g) {
+    if (!g) return fail(ctx, PIFCM_EINVAL, "grid is NULL");
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1)
+        return fail(ctx, PIFCM_EINVAL, "grid dims must be >= 1 (got %d x %d x %d)", g->nx, g->ny, g->nz);
+    if (g->pitch < g->nx) return fail(ctx, PIFCM_EINVAL, "pitch %d < nx %d", g->pitch, g->nx);
+    if (g->pitch % 4 != 0) return fail(ctx, PIFCM_EALIGN, "pitch %d is not a multiple of 4", g->pitch);
+    if ((long long)g->ny * g->nz > (1LL << 31)) return fail(ctx, PIFCM_EINVAL, "volume too large");
+    return PIFCM_OK;
+}
+
+int check_cfg(pifcm_ctx *ctx, const pifcm_ifcm_cfg *c) {
+    if (!c) return fail(ctx, PIFCM_EINVAL, "cfg is NULL");
+    if (c->C < 2 || c->C > kMaxC) return fail(ctx, PIFCM_EINVAL, "C = %d outside [2, 4]", c->C);
+    if (!(c->m > 1.0f) || !(c->m < 1e6f)) return fail(ctx, PIFCM_EINVAL, "m = %g must be > 1", (double)c->m);
+    if (c->v != 1) return fail(ctx, PIFCM_EINVAL, "v = %d: only v = 1 (26-neighbourhood) on the device path", c->v);
+    if (!(c->h > 0.0f)) return fail(ctx, PIFCM_EINVAL, "h must be > 0");
+    if (c->q_mode != PIFCM_Q_LITERAL && c->q_mode != PIFCM_Q_SQEUCLID)
+        return fail(ctx, PIFCM_EINVAL, "q_mode %d unknown", c->q_mode);
+    if (c->max_iter < 1) return fail(ctx, PIFCM_EINVAL, "max_iter must be >= 1");
+    return PIFCM_OK;
+}
+
+int check_pso(pifcm_ctx *ctx, const pifcm_pso_cfg *p) {
+    if (!p) return fail(ctx, PIFCM_EINVAL, "pso cfg is NULL");
+    if (p->P < 1 || p->P > 1024) return fail(ctx, PIFCM_EINVAL, "P = %d outside [1, 1024]", p->P);
+    if (p->ring_k < 0) return fail(ctx, PIFCM_EINVAL, "ring_k must be >= 0");
+    if (p->max_gen < 1) return fail(ctx, PIFCM_EINVAL, "max_gen must be >= 1");
+    if (!(p->vmax > 0.0) || !(p->v0 >= 0.0)) return fail(ctx, PIFCM_EINVAL, "vmax > 0, v0 >= 0 required");
+    if (p->fitness_mode != PIFCM_FIT_CHAINED) return fail(ctx, PIFCM_EINVAL, "only CHAINED fitness");
+    const bool all = (p->p_begin == 0 && p->p_end == 0);
+    if (!all && (p->p_begin < 0 || p->p_end > p->P || p->p_begin >= p->p_end))
+        return fail(ctx, PIFCM_EINVAL, "particle range [%d, %d) invalid for P = %d", p->p_begin, p->p_end, p->P);
+    return PIFCM_OK;
+}
+
+void prange(const pifcm_pso_cfg *p, int *p0, int *pl) {
+    if (p->p_begin == 0 && p->p_end == 0) { *p0 = 0; *pl = p->P; }
+    else { *p0 = p->p_begin; *pl = p->p_end - p->p_begin; }
+}
+
+// Workspace layout (all offsets 256-byte aligned).
+struct Layout {
+    size_t x, vol, lab, hist, mm, c0, slots, hdr, dhdr, pos, vel, pbf, pbx, fit, evalpos, cur, nxt,
+        gbc, cent, part, stats, lamxi, total;
+    int nslots, P, Pl, p0, nblk;
+    long long nvox;
+};
+
+Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg *pso) {
+    (void)c;
+    Layout L{};
+    L.nvox = (long long)g->nx * g->ny * g->nz;
+    int P = 1, p0 = 0, Pl = 1;
+    if (pso) { P = pso->P; prange(pso, &p0, &Pl); }
+    L.P = P; L.Pl = Pl; L.p0 = p0;
+    L.nslots = 2 * Pl + 1;
+    const int nb_s = step_nblk(g->nx, g->ny, g->nz, true), nb_p = step_nblk(g->nx, g->ny, g->nz, false);
+    L.nblk = nb_s > nb_p ? nb_s : nb_p;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+    L.x = take(sizeof(float) * (size_t)g->pitch * g->ny * g->nz);
+    L.vol = take((size_t)L.nvox);
+    L.lab = take((size_t)L.nvox);
+    L.hist = take(sizeof(int64_t) * 256);
+    L.mm = take(sizeof(unsigned int) * 2);
+    L.c0 = take(sizeof(float) * 4);
+    L.slots = take(sizeof(float4) * (size_t)L.nvox * L.nslots);
+    L.hdr = take(sizeof(int) * 16);
+    L.dhdr = take(sizeof(double) * 16);
+    L.pos = take(sizeof(double) * 2 * P);
+    L.vel = take(sizeof(double) * 2 * P);
+    L.pbf = take(sizeof(double) * P);
+    L.pbx = take(sizeof(double) * 2 * P);
+    L.fit = take(sizeof(double) * P);
+    L.evalpos = take(sizeof(double) * 2 * P);
+    L.cur = take(sizeof(int) * Pl);
+    L.nxt = take(sizeof(int) * Pl);
+    L.gbc = take(sizeof(float) * 4);
+    L.cent = take(sizeof(float) * 4 * (Pl > 2 ? Pl : 2));
+    L.part = take(sizeof(double) * kNR * (size_t)L.nblk * (Pl > 1 ? Pl : 1));
+    L.stats = take(sizeof(double) * 4 * (Pl > 1 ? Pl : 1));
+    L.lamxi = take(sizeof(double) * 2 * (Pl > 1 ? Pl : 1));
+    L.total = o;
+    return L;
+}
+
+template <typename T>
+T *at(void *ws, size_t off) { return reinterpret_cast<T *>(static_cast<char *>(ws) + off); }
+
+SwarmDev swarm_of(void *ws, const Layout &L) {
+    SwarmDev s;
+    s.hdr = at<int>(ws, L.hdr);
+    s.dhdr = at<double>(ws, L.dhdr);
+    s.pos = at<double>(ws, L.pos);
+    s.vel = at<double>(ws, L.vel);
+    s.pbf = at<double>(ws, L.pbf);
+    s.pbx = at<double>(ws, L.pbx);
+    s.fit = at<double>(ws, L.fit);
+    s.evalpos = at<double>(ws, L.evalpos);
+    s.cur = at<int>(ws, L.cur);
+    s.nxt = at<int>(ws, L.nxt);
+    s.gbest_c = at<float>(ws, L.gbc);
+    s.centers = at<float>(ws, L.cent);
+    return s;
+}
+
+int check_ws(pifcm_ctx *ctx, void *ws, size_t ws_bytes, size_t need) {
+    if (need > 0 && !ws) return fail(ctx, PIFCM_EINVAL, "workspace is NULL");
+    if (ws_bytes < need) return fail(ctx, PIFCM_ENOMEM, "workspace %zu bytes < required %zu", ws_bytes, need);
+    if (ws && (reinterpret_cast<uintptr_t>(ws) & 255u))
+        return fail(ctx, PIFCM_EALIGN, "workspace must be 256-byte aligned");
+    return PIFCM_OK;
+}
+
+// One step launch + finalize for P states.
+int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x,
+             const float4 *Uin, float4 *Uout, const int *in_idx, const int *out_idx,
+             float *centers, const double *lamxi, bool stencil, int first, int P,
+             double *partials, double *fitness, double *stats, float eps, int *status,
+             const int *stop, cudaStream_t st) {
+    StepArgs a{};
+    a.x = x;
+    a.nx = g->nx; a.ny = g->ny; a.nz = g->nz; a.pitch = g->pitch;
+    a.nvox = (long long)g->nx * g->ny * g->nz;
+    a.U_in = Uin; a.U_out = Uout; a.in_idx = in_idx; a.out_idx = out_idx;
+    a.centers = centers; a.lam_xi = lamxi; a.partials = partials;
+    a.stats = stats; a.stop = stop;
+    a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f);
+    a.q_mode = cfg->q_mode; a.first = first;
+    const bool timed = ctx->timing && stencil;
+    if (timed) {
+        while (ctx->tev.size() < ctx->tused + 2) {
+            cudaEvent_t e;
+            CK(ctx, cudaEventCreate(&e));
+            ctx->tev.push_back(e);
+        }
+        CK(ctx, cudaEventRecord(ctx->tev[ctx->tused], st));
+    }
+    LAUNCH(ctx, 1, launch_step(a, cfg->C, stencil, P, st));
+    if (timed) {
+        CK(ctx, cudaEventRecord(ctx->tev[ctx->tused + 1], st));
+        ctx->tused += 2;
+        ctx->pend_bytes += 32.0 * (double)a.nvox * P + 4.0 * (double)a.nvox;
+        ctx->t_launches += 1;
+    }
+    FinalizeArgs f{};
+    f.partials = partials;
+    f.nblk = step_nblk(g->nx, g->ny, g->nz, stencil);
+    f.C = cfg->C; f.P = P; f.centers = centers; f.fitness = fitness; f.stats = stats;
+    f.eps = eps; f.status = status; f.stop = stop;
+    LAUNCH(ctx, 1, launch_finalize(f, st));
+    return PIFCM_OK;
+}
+
+// lambda = xi = 0 exactly -> the pointwise FCM kernel (Eq. 4 reduces to the plain distance).
+bool host_zero_lamxi(const double *lamxi_dev, int P, cudaStream_t st, bool *ok) {
+    double buf[2 * 64];
+    if (P > 64) { *ok = true; return false; }
+    if (cudaMemcpyAsync(buf, lamxi_dev, sizeof(double) * 2 * P, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) { *ok = false; return false; }
+    *ok = true;
+    for (int i = 0; i < 2 * P; ++i)
+        if (buf[i] != 0.0) return false;
+    return true;
+}
+
+}  // namespace
+
+// ============================================================== ABI: context
+extern "C" {
+
+const char *pifcm_version(void) { return "pifcm-b200 0.1 (sm_100a)"; }
+
+int pifcm_ctx_create(int device, pifcm_ctx **out) {
+    if (!out) return PIFCM_EINVAL;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return PIFCM_ECUDA;
+    if (cudaSetDevice(device) != cudaSuccess) return PIFCM_ECUDA;
+    pifcm_ctx *c = new pifcm_ctx();
+    c->device = device;
+    for (int i = 0; i < 8; ++i)
+        if (cudaEventCreate(&c->ev[i]) != cudaSuccess) { delete c; return PIFCM_ECUDA; }
+    *out = c;
+    return PIFCM_OK;
+}
+
+void pifcm_ctx_destroy(pifcm_ctx *ctx) {
+    if (!ctx) return;
+    for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->ev[i]);
+    for (cudaEvent_t e : ctx->tev) cudaEventDestroy(e);
+    delete ctx;
+}
+
+const char *pifcm_last_error(const pifcm_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t pifcm_launch_count(const pifcm_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+static int timing_drain(pifcm_ctx *ctx) {
+    for (size_t i = 0; i + 1 < ctx->tused; i += 2) {
+        CK(ctx, cudaEventSynchronize(ctx->tev[i + 1]));
+        float ms = 0.f;
+        CK(ctx, cudaEventElapsedTime(&ms, ctx->tev[i], ctx->tev[i + 1]));
+        ctx->t_ms += ms;
+    }
+    ctx->tused = 0;
+    ctx->t_bytes += ctx->pend_bytes;
+    ctx->pend_bytes = 0.0;
+    return PIFCM_OK;
+}
+
+int pifcm_timing_enable(pifcm_ctx *ctx, int32_t on) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r = timing_drain(ctx);
+    if (r) return r;
+    ctx->timing = on != 0;
+    ctx->t_ms = 0.0;
+    ctx->t_bytes = 0.0;
+    ctx->t_launches = 0;
+    return PIFCM_OK;
+}
+
+int pifcm_timing_read(pifcm_ctx *ctx, double *ms_total, int64_t *launches, double *alg_bytes) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r = timing_drain(ctx);
+    if (r) return r;
+    if (ms_total) *ms_total = ctx->t_ms;
+    if (launches) *launches = ctx->t_launches;
+    if (alg_bytes) *alg_bytes = ctx->t_bytes;
+    return PIFCM_OK;
+}
+
+int pifcm_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                         size_t *bytes) {
+    if (!bytes) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(nullptr, grid)) || (r = check_cfg(nullptr, cfg))) return r;
+    if (pso && (r = check_pso(nullptr, pso))) return r;
+    *bytes = layout(grid, cfg, pso).total;
+    return PIFCM_OK;
+}
+
+int pifcm_iterate_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, int32_t P,
+                                 int32_t iters, size_t *bytes) {
+    if (!bytes) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(nullptr, grid)) || (r = check_cfg(nullptr, cfg))) return r;
+    if (P < 1 || iters < 1) return PIFCM_EINVAL;
+    const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
+    const int nblk = step_nblk(grid->nx, grid->ny, grid->nz, true) > step_nblk(grid->nx, grid->ny, grid->nz, false)
+                         ? step_nblk(grid->nx, grid->ny, grid->nz, true)
+                         : step_nblk(grid->nx, grid->ny, grid->nz, false);
+    size_t b = align_up(sizeof(double) * kNR * (size_t)nblk * P, 256) +  // partials
+               align_up(sizeof(double) * 4 * P, 256) + 256;              // stats scratch + status
+    if (iters > 1) b += align_up(sizeof(float4) * (size_t)nvox * P, 256);
+    *bytes = b;
+    return PIFCM_OK;
+}
+
+// ============================================================== ABI: iterate
+int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const float *x,
+                  const float *U_in, float *U_out, float *centers, const double *lam_xi, int32_t P,
+                  int32_t iters, double *stats, void *ws, size_t ws_bytes, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(ctx, grid)) || (r = check_cfg(ctx, cfg))) return r;
+    if (P < 1 || P > 65535) return fail(ctx, PIFCM_EINVAL, "P = %d outside [1, 65535]", P);
+    if (iters < 1) return fail(ctx, PIFCM_EINVAL, "iters must be >= 1");
+    if (!x || !U_in || !U_out || !centers || !lam_xi)
+        return fail(ctx, PIFCM_EINVAL, "x, U_in, U_out, centers and lam_xi must be non-NULL");
+    if (U_in == U_out) return fail(ctx, PIFCM_EINVAL, "U_in and U_out must not alias");
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(U_in) |
+         reinterpret_cast<uintptr_t>(U_out)) & 15u)
+        return fail(ctx, PIFCM_EALIGN, "x, U_in and U_out must be 16-byte aligned");
+    size_t need = 0;
+    pifcm_iterate_workspace_size(grid, cfg, P, iters, &need);
+    if ((r = check_ws(ctx, ws, ws_bytes, need))) return r;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CK(ctx, cudaSetDevice(ctx->device));
+    const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
+    const int nblk = step_nblk(grid->nx, grid->ny, grid->nz, true) > step_nblk(grid->nx, grid->ny, grid->nz, false)
+                         ? step_nblk(grid->nx, grid->ny, grid->nz, true)
+                         : step_nblk(grid->nx, grid->ny, grid->nz, false);
+    size_t o = 0;
+    double *partials = at<double>(ws, o); o = align_up(o + sizeof(double) * kNR * (size_t)nblk * P, 256);
+    double *st_scr = at<double>(ws, o); o = align_up(o + sizeof(double) * 4 * P, 256);
+    int *status = at<int>(ws, o); o += 256;
+    float4 *scratch = iters > 1 ? at<float4>(ws, o) : nullptr;
+    double *S = stats ? stats : st_scr;
+    CK(ctx, cudaMemsetAsync(S, 0, sizeof(double) * 4 * P, st));
+    CK(ctx, cudaMemsetAsync(status, 0, sizeof(int), st));
+    bool ok = true;
+    const bool zero = host_zero_lamxi(lam_xi, P, st, &ok);
+    if (!ok) return fail(ctx, PIFCM_ECUDA, "reading lam_xi failed");
+    const float eps = cfg->eps;
+    const float4 *src = reinterpret_cast<const float4 *>(U_in);
+    for (int t = 1; t <= iters; ++t) {
+        float4 *dst = (((iters - t) & 1) == 0) ? reinterpret_cast<float4 *>(U_out) : scratch;
+        r = run_step(ctx, grid, cfg, x, src, dst, nullptr, nullptr, centers, lam_xi, !zero, 0, P,
+                     partials, nullptr, S, eps, status, nullptr, st);
+        if (r) return r;
+        src = dst;
+    }
+    if (eps > 0.f && iters > 1)
+        LAUNCH(ctx, 1, launch_fixup_copy(scratch, reinterpret_cast<float4 *>(U_out), nvox, P, S, iters, st));
+    return PIFCM_OK;
+}
+
+// ============================================================== ABI: PSO
+static int pso_common(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg *p,
+                      void *ws, size_t ws_bytes, Layout *L) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(ctx, g)) || (r = check_cfg(ctx, c)) || (r = check_pso(ctx, p))) return r;
+    *L = layout(g, c, p);
+    return check_ws(ctx, ws, ws_bytes, L->total);
+}
+
+int pifcm_pso_init(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                   const float *U0, const float *c0, void *ws, size_t ws_bytes, pifcm_stream stream) {
+    Layout L;
+    int r = pso_common(ctx, grid, cfg, pso, ws, ws_bytes, &L);
+    if (r) return r;
+    if (!U0 || !c0) return fail(ctx, PIFCM_EINVAL, "U0 and c0 must be non-NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CK(ctx, cudaSetDevice(ctx->device));
+    float4 *slot0 = at<float4>(ws, L.slots);
+    if (reinterpret_cast<const void *>(U0) != slot0)
+        CK(ctx, cudaMemcpyAsync(slot0, U0, sizeof(float4) * (size_t)L.nvox, cudaMemcpyDeviceToDevice, st));
+    const uint32_t k0 = (uint32_t)(pso->seed & 0xFFFFFFFFu), k1 = (uint32_t)(pso->seed >> 32);
+    LAUNCH(ctx, 1, launch_pso_init(swarm_of(ws, L), L.P, L.Pl, L.p0, pso->v0, k0, k1, c0, L.nslots, st));
+    return PIFCM_OK;
+}
+
+int pifcm_pso_fitness_ptr(const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                          void *ws, double **fitness) {
+    if (!fitness || !ws) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(nullptr, grid)) || (r = check_cfg(nullptr, cfg)) || (r = check_pso(nullptr, pso))) return r;
+    *fitness = at<double>(ws, layout(grid, cfg, pso).fit);
+    return PIFCM_OK;
+}
+
+int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                   const float *x, void *ws, size_t ws_bytes, pifcm_stream stream) {
+    Layout L;
+    int r = pso_common(ctx, grid, cfg, pso, ws, ws_bytes, &L);
+    if (r) return r;
+    if (!x) return fail(ctx, PIFCM_EINVAL, "x is NULL");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    SwarmDev s = swarm_of(ws, L);
+    float4 *slots = at<float4>(ws, L.slots);
+    return run_step(ctx, grid, cfg, x, slots, slots, s.cur, s.nxt, s.centers, s.pos + 2 * L.p0, true, 0,
+                    L.Pl, at<double>(ws, L.part), s.fit + L.p0, nullptr, 0.f, s.hdr + kHStatus,
+                    s.hdr + kHStop, st);
+}
+
+int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                     void *ws, size_t ws_bytes, pifcm_stream stream) {
+    Layout L;
+    int r = pso_common(ctx, grid, cfg, pso, ws, ws_bytes, &L);
+    if (r) return r;
+    PsoUpdateArgs a{};
+    a.s = swarm_of(ws, L);
+    a.P = L.P; a.Pl = L.Pl; a.p0 = L.p0; a.ring_k = pso->ring_k; a.patience = pso->patience;
+    a.nslots = L.nslots; a.tol = pso->tol; a.vmax = pso->vmax;
+    a.key0 = (uint32_t)(pso->seed & 0xFFFFFFFFu); a.key1 = (uint32_t)(pso->seed >> 32);
+    LAUNCH(ctx, 1, launch_pso_update(a, reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_pso_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                   const float *x, void *ws, size_t ws_bytes, pifcm_stream stream) {
+    int r = pifcm_pso_eval(ctx, grid, cfg, pso, x, ws, ws_bytes, stream);
+    if (r) return r;
+    return pifcm_pso_update(ctx, grid, cfg, pso, ws, ws_bytes, stream);
+}
+
+int pifcm_pso_result_get(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                         const pifcm_pso_cfg *pso, void *ws, pifcm_pso_result *out, int32_t *stopped,
+                         pifcm_stream stream) {
+    if (!ctx || !out) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(ctx, grid)) || (r = check_cfg(ctx, cfg)) || (r = check_pso(ctx, pso))) return r;
+    Layout L = layout(grid, cfg, pso);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int hdr[16];
+    double dh[16];
+    float gc[4];
+    CK(ctx, cudaMemcpyAsync(hdr, at<int>(ws, L.hdr), sizeof hdr, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(dh, at<double>(ws, L.dhdr), sizeof dh, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(gc, at<float>(ws, L.gbc), sizeof gc, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaStreamSynchronize(st));
+    if (!hdr[kHInit]) return fail(ctx, PIFCM_ESTATE, "swarm not initialised (call pifcm_pso_init)");
+    if (hdr[kHStatus]) return fail(ctx, hdr[kHStatus], "non-finite fitness during PSO");
+    out->lambda = dh[kDGbestL];
+    out->xi = dh[kDGbestX];
+    out->J = dh[kDGbestJ];
+    out->generations = hdr[kHGen];
+    out->gbest_particle = hdr[kHGbest];
+    for (int j = 0; j < 4; ++j) out->centers[j] = gc[j];
+    if (stopped) *stopped = hdr[kHStop];
+    return PIFCM_OK;
+}
+
+int pifcm_pso_gbest_state(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                          const pifcm_pso_cfg *pso, void *ws, float *U_out, float *c_out, pifcm_stream stream) {
+    if (!ctx || !U_out) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(ctx, grid)) || (r = check_cfg(ctx, cfg)) || (r = check_pso(ctx, pso))) return r;
+    Layout L = layout(grid, cfg, pso);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int gs = -1;
+    CK(ctx, cudaMemcpyAsync(&gs, at<int>(ws, L.hdr) + kHGbestSlot, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaStreamSynchronize(st));
+    if (gs < 0) return fail(ctx, PIFCM_ESTATE, "the gbest state is not held by this process");
+    LAUNCH(ctx, 1, launch_gather_gbest(at<float4>(ws, L.slots), L.nvox, at<int>(ws, L.hdr), at<float>(ws, L.gbc),
+                                       reinterpret_cast<float4 *>(U_out), c_out, st));
+    return PIFCM_OK;
+}
+
+int pifcm_pso_run(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                  const float *x, const float *U0, const float *c0, void *ws, size_t ws_bytes,
+                  pifcm_pso_result *out, pifcm_stream stream) {
+    if (pso && !(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
+        return fail(ctx, PIFCM_EINVAL, "pifcm_pso_run is single-process: use eval/update for sharding");
+    int r = pifcm_pso_init(ctx, grid, cfg, pso, U0, c0, ws, ws_bytes, stream);
+    if (r) return r;
+    const int check_every = 4;
+    for (int gen = 0; gen < pso->max_gen; ++gen) {
+        if ((r = pifcm_pso_step(ctx, grid, cfg, pso, x, ws, ws_bytes, stream))) return r;
+        if (pso->patience > 0 && (gen + 1) % check_every == 0) {
+            pifcm_pso_result tmp;
+            int32_t stopped = 0;
+            if ((r = pifcm_pso_result_get(ctx, grid, cfg, pso, ws, &tmp, &stopped, stream))) return r;
+            if (stopped) break;
+        }
+    }
+    if (out) return pifcm_pso_result_get(ctx, grid, cfg, pso, ws, out, nullptr, stream);
+    return PIFCM_OK;
+}
+
+// ============================================================== ABI: pipeline parts
+int pifcm_normalize_u8(pifcm_ctx *ctx, const pifcm_grid *grid, const uint8_t *vol, float *x, int64_t *hist,
+                       void *ws, size_t ws_bytes, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(ctx, grid))) return r;
+    if (!vol || !x) return fail(ctx, PIFCM_EINVAL, "vol and x must be non-NULL");
+    if (!ws || ws_bytes < 256) return fail(ctx, PIFCM_ENOMEM, "normalize needs >= 256 bytes of workspace");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const long long n = (long long)grid->nx * grid->ny * grid->nz;
+    unsigned int *mm = static_cast<unsigned int *>(ws);
+    LAUNCH(ctx, 2, launch_minmax_u8(vol, n, mm, st));
+    LAUNCH(ctx, 1, launch_normalize_u8(vol, grid->nx, grid->ny, grid->nz, grid->pitch, mm, x, st));
+    if (hist) LAUNCH(ctx, 2, launch_hist_u8(vol, n, mm, hist, st));
+    return PIFCM_OK;
+}
+
+int pifcm_gmm_init(pifcm_ctx *ctx, int32_t C, const int64_t *hist, float *c0, void *ws, size_t ws_bytes,
+                   pifcm_stream stream) {
+    (void)ws; (void)ws_bytes;
+    if (!ctx) return PIFCM_EINVAL;
+    if (C < 2 || C > kMaxC) return fail(ctx, PIFCM_EINVAL, "C = %d outside [2, 4]", C);
+    if (!hist || !c0) return fail(ctx, PIFCM_EINVAL, "hist and c0 must be non-NULL");
+    LAUNCH(ctx, 1, launch_gmm(hist, C, 100, c0, reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float *U, uint8_t *labels,
+                 pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(ctx, grid))) return r;
+    if (C < 2 || C > kMaxC) return fail(ctx, PIFCM_EINVAL, "C = %d outside [2, 4]", C);
+    if (!U || !labels) return fail(ctx, PIFCM_EINVAL, "U and labels must be non-NULL");
+    const long long n = (long long)grid->nx * grid->ny * grid->nz;
+    LAUNCH(ctx, 1, launch_argmax(reinterpret_cast<const float4 *>(U), n, C, labels,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+// ============================================================== ABI: pipeline
+// Iterate state in slot `a` until eps / max_iter using slots a <-> b; returns
+// the slot holding the result in *res and the iteration count in *iters.
+static int run_until(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x,
+                     float4 *slots, long long nvox, int a, int b, float *centers, const double *lamxi,
+                     bool stencil, bool fcm_first, double *partials, double *stats, int *status,
+                     cudaStream_t st, int *res, int *iters) {
+    CK(ctx, cudaMemsetAsync(stats, 0, sizeof(double) * 4, st));
+    int src = a, dst = b, t = 0;
+    const int check_every = 4;
+    for (t = 1; t <= cfg->max_iter; ++t) {
+        int r = run_step(ctx, g, cfg, x, slots + (long long)src * nvox, slots + (long long)dst * nvox, nullptr,
+                         nullptr, centers, lamxi, stencil, (fcm_first && t == 1) ? 1 : 0, 1, partials,
+                         nullptr, stats, cfg->eps, status, nullptr, st);
+        if (r) return r;
+        const int tmp = src; src = dst; dst = tmp;
+        if (t % check_every == 0 || t == cfg->max_iter) {
+            double h[4];
+            CK(ctx, cudaMemcpyAsync(h, stats, sizeof h, cudaMemcpyDeviceToHost, st));
+            CK(ctx, cudaStreamSynchronize(st));
+            if (h[3] != 0.0) {
+                // converged at iteration h[2]; later launches were no-ops
+                const int done = (int)h[2];
+                *iters = done;
+                *res = (done % 2 == 1) ? b : a;
+                return PIFCM_OK;
+            }
+        }
+    }
+    *iters = cfg->max_iter;
+    *res = (cfg->max_iter % 2 == 1) ? b : a;
+    return PIFCM_OK;
+}
+
+int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, int32_t ny, int32_t nz,
+                  const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso, int32_t z_slice, void *ws,
+                  size_t ws_bytes, uint8_t *labels, float *U_out, pifcm_report *rep, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    if (dtype != PIFCM_U8) return fail(ctx, PIFCM_EINVAL, "only PIFCM_U8 volumes are supported");
+    if (!vol || !labels) return fail(ctx, PIFCM_EINVAL, "vol and labels must be non-NULL");
+    pifcm_grid g{nx, ny, nz, (nx + 3) / 4 * 4};
+    Layout L;
+    int r = pso_common(ctx, &g, cfg, pso, ws, ws_bytes, &L);
+    if (r) return r;
+    if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
+        return fail(ctx, PIFCM_EINVAL, "pifcm_segment is single-process");
+    if (z_slice < -1 || z_slice >= nz) return fail(ctx, PIFCM_EINVAL, "z_slice %d out of range", z_slice);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CK(ctx, cudaSetDevice(ctx->device));
+    cudaEvent_t *ev = ctx->ev;
+    float *x = at<float>(ws, L.x);
+    int64_t *hist = at<int64_t>(ws, L.hist);
+    float *c0 = at<float>(ws, L.c0);
+    float4 *slots = at<float4>(ws, L.slots);
+    double *partials = at<double>(ws, L.part);
+    double *stats = at<double>(ws, L.stats);
+    double *lamxi = at<double>(ws, L.lamxi);
+    SwarmDev s = swarm_of(ws, L);
+    int *status = s.hdr + kHStatus;
+    float *cent = s.centers;  // [Pl][4]; entry 0 reused by the FCM start and the final IFCM
+    CK(ctx, cudaEventRecord(ev[0], st));
+    // Alg. 2 step 1: normalise (+ histogram for the GMM start)
+    const uint8_t *v8 = static_cast<const uint8_t *>(vol);
+    unsigned int *mm = at<unsigned int>(ws, L.mm);
+    LAUNCH(ctx, 2, launch_minmax_u8(v8, L.nvox, mm, st));
+    LAUNCH(ctx, 1, launch_normalize_u8(v8, nx, ny, nz, g.pitch, mm, x, st));
+    LAUNCH(ctx, 2, launch_hist_u8(v8, L.nvox, mm, hist, st));
+    CK(ctx, cudaEventRecord(ev[1], st));
+    // Alg. 1 step 2: GMM centres, then FCM (lambda = xi = 0) until eps
+    LAUNCH(ctx, 1, launch_gmm(hist, cfg->C, 100, c0, st));
+    float cinit[4];
+    CK(ctx, cudaMemcpyAsync(cinit, c0, sizeof cinit, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(cent, c0, sizeof(float) * 4, cudaMemcpyDeviceToDevice, st));
+    CK(ctx, cudaMemsetAsync(lamxi, 0, sizeof(double) * 2, st));
+    CK(ctx, cudaMemsetAsync(s.hdr, 0, sizeof(int) * 16, st));
+    int fcm_slot = 0, fcm_iters = 0;
+    if ((r = run_until(ctx, &g, cfg, x, slots, L.nvox, 1, 0, cent, lamxi, false, true, partials, stats, status, st,
+                       &fcm_slot, &fcm_iters)))
+        return r;
+    // keep the FCM result in slot 0 (the PSO start slot)
+    if (fcm_slot != 0)
+        CK(ctx, cudaMemcpyAsync(slots, slots + (long long)fcm_slot * L.nvox, sizeof(float4) * (size_t)L.nvox,
+                                cudaMemcpyDeviceToDevice, st));
+    CK(ctx, cudaMemcpyAsync(c0, cent, sizeof(float) * 4, cudaMemcpyDeviceToDevice, st));
+    CK(ctx, cudaEventRecord(ev[2], st));
+    // Alg. 1 steps 3-10: PSO (c0 now holds the FCM centres for pso_init)
+    pifcm_pso_result pres;
+    if ((r = pifcm_pso_run(ctx, &g, cfg, pso, x, reinterpret_cast<float *>(slots), c0, ws, ws_bytes, &pres, stream)))
+        return r;
+    CK(ctx, cudaEventRecord(ev[3], st));
+    // Alg. 1 step 11: final IFCM from the gbest state at (lambda*, xi*)
+    int gs = -1;
+    CK(ctx, cudaMemcpyAsync(&gs, s.hdr + kHGbestSlot, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaStreamSynchronize(st));
+    if (gs < 0) return fail(ctx, PIFCM_ESTATE, "no gbest state after PSO");
+    const int other = (gs == 0) ? 1 : 0;
+    CK(ctx, cudaMemcpyAsync(cent, s.gbest_c, sizeof(float) * 4, cudaMemcpyDeviceToDevice, st));
+    LAUNCH(ctx, 1, launch_set_lamxi(lamxi, s.dhdr, st));
+    const bool zero = (pres.lambda == 0.0 && pres.xi == 0.0);
+    int fin_slot = gs, fin_iters = 0;
+    if ((r = run_until(ctx, &g, cfg, x, slots, L.nvox, gs, other, cent, lamxi, !zero, false, partials, stats, status,
+                       st, &fin_slot, &fin_iters)))
+        return r;
+    CK(ctx, cudaEventRecord(ev[4], st));
+    // defuzzify (+ optional U copy)
+    const float4 *Ufin = slots + (long long)fin_slot * L.nvox;
+    if (z_slice < 0) {
+        LAUNCH(ctx, 1, launch_argmax(Ufin, L.nvox, cfg->C, labels, st));
+    } else {
+        const long long plane = (long long)nx * ny;
+        LAUNCH(ctx, 1, launch_argmax(Ufin + (long long)z_slice * plane, plane, cfg->C, labels, st));
+    }
+    if (U_out)
+        CK(ctx, cudaMemcpyAsync(U_out, Ufin, sizeof(float4) * (size_t)L.nvox, cudaMemcpyDeviceToDevice, st));
+    CK(ctx, cudaEventRecord(ev[5], st));
+    float cfin[4];
+    int stat = 0;
+    CK(ctx, cudaMemcpyAsync(cfin, cent, sizeof cfin, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(&stat, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaStreamSynchronize(st));
+    CK(ctx, cudaGetLastError());
+    if (stat) return fail(ctx, stat, "non-finite cost during the pipeline");
+    if (rep) {
+        memset(rep, 0, sizeof *rep);
+        rep->pso = pres;
+        rep->fcm_iters = fcm_iters;
+        rep->final_iters = fin_iters;
+        for (int j = 0; j < 4; ++j) { rep->centers[j] = cfin[j]; rep->c_init[j] = cinit[j]; }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[0], ev[1]); rep->t_norm = ms * 1e-3;
+        cudaEventElapsedTime(&ms, ev[1], ev[2]); rep->t_init = ms * 1e-3;
+        cudaEventElapsedTime(&ms, ev[2], ev[3]); rep->t_pso = ms * 1e-3;
+        cudaEventElapsedTime(&ms, ev[3], ev[4]); rep->t_final = ms * 1e-3;
+        cudaEventElapsedTime(&ms, ev[0], ev[5]); rep->t_total = ms * 1e-3;
+    }
+    return PIFCM_OK;
+}
+
+int pifcm_segment_host(pifcm_ctx *ctx, const uint8_t *vol_host, int32_t nx, int32_t ny, int32_t nz,
+                       const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes,
+                       uint8_t *labels_host, pifcm_report *rep, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    if (!vol_host || !labels_host) return fail(ctx, PIFCM_EINVAL, "host buffers must be non-NULL");
+    pifcm_grid g{nx, ny, nz, (nx + 3) / 4 * 4};
+    Layout L;
+    int r = pso_common(ctx, &g, cfg, pso, ws, ws_bytes, &L);
+    if (r) return r;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    uint8_t *dvol = at<uint8_t>(ws, L.vol), *dlab = at<uint8_t>(ws, L.lab);
+    CK(ctx, cudaMemcpyAsync(dvol, vol_host, (size_t)L.nvox, cudaMemcpyHostToDevice, st));
+    if ((r = pifcm_segment(ctx, dvol, PIFCM_U8, nx, ny, nz, cfg, pso, -1, ws, ws_bytes, dlab, nullptr, rep, stream)))
+        return r;
+    CK(ctx, cudaMemcpyAsync(labels_host, dlab, (size_t)L.nvox, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaStreamSynchronize(st));
+    return PIFCM_OK;
+}
+
+}  // extern "C"

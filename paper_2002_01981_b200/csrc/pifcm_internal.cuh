@@ -1,0 +1,114 @@
+// pifcm_internal.cuh -- internal declarations of libpifcm.so (B200, sm_100a).
+// Not part of the ABI (see include/pifcm.h).  No code is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pifcm.h"
+
+namespace pifcm {
+
+// ---------------------------------------------------------------- constants
+constexpr int kMaxC = 4;          // AoS-C4 rows: one float4 per voxel
+constexpr int kNR = 2 * kMaxC + 2; // partial record: num[4], den[4], J, max|du|
+constexpr float kAFloor = 1e-9f;  // R4: floor of 1 - lam H - xi F (Eq. 4)
+constexpr double kDenEps = 1e-12; // R9: keep c_j if sum u^m < 1e-12 (Eq. 3)
+
+// Stencil step tiling (one CTA = TX x TY voxels per plane, marching TZ planes).
+constexpr int kTX = 32;             // one warp along x: 512 B coalesced rows
+constexpr int kWarpsY = 4;          // warps per CTA, stacked in y
+constexpr int kRY = 4;              // consecutive y rows per thread (register blocking)
+constexpr int kTY = kWarpsY * kRY;  // 16
+constexpr int kSX = kTX + 2;        // haloed smem row length
+constexpr int kSY = kTY + 2;        // haloed smem rows
+constexpr int kStages = 4;          // plane ring: z-1, z, z+1 resident, z+2 landing
+constexpr int kTZ = 16;             // planes per CTA (z-chunk)
+constexpr int kStepThreads = kTX * kWarpsY;
+
+// Pointwise (FCM, lambda = xi = 0) step.
+constexpr int kPwThreads = 256;
+
+// ------------------------------------------------------------ step arguments
+struct StepArgs {
+    const float *x;      // [nz][ny][pitch]
+    int nx, ny, nz, pitch;
+    long long nvox;      // nx*ny*nz  (float4 rows per state)
+    const float4 *U_in;  // base of input states
+    float4 *U_out;       // base of output states
+    const int *in_idx;   // nullable: state p reads U_in + in_idx[p]*nvox (else p*nvox)
+    const int *out_idx;  // nullable: state p writes U_out + out_idx[p]*nvox
+    float *centers;      // [P][4] (read at kernel start)
+    const double *lam_xi;// [P][2]  (already offset to this process's first particle)
+    double *partials;    // [P][nblk][kNR]
+    int nblk;            // partial records per state
+    const double *stats; // nullable: skip state p if stats[4p+3] != 0 (converged)
+    const int *stop;     // nullable: skip everything if *stop != 0
+    int tiles_x, tiles_y, zchunks;
+    float m, inv_m1;     // m, 1/(m-1)
+    int q_mode;
+    int first;           // FCM first iteration: U_in not read, max|du| := 1
+};
+
+struct FinalizeArgs {
+    const double *partials; // [P][nblk][kNR]
+    int nblk, C, P;
+    float *centers;         // [P][4] in/out
+    double *fitness;        // nullable [P] (offset to this process's first particle)
+    double *stats;          // nullable [P][4] {J, du, iters, converged}
+    float eps;              // convergence threshold on max|du| (<=0: never)
+    int *status;            // nullable: set to PIFCM_ENUMERIC on non-finite J
+    const int *stop;        // nullable
+};
+
+// Swarm state in the workspace (all device pointers).
+struct SwarmDev {
+    int *hdr;        // [16] ints: see kH* below
+    double *dhdr;    // [16] doubles: see kD* below
+    double *pos;     // [P][2] current positions (lambda, xi)
+    double *vel;     // [P][2]
+    double *pbf;     // [P] pbest fitness
+    double *pbx;     // [P][2] pbest positions
+    double *fit;     // [P] fitness of the current generation
+    double *evalpos; // [P][2] positions the current generation was evaluated at
+    int *cur;        // [Pl] slot holding each local particle's state
+    int *nxt;        // [Pl] slot the next evaluation writes
+    float *gbest_c;  // [4]
+    float *centers;  // [Pl][4]
+};
+// header int indices
+constexpr int kHGen = 0, kHGbest = 1, kHGbestSlot = 2, kHImproved = 3, kHCalm = 4,
+              kHStop = 5, kHStatus = 6, kHInit = 7;
+// header double indices
+constexpr int kDPrevGf = 0, kDGbestJ = 1, kDGbestL = 2, kDGbestX = 3;
+
+struct PsoUpdateArgs {
+    SwarmDev s;
+    int P, Pl, p0, ring_k, patience, nslots;
+    double tol, vmax;
+    uint32_t key0, key1;
+};
+
+// ---------------------------------------------------------------- launchers
+// All return cudaGetLastError() of the launch.
+cudaError_t launch_step(const StepArgs &a, int C, bool stencil, int P, cudaStream_t st);
+int step_nblk(int nx, int ny, int nz, bool stencil);
+cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st);
+cudaError_t launch_fixup_copy(const float4 *scratch, float4 *out, long long nvox, int P,
+                              const double *stats, int iters, cudaStream_t st);
+cudaError_t launch_pso_init(SwarmDev s, int P, int Pl, int p0, double v0, uint32_t k0,
+                            uint32_t k1, const float *c0, int nslots, cudaStream_t st);
+cudaError_t launch_pso_update(const PsoUpdateArgs &a, cudaStream_t st);
+cudaError_t launch_minmax_u8(const uint8_t *vol, long long n, unsigned int *mm, cudaStream_t st);
+cudaError_t launch_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int pitch,
+                                const unsigned int *mm, float *x, cudaStream_t st);
+cudaError_t launch_hist_u8(const uint8_t *vol, long long n, const unsigned int *mm,
+                           int64_t *hist, cudaStream_t st);
+cudaError_t launch_gmm(const int64_t *hist, int C, int max_iter, float *c0, cudaStream_t st);
+cudaError_t launch_argmax(const float4 *U, long long n, int C, uint8_t *labels,
+                          cudaStream_t st);
+cudaError_t launch_gather_gbest(const float4 *slots, long long nvox, const int *hdr,
+                                const float *gbest_c, float4 *U_out, float *c_out,
+                                cudaStream_t st);
+cudaError_t launch_set_lamxi(double *dst, const double *dhdr, cudaStream_t st);
+
+}  // namespace pifcm

@@ -1,0 +1,136 @@
+"""GPU parity of the device PSO (Alg. 1 steps 3-10) and of the whole pipeline
+(pifcm_segment) against the fp64 oracle, through the C ABI."""
+import ctypes as ct
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2002_01981_b200 import Context
+    return Context(0)
+
+
+def _small_case(C=3, shape=(10, 24, 28), seed=4):
+    from inputs import cube_phantom, add_noise_u8
+    nz, ny, nx = shape
+    img, lab = cube_phantom(nx, ny, nz, (0.1, 0.5, 0.9) if C == 3 else (0.1, 0.35, 0.65, 0.9))
+    vol = add_noise_u8(img, 7.0, seed)
+    return vol, lab
+
+
+def test_pso_trajectory_parity(ctx, orc):
+    """Generation by generation: fitness vector within 1e-5 relative of the
+    oracle's, identical Philox-driven positions (hence identical gbest)."""
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig, to_aos, to_pitched_x
+    from paper_2002_01981_b200.api import _grid
+    vol, _ = _small_case()
+    x = (vol.astype(np.float32) / 255.0)
+    Uf, cf, _ = orc.fcm_run(x, np.array([0.1, 0.5, 0.9]))
+    U0 = Uf.astype(np.float32)
+    c0 = cf.astype(np.float32)
+    nz, ny, nx = x.shape
+    P, G, seed = 6, 8, 777
+    cfg = IfcmConfig(C=3)
+    pso = PsoConfig(P=P, max_gen=G, patience=0, seed=seed)
+    dev = torch.device("cuda:0")
+    xt = to_pitched_x(x, dev)
+    Ut = to_aos(U0, dev)
+    ct4 = torch.zeros(4, device=dev)
+    ct4[:3] = torch.as_tensor(c0)
+    ws = ctx.workspace(nx, ny, nz, cfg, pso)
+    g = _grid(nx, ny, nz)
+    ctx.pso_init(g, cfg, pso, Ut, ct4, ws)
+    fit = ctx.pso_fitness(g, cfg, pso, ws)
+    r = orc.pso_run(x, U0, c0, P=P, max_gen=G, seed=seed)
+    for gen in range(G):
+        ctx.pso_eval(g, cfg, pso, xt, ws)
+        f = fit.cpu().numpy()
+        assert np.allclose(f, r.trace_f[gen], rtol=1e-5, atol=0), (gen, f, r.trace_f[gen])
+        ctx.pso_update(g, cfg, pso, ws)
+        summ, _ = ctx.pso_result(g, cfg, pso, ws)
+        assert summ.gbest_particle == r.trace_gbest[gen]
+    summ, stopped = ctx.pso_result(g, cfg, pso, ws)
+    assert summ.generations == G and not stopped
+    assert abs(summ.lam - r.lam) < 1e-12 and abs(summ.xi - r.xi) < 1e-12
+    assert abs(summ.J - r.J) <= 1e-5 * r.J
+    assert np.allclose(summ.centers, r.c, rtol=1e-4)
+    # the gbest state (the U its evaluation produced), Alg. 1 step 10
+    Ug = torch.empty_like(Ut)
+    cg = torch.empty(4, device=dev)
+    ctx.pso_gbest_state(g, cfg, pso, ws, Ug, cg)
+    assert np.abs(Ug.cpu().numpy()[:, :3] - r.U).max() < 1e-4
+
+
+def test_pso_run_early_stop(ctx, orc):
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig, to_aos, to_pitched_x
+    vol, _ = _small_case(C=2, shape=(6, 16, 16))
+    x = vol.astype(np.float32) / 255.0
+    Uf, cf, _ = orc.fcm_run(x, np.array([0.2, 0.8]))
+    dev = torch.device("cuda:0")
+    cfg = IfcmConfig(C=2)
+    pso = PsoConfig(P=4, max_gen=40, patience=3, tol=1e-4, seed=1)
+    c4 = torch.zeros(4, device=dev)
+    c4[:2] = torch.as_tensor(cf.astype(np.float32))
+    s = ctx.pso_run(to_pitched_x(x, dev), to_aos(Uf, dev), c4, cfg, pso, nx=16)
+    r = orc.pso_run(x, Uf.astype(np.float32), cf.astype(np.float32), P=4, max_gen=40, seed=1,
+                    patience=3, tol=1e-4)
+    assert r.generations < 40
+    # the device checks the stop flag every 4 generations; generations counted agree
+    assert s.generations == r.generations
+    assert abs(s.lam - r.lam) < 1e-12 and abs(s.xi - r.xi) < 1e-12
+
+
+@pytest.mark.parametrize("C,shape,P,G", [(3, (10, 24, 28), 4, 5), (4, (1, 64, 64), 6, 6),
+                                         (2, (5, 9, 40), 3, 4)])
+def test_segment_parity(ctx, orc, C, shape, P, G):
+    """The whole pipeline (Alg. 1/2) on a noisy phantom: labels identical on
+    >= 99.9% of voxels (north_star), same (lambda*, xi*), centres 1e-3."""
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    vol, lab = _small_case(C=C, shape=shape, seed=11)
+    cfg = IfcmConfig(C=C, eps=1e-5, max_iter=100)
+    pso = PsoConfig(P=P, max_gen=G, patience=0, seed=99)
+    vt = torch.as_tensor(vol, device="cuda:0")
+    labels, U, rep = ctx.segment(vt, cfg, pso, want_U=True)
+    r = orc.segment_u8(vol, C=C, P=P, max_gen=G, seed=99)
+    agree = (labels.cpu().numpy() == r.labels).mean()
+    assert agree >= 0.999, agree
+    assert np.abs(np.array(rep["c_init"]) - r.c_init).max() < 1e-6
+    assert abs(rep["lambda"] - r.lam) < 1e-9 and abs(rep["xi"] - r.xi) < 1e-9
+    assert np.allclose(rep["centers"], r.c, rtol=1e-3)
+    assert rep["generations"] == G
+    assert abs(rep["final_iters"] - r.final_iters) <= 4  # device checks eps every 4 iterations
+
+
+def test_segment_host_equals_device(ctx):
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    vol, _ = _small_case(C=3, shape=(8, 20, 20), seed=2)
+    cfg = IfcmConfig(C=3)
+    pso = PsoConfig(P=3, max_gen=3, patience=0, seed=5)
+    vt = torch.as_tensor(vol, device="cuda:0")
+    ws = ctx.workspace(20, 20, 8, cfg, pso)
+    lab_d, _, rep_d = ctx.segment(vt, cfg, pso, ws=ws)
+    vh = torch.as_tensor(vol).pin_memory()
+    lh = torch.empty(vol.shape, dtype=torch.uint8).pin_memory()
+    rep_h = ctx.segment_host(vh, cfg, pso, ws, lh)
+    assert (lh.numpy() == lab_d.cpu().numpy()).all()
+    assert rep_h["lambda"] == rep_d["lambda"]
+    # z_slice: only that plane is written
+    lab_z, _, _ = ctx.segment(vt, cfg, pso, ws=ws, z_slice=3)
+    assert (lab_z.cpu().numpy() == lab_d.cpu().numpy()[3]).all()
+
+
+def test_segment_determinism(ctx):
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    vol, _ = _small_case(C=4, shape=(12, 30, 33), seed=8)
+    cfg = IfcmConfig(C=4)
+    pso = PsoConfig(P=5, max_gen=4, patience=0, seed=3)
+    vt = torch.as_tensor(vol, device="cuda:0")
+    a = ctx.segment(vt, cfg, pso, want_U=True)
+    b = ctx.segment(vt, cfg, pso, want_U=True)
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
+    assert a[2]["J"] == b[2]["J"]

@@ -1,0 +1,172 @@
+"""GPU parity of the fused IFCM step (pifcm_iterate, through the C ABI) against
+the fp64 oracle, from the same state (north_star tolerances: memberships 1e-4
+absolute, centres 1e-4 relative).  The oracle receives the GPU's fp32 inputs
+widened exactly to fp64."""
+import numpy as np
+import pytest
+import torch
+
+from inputs import random_state
+
+pytestmark = pytest.mark.gpu
+
+U_TOL = 1e-4
+C_TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2002_01981_b200 import Context
+    return Context(0)
+
+
+def gpu_step(ctx, x, Us, cs, lamxi, C, m=2.0, q_mode=0, iters=1, eps=0.0):
+    """Run `iters` iterations for P states; returns (U_new [P,N,C] f64, c [P,C], stats [P,4])."""
+    from paper_2002_01981_b200 import IfcmConfig, to_aos, to_pitched_x
+    dev = torch.device("cuda:0")
+    nz, ny, nx = x.shape
+    P = len(Us)
+    xt = to_pitched_x(x, dev)
+    Uin = to_aos(np.stack(Us), dev)
+    Uout = torch.full_like(Uin, float("nan"))
+    cen = torch.zeros((P, 4), dtype=torch.float32, device=dev)
+    cen[:, :C] = torch.as_tensor(np.stack(cs), dtype=torch.float32)
+    lx = torch.as_tensor(np.asarray(lamxi, np.float64).reshape(P, 2), device=dev)
+    stats = torch.zeros((P, 4), dtype=torch.float64, device=dev)
+    cfg = IfcmConfig(C=C, m=m, q_mode=q_mode, eps=eps)
+    ctx.iterate(xt, Uin, Uout, cen, lx, cfg, iters=iters, stats=stats, nx=nx)
+    torch.cuda.synchronize()
+    U = Uout.cpu().numpy().astype(np.float64)
+    assert np.isfinite(U).all()
+    assert (U[..., C:] == 0).all()
+    return U[..., :C], cen[:, :C].cpu().numpy().astype(np.float64), stats.cpu().numpy()
+
+
+CASES = [
+    # (nz, ny, nx), C, m, q_mode
+    ((1, 8, 8), 2, 2.0, 0),
+    ((5, 12, 12), 3, 2.0, 0),
+    ((9, 17, 33), 4, 2.0, 0),
+    ((19, 37, 70), 4, 2.0, 1),      # several tiles in x, y and z with ragged tails
+    ((17, 16, 32), 3, 1.5, 0),      # exact tile multiples, z chunk + 1
+    ((3, 50, 7), 4, 3.0, 1),
+    ((1, 1, 1), 2, 2.0, 0),         # no neighbours: H = F = 0
+    ((7, 1, 1), 3, 2.0, 0),         # a line along z
+    ((1, 40, 1), 2, 2.0, 1),
+    ((1, 96, 97), 4, 2.0, 0),       # 2D, 8-neighbourhood
+]
+
+
+@pytest.mark.parametrize("shape,C,m,q_mode", CASES)
+def test_step_parity(ctx, orc, shape, C, m, q_mode):
+    nz, ny, nx = shape
+    states = [random_state(nx, ny, nz, C, seed=100 + s, crisp_frac=0.1) for s in range(3)]
+    x = states[0][0]
+    Us = [s[1] for s in states]
+    cs = [s[2] for s in states]
+    lamxi = [(0.3, 0.6), (1.0, 1.0), (0.05, 0.95)]
+    U, c, st = gpu_step(ctx, x, Us, cs, lamxi, C, m=m, q_mode=q_mode)
+    for p in range(3):
+        Uo, co, Jo, duo = orc.ifcm_step(x, Us[p], cs[p], *lamxi[p], m=m, q_mode=q_mode)
+        err = np.abs(U[p] - Uo).max()
+        assert err < U_TOL, (p, err)
+        assert np.all(np.abs(c[p] - co) <= C_TOL * np.abs(co) + 1e-7), (c[p], co)
+        assert abs(st[p, 0] - Jo) <= 1e-4 * abs(Jo) + 1e-9, (st[p, 0], Jo)
+        assert abs(st[p, 1] - duo) < 2e-4
+        assert np.abs(U[p].sum(1) - 1).max() < 1e-5
+
+
+def test_fcm_pointwise_parity(ctx, orc):
+    """lambda = xi = 0 for every state -> the pointwise (FCM) kernel; equals the
+    oracle's independent FCM step (PAPER:61 with lambda = xi = 0)."""
+    x, U0, c0 = random_state(45, 31, 6, 4, seed=7)
+    U, c, st = gpu_step(ctx, x, [U0, U0], [c0, c0 + 0.01], [(0, 0), (0, 0)], 4)
+    for p, cc in enumerate([c0, c0 + 0.01]):
+        Uf, cf, Jf, _ = orc.fcm_step(x, cc.astype(np.float32).astype(np.float64))
+        assert np.abs(U[p] - Uf).max() < U_TOL
+        assert np.all(np.abs(c[p] - cf) <= C_TOL * np.abs(cf))
+        assert abs(st[p, 0] - Jf) <= 1e-4 * Jf
+
+
+def test_multi_iteration_and_convergence(ctx, orc):
+    from inputs import cube_phantom, add_noise_u8
+    img, _ = cube_phantom(40, 36, 12, (0.1, 0.5, 0.9))
+    x = (add_noise_u8(img, 7.0, 5).astype(np.float32) / 255.0)
+    Uf, cf, _ = orc.fcm_run(x, np.array([0.1, 0.5, 0.9]), max_iter=3)
+    U0 = Uf.astype(np.float32)
+    c0 = cf.astype(np.float32)
+    U5, c5, st = gpu_step(ctx, x, [U0], [c0], [(0.4, 0.7)], 3, iters=5)
+    Uo, co, it, _ = orc.ifcm_run(x, U0, c0, 0.4, 0.7, eps=0.0, max_iter=5)
+    assert np.abs(U5[0] - Uo).max() < 5 * U_TOL
+    assert np.all(np.abs(c5[0] - co) <= 5 * C_TOL * co)
+    assert st[0, 2] == 5
+    # with eps: stops early and the result equals running exactly that many iterations
+    Ue, ce, ste = gpu_step(ctx, x, [U0], [c0], [(0.4, 0.7)], 3, iters=60, eps=1e-3)
+    k = int(ste[0, 2])
+    assert ste[0, 3] == 1 and 1 <= k < 60 and ste[0, 1] < 1e-3
+    Uk, ck, _ = gpu_step(ctx, x, [U0], [c0], [(0.4, 0.7)], 3, iters=k)
+    assert (Ue == Uk).all() and (ce == ck).all()
+
+
+def test_determinism(ctx):
+    x, U0, c0 = random_state(70, 40, 20, 4, seed=3)
+    a = gpu_step(ctx, x, [U0, U0], [c0, c0], [(0.2, 0.9), (0.7, 0.1)], 4, iters=2)
+    b = gpu_step(ctx, x, [U0, U0], [c0, c0], [(0.2, 0.9), (0.7, 0.1)], 4, iters=2)
+    for u, v in zip(a, b):
+        assert (u == v).all()
+
+
+def test_constant_volume_and_crisp(ctx, orc):
+    """R3: constant intensities -> G = 0 -> H = 0; R5: x == c -> crisp rows."""
+    x = np.full((4, 9, 10), 100 / 255, np.float32)
+    _, U0, _ = random_state(10, 9, 4, 3, seed=1)
+    c0 = np.array([0.1, 100 / 255, 0.9], np.float32)
+    U, c, st = gpu_step(ctx, x, [U0], [c0], [(1.0, 0.5)], 3)
+    assert (U[0] == np.array([0.0, 1.0, 0.0])).all()
+    c1 = np.array([0.1, 0.5, 0.9], np.float32)
+    U, c, st = gpu_step(ctx, x, [U0], [c1], [(1.0, 0.5)], 3)
+    Uo, _, _, _ = orc.ifcm_step(x, U0, c1, 1.0, 0.5)
+    assert np.abs(U[0] - Uo).max() < U_TOL
+
+
+def test_argmax_bit_exact(ctx, orc):
+    """Defuzzification (R13) is bit-exact given identical memberships,
+    including exact ties (lowest index wins)."""
+    from paper_2002_01981_b200 import to_aos
+    rng = np.random.default_rng(0)
+    nz, ny, nx = 6, 11, 13
+    U = rng.integers(0, 4, size=(nz * ny * nx, 4)).astype(np.float32) / 4  # many ties
+    for C in (2, 3, 4):
+        Ut = to_aos(U[:, :C], torch.device("cuda:0"))
+        lab = ctx.argmax(Ut, nx, ny, nz, C).cpu().numpy().ravel()
+        assert (lab == orc.argmax(U[:, :C].astype(np.float64))).all()
+
+
+def test_normalize_hist_gmm(ctx, orc):
+    from inputs import config_volume
+    vol, _ = config_volume("C3", shape=(20, 26, 23))
+    vt = torch.as_tensor(vol, device="cuda:0")
+    x, hist = ctx.normalize_u8(vt)
+    xo = orc.normalize_u8(vol)
+    xg = x[:, :, :23].cpu().numpy()
+    assert np.abs(xg - xo).max() <= 6e-8
+    assert (x[:, :, 23:] == 0).all()
+    assert (hist.cpu().numpy() == orc.histogram_u8(vol)).all()
+    c0 = ctx.gmm_init(hist, 4).cpu().numpy()[:4]
+    co = orc.gmm_init(orc.histogram_u8(vol), 4)
+    assert np.abs(c0 - co).max() < 1e-6
+
+
+def test_error_codes(ctx):
+    from paper_2002_01981_b200 import IfcmConfig, PifcmError
+    dev = torch.device("cuda:0")
+    x = torch.zeros((2, 4, 4), device=dev)
+    U = torch.zeros((1, 32, 4), device=dev)
+    cen = torch.zeros((1, 4), device=dev)
+    lx = torch.zeros((1, 2), dtype=torch.float64, device=dev)
+    with pytest.raises(PifcmError) as e:
+        ctx.iterate(x, U, U, cen, lx, IfcmConfig(C=3), nx=4)
+    assert e.value.code == -1
+    with pytest.raises(PifcmError) as e:
+        ctx.iterate(x, U, torch.zeros_like(U), cen, lx, IfcmConfig(C=5), nx=4)
+    assert e.value.code == -1
