@@ -124,8 +124,8 @@ __global__ void k_pso_init(SwarmDev s, int P, int Pl, int p0, double v0, uint32_
         s.pos[2 * p] = a;
         s.pos[2 * p + 1] = b;
         draw2(0xFFFFFFFFu, (uint32_t)p, 2u, k0, k1, a, b);
-        s.vel[2 * p] = (2.0 * a - 1.0) * v0;
-        s.vel[2 * p + 1] = (2.0 * b - 1.0) * v0;
+        s.vel[2 * p] = __dmul_rn(__dsub_rn(__dmul_rn(2.0, a), 1.0), v0);
+        s.vel[2 * p + 1] = __dmul_rn(__dsub_rn(__dmul_rn(2.0, b), 1.0), v0);
         s.pbf[p] = INFINITY;
         s.pbx[2 * p] = s.pos[2 * p];
         s.pbx[2 * p + 1] = s.pos[2 * p + 1];
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs 
         // step 9 stop rule on the relative decrease of the gbest fitness
         const double gf = s.pbf[g];
         if (t > 0 && a.patience > 0) {
-            const double rel = (s.dhdr[kDPrevGf] - gf) / (gf > 0.0 ? gf : 1.0);
+            const double rel = __ddiv_rn(__dsub_rn(s.dhdr[kDPrevGf], gf), (gf > 0.0 ? gf : 1.0));
             s.hdr[kHCalm] = (rel < a.tol) ? s.hdr[kHCalm] + 1 : 0;
             if (s.hdr[kHCalm] >= a.patience) s.hdr[kHStop] = 1;
         }
@@ -251,11 +251,15 @@ __global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs 
         const int lb = lb_sh[p];
 #pragma unroll
         for (int d = 0; d < 2; ++d) {
-            double v = s.vel[2 * p + d] + p1 * (s.pbx[2 * p + d] - s.pos[2 * p + d]) +
-                       p2 * (s.pbx[2 * lb + d] - s.pos[2 * p + d]);
+            // explicit roundings (no FMA contraction): the same fp64 operations,
+            // in the same order, as the written formula
+            const double x = s.pos[2 * p + d];
+            const double t1 = __dmul_rn(p1, __dsub_rn(s.pbx[2 * p + d], x));
+            const double t2 = __dmul_rn(p2, __dsub_rn(s.pbx[2 * lb + d], x));
+            double v = __dadd_rn(__dadd_rn(s.vel[2 * p + d], t1), t2);
             v = fmin(fmax(v, -a.vmax), a.vmax);
             s.vel[2 * p + d] = v;
-            s.pos[2 * p + d] = fmin(fmax(s.pos[2 * p + d] + v, 0.0), 1.0);
+            s.pos[2 * p + d] = fmin(fmax(__dadd_rn(x, v), 0.0), 1.0);
         }
     }
 }

@@ -13,6 +13,10 @@ constexpr int kMaxC = 4;          // AoS-C4 rows: one float4 per voxel
 constexpr int kNR = 2 * kMaxC + 2; // partial record: num[4], den[4], J, max|du|
 constexpr float kAFloor = 1e-9f;  // R4: floor of 1 - lam H - xi F (Eq. 4)
 constexpr double kDenEps = 1e-12; // R9: keep c_j if sum u^m < 1e-12 (Eq. 3)
+// Ill-conditioned band of the Eq. 4 factor: fp32 a in (-kBandLo, kBandHi) is
+// re-evaluated in fp64 (u is proportional to a there).
+constexpr float kBandLo = 1e-4f;
+constexpr float kBandHi = 1e-2f;
 
 // Stencil step tiling (one CTA = TX x TY voxels per plane, marching TZ planes).
 constexpr int kTX = 32;             // one warp along x: 512 B coalesced rows

@@ -51,17 +51,14 @@ __device__ __forceinline__ void cp_async_wait() {
 // the given H, F; Eq. 2; accumulation of the Eq. 3 / Eq. 1 partial sums.
 template <int C, bool M2>
 __device__ __forceinline__ float4 membership(float xv, const float (&c)[kMaxC],
-                                             const float (&H)[kMaxC], const float (&F)[kMaxC],
-                                             float lam, float xi, float m, float inv_m1,
+                                             const float (&a)[kMaxC], float m, float inv_m1,
                                              float (&num)[kMaxC], float (&den)[kMaxC],
                                              float &Jacc) {
     float d2[C];
 #pragma unroll
     for (int j = 0; j < C; ++j) {
-        float a = fmaf(-lam, H[j], fmaf(-xi, F[j], 1.0f));  // Eq. 4 factor
-        a = fmaxf(a, kAFloor);                              // R4
         const float d = xv - c[j];
-        d2[j] = d * d * a;                                  // Eq. 4
+        d2[j] = d * d * a[j];                               // Eq. 4 (a already floored, R4)
     }
     float u[kMaxC] = {0.f, 0.f, 0.f, 0.f};
     int jz = C;
@@ -94,6 +91,47 @@ __device__ __forceinline__ float4 membership(float xv, const float (&c)[kMaxC],
     }
     Jacc += Ji;
     return make_float4(u[0], u[1], u[2], u[3]);
+}
+
+// Attraction factor a_j = 1 - lam H_ij - xi F_ij (Eq. 4) re-evaluated in fp64
+// directly from the definitions (Eq. 5-8: G = sum of in-bounds g, literal
+// per-neighbour q2 weights) for a voxel whose fp32 factor fell in the
+// ill-conditioned band near 0.  There d2_ij (and so u_ij) is proportional to
+// a_j, so fp32 rounding of H and F (~1e-7 absolute) would be amplified by
+// 1/a_j; fp64 keeps the step within the parity tolerance.
+__device__ __noinline__ void attraction_fp64(const float4 *__restrict__ sU0, const float *__restrict__ sX0,
+                                             int stage_stride, int sm, int sc, int sp, int row, int col,
+                                             float xr, int gx, int gy, int z, int nx, int ny, int nz,
+                                             double lam, double xi, float w2, float w3, int C, float *a_out) {
+    double G = 0.0, Qs = 0.0, Hn[kMaxC] = {0.0, 0.0, 0.0, 0.0}, Fn[kMaxC] = {0.0, 0.0, 0.0, 0.0};
+    for (int dz = -1; dz <= 1; ++dz) {
+        const int s = dz < 0 ? sm : (dz == 0 ? sc : sp);
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                if (dx == 0 && dy == 0 && dz == 0) continue;
+                if (gx + dx < 0 || gx + dx >= nx || gy + dy < 0 || gy + dy >= ny || z + dz < 0 ||
+                    z + dz >= nz)
+                    continue;
+                const int e = s * stage_stride + (row + dy) * kSX + (col + dx);
+                const float4 u = sU0[e];
+                const double g = fabs((double)xr - (double)sX0[e]);
+                const int n = (dx != 0) + (dy != 0) + (dz != 0);
+                const double q2 = n == 1 ? 1.0 : (n == 2 ? (double)w2 : (double)w3);
+                const double uk[4] = {u.x, u.y, u.z, u.w};
+                G += g;
+                Qs += q2;
+                for (int j = 0; j < C; ++j) {
+                    Hn[j] += uk[j] * g;
+                    Fn[j] += uk[j] * uk[j] * q2;
+                }
+            }
+    }
+    for (int j = 0; j < C; ++j) {
+        const double H = G > 0.0 ? Hn[j] / G : 0.0;
+        const double F = Qs > 0.0 ? Fn[j] / Qs : 0.0;
+        const double a = __dadd_rn(__dadd_rn(1.0, -__dmul_rn(lam, H)), -__dmul_rn(xi, F));
+        a_out[j] = (float)fmax(a, (double)kAFloor);
+    }
 }
 
 // Reduce the per-thread partial sums of the CTA into one fp64 record
@@ -251,13 +289,21 @@ __global__ void __launch_bounds__(kStepThreads, 4) k_step_stencil(const StepArgs
 #pragma unroll
             for (int j = 0; j < C; ++j) G += hn[r][j];  // = sum_k g_ik (rows of U sum to 1)
             const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
-            float H[kMaxC] = {0.f, 0.f, 0.f, 0.f}, F[kMaxC] = {0.f, 0.f, 0.f, 0.f};
+            float av[kMaxC] = {1.f, 1.f, 1.f, 1.f};
+            bool band = false;
 #pragma unroll
             for (int j = 0; j < C; ++j) {
-                H[j] = hn[r][j] * invG;
-                F[j] = fmaf(w3, fa[r][2][j], fmaf(w2, fa[r][1][j], w1 * fa[r][0][j])) * invQ;
+                const float H = hn[r][j] * invG;                                           // Eq. 5
+                const float F = fmaf(w3, fa[r][2][j], fmaf(w2, fa[r][1][j], w1 * fa[r][0][j])) * invQ;  // Eq. 7
+                const float a1 = fmaf(-lam, H, fmaf(-xi, F, 1.0f));                      // Eq. 4 factor
+                band |= (a1 > -kBandLo) && (a1 < kBandHi);
+                av[j] = fmaxf(a1, kAFloor);                                              // R4
             }
-            const float4 un = membership<C, M2>(xr[r], c, H, F, lam, xi, a.m, a.inv_m1, num, den, Jacc);
+            if (band && (lam > 0.f || xi > 0.f))
+                attraction_fp64(&sU[0][0][0], &sX[0][0][0], kSY * kSX, sm, sc, sp, ty * kRY + 1 + r, tx + 1,
+                                xr[r], gx, gy, z, a.nx, a.ny, a.nz, a.lam_xi[2 * p], a.lam_xi[2 * p + 1], w2, w3,
+                                C, av);
+            const float4 un = membership<C, M2>(xr[r], c, av, a.m, a.inv_m1, num, den, Jacc);
             const float4 uo = sU[sc][ty * kRY + 1 + r][tx + 1];
             duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
                                        fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
@@ -284,7 +330,7 @@ __global__ void __launch_bounds__(kPwThreads) k_step_pointwise(const StepArgs a)
     float c[kMaxC];
 #pragma unroll
     for (int j = 0; j < kMaxC; ++j) c[j] = a.centers[4 * p + j];
-    const float H[kMaxC] = {0.f, 0.f, 0.f, 0.f}, F[kMaxC] = {0.f, 0.f, 0.f, 0.f};
+    const float av[kMaxC] = {1.f, 1.f, 1.f, 1.f};  // lambda = xi = 0: Eq. 4 factor is 1
     float num[kMaxC] = {0.f, 0.f, 0.f, 0.f}, den[kMaxC] = {0.f, 0.f, 0.f, 0.f};
     float Jacc = 0.f, duacc = a.first ? 1.0f : 0.f;
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -292,7 +338,7 @@ __global__ void __launch_bounds__(kPwThreads) k_step_pointwise(const StepArgs a)
         const int X = (int)(i % a.nx);
         const long long row = i / a.nx;  // = z*ny + y
         const float xv = a.x[row * a.pitch + X];
-        const float4 un = membership<C, M2>(xv, c, H, F, 0.f, 0.f, a.m, a.inv_m1, num, den, Jacc);
+        const float4 un = membership<C, M2>(xv, c, av, a.m, a.inv_m1, num, den, Jacc);
         if (!a.first) {
             const float4 uo = Uin[i];
             duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
