@@ -176,7 +176,7 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
              const float4 *Uin, float4 *Uout, const int *in_idx, const int *out_idx,
              float *centers, const double *lamxi, bool stencil, int first, int P,
              double *partials, double *fitness, double *stats, float eps, int *status,
-             const int *stop, cudaStream_t st) {
+             const int *stop, cudaStream_t st, int n_in_states) {
     StepArgs a{};
     a.x = x;
     a.nx = g->nx; a.ny = g->ny; a.nz = g->nz; a.pitch = g->pitch;
@@ -186,6 +186,8 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     a.stats = stats; a.stop = stop;
     a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f);
     a.q_mode = cfg->q_mode; a.first = first;
+    a.n_in_states = n_in_states;
+    a.want_du = (stats != nullptr) ? 1 : 0;
     const bool timed = ctx->timing && stencil;
     if (timed) {
         while (ctx->tev.size() < ctx->tused + 2) {
@@ -356,7 +358,7 @@ int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
     for (int t = 1; t <= iters; ++t) {
         float4 *dst = (((iters - t) & 1) == 0) ? reinterpret_cast<float4 *>(U_out) : scratch;
         r = run_step(ctx, grid, cfg, x, src, dst, nullptr, nullptr, centers, lam_xi, !zero, 0, P,
-                     partials, nullptr, S, eps, status, nullptr, st);
+                     partials, nullptr, S, eps, status, nullptr, st, P);
         if (r) return r;
         src = dst;
     }
@@ -411,7 +413,7 @@ int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
     float4 *slots = at<float4>(ws, L.slots);
     return run_step(ctx, grid, cfg, x, slots, slots, s.cur, s.nxt, s.centers, s.pos + 2 * L.p0, true, 0,
                     L.Pl, at<double>(ws, L.part), s.fit + L.p0, nullptr, 0.f, s.hdr + kHStatus,
-                    s.hdr + kHStop, st);
+                    s.hdr + kHStop, st, L.nslots);
 }
 
 int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
@@ -552,7 +554,7 @@ static int run_until(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *
     for (t = 1; t <= cfg->max_iter; ++t) {
         int r = run_step(ctx, g, cfg, x, slots + (long long)src * nvox, slots + (long long)dst * nvox, nullptr,
                          nullptr, centers, lamxi, stencil, (fcm_first && t == 1) ? 1 : 0, 1, partials,
-                         nullptr, stats, cfg->eps, status, nullptr, st);
+                         nullptr, stats, cfg->eps, status, nullptr, st, 1);
         if (r) return r;
         const int tmp = src; src = dst; dst = tmp;
         if (t % check_every == 0 || t == cfg->max_iter) {

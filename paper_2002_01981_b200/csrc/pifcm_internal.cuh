@@ -16,7 +16,7 @@ constexpr double kDenEps = 1e-12; // R9: keep c_j if sum u^m < 1e-12 (Eq. 3)
 // Ill-conditioned band of the Eq. 4 factor: fp32 a in (-kBandLo, kBandHi) is
 // re-evaluated in fp64 (u is proportional to a there).
 constexpr float kBandLo = 1e-4f;
-constexpr float kBandHi = 1e-2f;
+constexpr float kBandHi = 2.5e-3f;
 
 // Stencil step tiling (one CTA = TX x TY voxels per plane, marching TZ planes).
 constexpr int kTX = 32;             // one warp along x: 512 B coalesced rows
@@ -51,6 +51,8 @@ struct StepArgs {
     float m, inv_m1;     // m, 1/(m-1)
     int q_mode;
     int first;           // FCM first iteration: U_in not read, max|du| := 1
+    int n_in_states;     // states addressable from U_in (TMA tensor-map extent)
+    int want_du;         // accumulate max|u_new - u_old| (convergence tests)
 };
 
 struct FinalizeArgs {

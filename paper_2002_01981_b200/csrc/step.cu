@@ -19,6 +19,8 @@
 // denominator is recovered as G_i = sum_j Hn_ij = sum_k g_ik sum_j u_kj, which
 // automatically excludes out-of-bounds neighbours; the Eq. 7 denominator is a
 // closed form of the in-bounds neighbour counts per offset class.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include "pifcm_internal.cuh"
@@ -29,22 +31,6 @@ __device__ __forceinline__ float rcp_approx(float v) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
     return r;
-}
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    const int n = pred ? 16 : 0;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
-}
-__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool pred) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    const int n = pred ? 4 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
 // Per-voxel epilogue shared by the stencil and pointwise kernels: Eq. 4 with
@@ -99,41 +85,6 @@ __device__ __forceinline__ float4 membership(float xv, const float (&c)[kMaxC],
 // ill-conditioned band near 0.  There d2_ij (and so u_ij) is proportional to
 // a_j, so fp32 rounding of H and F (~1e-7 absolute) would be amplified by
 // 1/a_j; fp64 keeps the step within the parity tolerance.
-__device__ __noinline__ void attraction_fp64(const float4 *__restrict__ sU0, const float *__restrict__ sX0,
-                                             int stage_stride, int sm, int sc, int sp, int row, int col,
-                                             float xr, int gx, int gy, int z, int nx, int ny, int nz,
-                                             double lam, double xi, float w2, float w3, int C, float *a_out) {
-    double G = 0.0, Qs = 0.0, Hn[kMaxC] = {0.0, 0.0, 0.0, 0.0}, Fn[kMaxC] = {0.0, 0.0, 0.0, 0.0};
-    for (int dz = -1; dz <= 1; ++dz) {
-        const int s = dz < 0 ? sm : (dz == 0 ? sc : sp);
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                if (dx == 0 && dy == 0 && dz == 0) continue;
-                if (gx + dx < 0 || gx + dx >= nx || gy + dy < 0 || gy + dy >= ny || z + dz < 0 ||
-                    z + dz >= nz)
-                    continue;
-                const int e = s * stage_stride + (row + dy) * kSX + (col + dx);
-                const float4 u = sU0[e];
-                const double g = fabs((double)xr - (double)sX0[e]);
-                const int n = (dx != 0) + (dy != 0) + (dz != 0);
-                const double q2 = n == 1 ? 1.0 : (n == 2 ? (double)w2 : (double)w3);
-                const double uk[4] = {u.x, u.y, u.z, u.w};
-                G += g;
-                Qs += q2;
-                for (int j = 0; j < C; ++j) {
-                    Hn[j] += uk[j] * g;
-                    Fn[j] += uk[j] * uk[j] * q2;
-                }
-            }
-    }
-    for (int j = 0; j < C; ++j) {
-        const double H = G > 0.0 ? Hn[j] / G : 0.0;
-        const double F = Qs > 0.0 ? Fn[j] / Qs : 0.0;
-        const double a = __dadd_rn(__dadd_rn(1.0, -__dmul_rn(lam, H)), -__dmul_rn(xi, F));
-        a_out[j] = (float)fmax(a, (double)kAFloor);
-    }
-}
-
 // Reduce the per-thread partial sums of the CTA into one fp64 record
 // (fixed order: xor-shuffle tree in each warp, then warps in index order).
 template <int NW>
@@ -170,13 +121,196 @@ __device__ __forceinline__ void block_partials(const float (&num)[kMaxC], const 
 }
 
 // ----------------------------------------------------------------------------
-// Stencil step (lambda, xi arbitrary): the hot kernel.
+// TMA / mbarrier helpers (sm_90+ PTX, compiled for sm_100a).
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Shared-memory ring: kStages planes of the haloed U tile (float4) and of the
+// intensity tile (float, rows padded to kSXP for 16-byte TMA boxes).
+// TMA requires a 16-byte-aligned start of the innermost box dimension, so the
+// intensity box starts at x0 - 4 (not x0 - 1) and is 40 floats wide; the
+// thread's own column sits at kXOff = 4.
+constexpr int kSXP = 40;
+constexpr int kXOff = 4;
+constexpr int kUStageBytes = kSY * kSX * 16;  // 9792
+constexpr int kXStageBytes = kSY * kSXP * 4;  // 2592
+constexpr int kUStagePad = (kUStageBytes + 127) / 128 * 128;
+constexpr int kXStagePad = (kXStageBytes + 127) / 128 * 128;
+constexpr int kStencilSmem = kStages * (kUStagePad + kXStagePad) + 128;
+
+// ----------------------------------------------------------------------------
+// Packed (FFMA2) epilogue of one voxel: Eq. 4 distances from the attraction
+// factors A (already floored), Eq. 2 memberships, Eq. 1 / Eq. 3 partial sums.
+// Cluster pairs (0,1), (2,3); for odd C the padded component is masked.
 template <int C, bool M2>
-__global__ void __launch_bounds__(kStepThreads, 4) k_step_stencil(const StepArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    float4(*sU)[kSY][kSX] = reinterpret_cast<float4(*)[kSY][kSX]>(smem_raw);
-    float(*sX)[kSY][kSX] =
-        reinterpret_cast<float(*)[kSY][kSX]>(smem_raw + sizeof(float4) * kStages * kSY * kSX);
+__device__ __forceinline__ float4 membership2(float xv, const float2 (&c2)[2], const float2 (&A)[2], float m,
+                                              float inv_m1, float2 (&num2)[2], float2 (&den2)[2],
+                                              float &Jacc) {
+    constexpr int NP = (C + 1) / 2;
+    const float2 x2 = make_float2(xv, xv);
+    float d2[4];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        const float2 d = __fadd2_rn(x2, make_float2(-c2[q].x, -c2[q].y));
+        const float2 e = __fmul2_rn(__fmul2_rn(d, d), A[q]);  // Eq. 4
+        d2[2 * q] = e.x;
+        d2[2 * q + 1] = e.y;
+    }
+    float u[4] = {0.f, 0.f, 0.f, 0.f};
+    int jz = C;
+#pragma unroll
+    for (int j = C - 1; j >= 0; --j)
+        if (d2[j] == 0.0f) jz = j;
+    float Ji;
+    if (jz < C) {  // R5: zero distance -> crisp row at the lowest such j
+#pragma unroll
+        for (int j = 0; j < C; ++j) u[j] = (j == jz) ? 1.0f : 0.0f;
+        Ji = 0.0f;
+    } else {
+        float w[4] = {0.f, 0.f, 0.f, 0.f}, S = 0.0f;
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            w[j] = M2 ? rcp_approx(d2[j]) : exp2f(-log2f(d2[j]) * inv_m1);
+            S += w[j];
+        }
+        const float invS = rcp_approx(S);
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const float2 uu = __fmul2_rn(make_float2(w[2 * q], w[2 * q + 1]), make_float2(invS, invS));  // Eq. 2
+            u[2 * q] = uu.x;
+            u[2 * q + 1] = uu.y;
+        }
+        Ji = M2 ? invS : exp2f((1.0f - m) * log2f(S));  // Eq. 1 per voxel: S^{1-m}
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        const float2 uu = make_float2(u[2 * q], u[2 * q + 1]);
+        float2 um;
+        if (M2) {
+            um = __fmul2_rn(uu, uu);
+        } else {
+            um.x = uu.x > 0.f ? exp2f(m * log2f(uu.x)) : 0.f;
+            um.y = uu.y > 0.f ? exp2f(m * log2f(uu.y)) : 0.f;
+        }
+        num2[q] = __ffma2_rn(um, x2, num2[q]);  // Eq. 3 numerator
+        den2[q] = __fadd2_rn(den2[q], um);      // Eq. 3 denominator
+    }
+    Jacc += Ji;
+    return make_float4(u[0], u[1], u[2], u[3]);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-cooperative fp64 re-evaluation of the Eq. 4 factors of one voxel (the
+// ill-conditioned band): lane k < 26 takes neighbour k of
+// the 26-neighbourhood (Eq. 9), the per-neighbour terms of Eq. 5 / Eq. 7
+// (G = sum of in-bounds g, Qs = sum of in-bounds q2, numerators) are summed
+// across the warp in fp64, and every lane returns the floored factors.
+template <int C>
+__device__ __forceinline__ float4 attraction_coop(const float4 *Um, const float4 *Uc, const float4 *Up,
+                                                  const float *Xm, const float *Xc, const float *Xp,
+                                                  int row, int col, int gx, int gy, int z, int nx, int ny,
+                                                  int nz, double lam, double xi, double w2, double w3) {
+    const int lane = threadIdx.x & 31;
+    const int idx = lane < 13 ? lane : lane + 1;  // skip the centre (idx 13)
+    const int dz = idx / 9 - 1, dy = (idx / 3) % 3 - 1, dx = idx % 3 - 1;
+    double v[2 + 2 * kMaxC];
+#pragma unroll
+    for (int i = 0; i < 2 + 2 * kMaxC; ++i) v[i] = 0.0;
+    const bool inb = lane < 26 && gx + dx >= 0 && gx + dx < nx && gy + dy >= 0 && gy + dy < ny &&
+                     z + dz >= 0 && z + dz < nz;
+    if (inb) {
+        const float4 *Us = dz < 0 ? Um : (dz == 0 ? Uc : Up);
+        const float *Xs = dz < 0 ? Xm : (dz == 0 ? Xc : Xp);
+        const float4 u = Us[(row + dy) * kSX + col + 1 + dx];
+        const double xr = (double)Xc[row * kSXP + col + kXOff];
+        const double g = fabs(xr - (double)Xs[(row + dy) * kSXP + col + kXOff + dx]);  // Eq. 6
+        const int n = (dx != 0) + (dy != 0) + (dz != 0);
+        const double q2 = n == 1 ? 1.0 : (n == 2 ? w2 : w3);                            // Eq. 8, R1
+        const double uk[4] = {u.x, u.y, u.z, u.w};
+        v[0] = g;
+        v[1] = q2;
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            v[2 + j] = uk[j] * g;                     // Eq. 5 numerator term
+            v[2 + kMaxC + j] = uk[j] * uk[j] * q2;   // Eq. 7 numerator term
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 2 + 2 * kMaxC; ++i) {
+        if (i >= 2 + C && i < 2 + kMaxC) continue;
+        if (i >= 2 + kMaxC + C) continue;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    }
+    float out[4] = {1.f, 1.f, 1.f, 1.f};
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+        const double H = v[0] > 0.0 ? v[2 + j] / v[0] : 0.0;          // Eq. 5, R3
+        const double F = v[1] > 0.0 ? v[2 + kMaxC + j] / v[1] : 0.0;  // Eq. 7
+        const double av = __dadd_rn(__dadd_rn(1.0, -__dmul_rn(lam, H)), -__dmul_rn(xi, F));  // Eq. 4
+        out[j] = (float)fmax(av, (double)kAFloor);                   // R4
+    }
+    return make_float4(out[0], out[1], out[2], out[3]);
+}
+
+// ----------------------------------------------------------------------------
+// Stencil step (lambda, xi arbitrary): the hot kernel.
+//   thread (tx, ty): x = x0 + tx, rows y0 + ty*kRY + r (r < kRY) of plane z.
+//   Per plane it streams the 9 (dx, dz) columns of kRY+2 haloed rows from
+//   shared memory; each loaded neighbour row updates up to 3 of the thread's
+//   voxels.  Per (neighbour, voxel) pair: one FADD (g, Eq. 6) and, per cluster
+//   pair, one FFMA2 for the Eq. 5 numerator and one for the Eq. 7 class sum.
+//   Planes arrive by TMA into a 4-stage ring (full barriers); each warp
+//   releases a stage on its empty barrier, so warps are not lock-stepped.
+template <int C, bool M2, bool DU>
+__global__ void __launch_bounds__(kStepThreads, 4)
+    k_step_stencil(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
+                   const StepArgs a) {
+    constexpr int NP = (C + 1) / 2;  // cluster pairs (FFMA2 lanes)
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *base = smem_raw;  // >= 16-byte aligned: enough for non-swizzled TMA boxes
+    auto sUst = [&](int s) { return reinterpret_cast<float4 *>(base + s * kUStagePad); };
+    auto sXst = [&](int s) { return reinterpret_cast<float *>(base + kStages * kUStagePad + s * kXStagePad); };
+    __shared__ __align__(8) uint64_t full[kStages];
+    __shared__ __align__(8) uint64_t empty[kStages];
 
     const int p = blockIdx.z;
     if (a.stop && *a.stop) return;
@@ -189,130 +323,199 @@ __global__ void __launch_bounds__(kStepThreads, 4) k_step_stencil(const StepArgs
     const int ze = min(zb + kTZ, a.nz);
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
+    const int slot = a.in_idx ? a.in_idx[p] : p;
 
-    const long long plane = (long long)a.nx * a.ny;
-    const float4 *Uin = a.U_in + (long long)(a.in_idx ? a.in_idx[p] : p) * a.nvox;
-    float4 *Uout = a.U_out + (long long)(a.out_idx ? a.out_idx[p] : p) * a.nvox;
-
-    float c[kMaxC];
-#pragma unroll
-    for (int j = 0; j < kMaxC; ++j) c[j] = a.centers[4 * p + j];
-    const float lam = (float)a.lam_xi[2 * p], xi = (float)a.lam_xi[2 * p + 1];
-    // Eq. 7 class weights: q2 for 1, 2, 3 non-zero offsets (R1)
-    const float w1 = 1.0f, w2 = a.q_mode == 0 ? 4.0f : 2.0f, w3 = a.q_mode == 0 ? 9.0f : 3.0f;
-
-    auto load_plane = [&](int z) {
-        const int s = (z + kStages) & (kStages - 1);
-        const bool zin = (z >= 0) && (z < a.nz);
-        for (int e = tid; e < kSY * kSX; e += kStepThreads) {
-            const int yy = e / kSX, xx = e - yy * kSX;
-            const int gy = y0 - 1 + yy, gx = x0 - 1 + xx;
-            const bool in = zin && gy >= 0 && gy < a.ny && gx >= 0 && gx < a.nx;
-            const long long vi = in ? ((long long)z * plane + (long long)gy * a.nx + gx) : 0;
-            cp_async16(&sU[s][yy][xx], Uin + vi, in);
-            const long long xo = in ? ((long long)z * a.ny + gy) * a.pitch + gx : 0;
-            cp_async4(&sX[s][yy][xx], a.x + xo, in);
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarpsY);
         }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // TMA of plane q (q may lie outside [0, nz): the box is zero-filled).  The
+    // tensor maps are used through their kernel-parameter addresses.
+    const CUtensorMap *pmU = &tmU, *pmX = &tmX;
+#define PIFCM_ISSUE_PLANE(q_)                                                        \
+    do {                                                                             \
+        const int l_ = (q_) - (zb - 1);                                              \
+        const int s_ = l_ & (kStages - 1);                                           \
+        if (l_ >= kStages) mbar_wait(&empty[s_], ((l_ >> 2) - 1) & 1);               \
+        mbar_expect_tx(&full[s_], kUStageBytes + kXStageBytes);                      \
+        tma_load_5d(sUst(s_), pmU, &full[s_], 0, x0 - 1, y0 - 1, (q_), slot);        \
+        tma_load_3d(sXst(s_), pmX, &full[s_], x0 - kXOff, y0 - 1, (q_));            \
+    } while (0)
+    auto wait_plane = [&](int q) {
+        const int l = q - (zb - 1);
+        mbar_wait(&full[l & (kStages - 1)], (l >> 2) & 1);
     };
 
-    float num[kMaxC] = {0.f, 0.f, 0.f, 0.f}, den[kMaxC] = {0.f, 0.f, 0.f, 0.f};
+    if (tid == 0) {
+        PIFCM_ISSUE_PLANE(zb - 1);
+        PIFCM_ISSUE_PLANE(zb);
+        if (zb + 1 <= ze) PIFCM_ISSUE_PLANE(zb + 1);
+    }
+
+    float4 *Uout = a.U_out + (long long)(a.out_idx ? a.out_idx[p] : p) * a.nvox;
+    const long long plane = (long long)a.nx * a.ny;
+    float2 c2[2];
+    c2[0] = make_float2(a.centers[4 * p + 0], a.centers[4 * p + 1]);
+    c2[1] = make_float2(a.centers[4 * p + 2], a.centers[4 * p + 3]);
+    const float lam = (float)a.lam_xi[2 * p], xi = (float)a.lam_xi[2 * p + 1];
+    const float2 nlam2 = make_float2(-lam, -lam), nxi2 = make_float2(-xi, -xi);
+    const float w2 = a.q_mode == 0 ? 4.0f : 2.0f, w3 = a.q_mode == 0 ? 9.0f : 3.0f;  // Eq. 7 q2 (R1)
+    const float2 w22 = make_float2(w2, w2), w32 = make_float2(w3, w3);
+    const int gx = x0 + tx;
+    const int px = (gx > 0) + (gx < a.nx - 1);
+    // Eq. 7 denominator (closed form of the in-bounds neighbour counts per
+    // class) for interior planes (pz = 2), per own row
+    float invQi[kRY];
+#pragma unroll
+    for (int r = 0; r < kRY; ++r) {
+        const int gy = y0 + ty * kRY + r;
+        const int py = (gy > 0) + (gy < a.ny - 1);
+        const float Qs = (float)(px + py + 2) + w2 * (float)(px * py + 2 * py + 2 * px) + w3 * (float)(px * py * 2);
+        invQi[r] = 1.0f / Qs;
+    }
+
+    float2 num2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float2 den2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     float Jacc = 0.f, duacc = 0.f;
 
-    load_plane(zb - 1);
-    load_plane(zb);
-    load_plane(zb + 1);
-    cp_async_commit();
-
+    wait_plane(zb - 1);
+    wait_plane(zb);
     for (int z = zb; z < ze; ++z) {
-        if (z + 2 <= ze) load_plane(z + 2);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-
-        const int sm = (z - 1 + kStages) & (kStages - 1);
-        const int sc = z & (kStages - 1);
-        const int sp = (z + 1) & (kStages - 1);
+        if (tid == 0 && z + 2 <= ze) PIFCM_ISSUE_PLANE(z + 2);
+        wait_plane(z + 1);
+        const int lz = z - (zb - 1);
+        const int sm = (lz - 1) & (kStages - 1), sc = lz & (kStages - 1), sp = (lz + 1) & (kStages - 1);
+        const float4 *Um = sUst(sm), *Uc = sUst(sc), *Up = sUst(sp);
+        const float *Xm = sXst(sm), *Xc = sXst(sc), *Xp = sXst(sp);
 
         float xr[kRY];
 #pragma unroll
-        for (int r = 0; r < kRY; ++r) xr[r] = sX[sc][ty * kRY + 1 + r][tx + 1];
+        for (int r = 0; r < kRY; ++r) xr[r] = Xc[(ty * kRY + 1 + r) * kSXP + tx + kXOff];
 
-        float hn[kRY][C], fa[kRY][3][C];
+        float2 hn[kRY][NP], fa[kRY][3][NP];
 #pragma unroll
         for (int r = 0; r < kRY; ++r)
 #pragma unroll
-            for (int j = 0; j < C; ++j) {
-                hn[r][j] = 0.f;
-                fa[r][0][j] = 0.f; fa[r][1][j] = 0.f; fa[r][2][j] = 0.f;
+            for (int q = 0; q < NP; ++q) {
+                hn[r][q] = make_float2(0.f, 0.f);
+                fa[r][0][q] = make_float2(0.f, 0.f);
+                fa[r][1][q] = make_float2(0.f, 0.f);
+                fa[r][2][q] = make_float2(0.f, 0.f);
             }
 
 #pragma unroll
         for (int dz = -1; dz <= 1; ++dz) {
-            const int s = dz < 0 ? sm : (dz == 0 ? sc : sp);
+            const float4 *Us = dz < 0 ? Um : (dz == 0 ? Uc : Up);
+            const float *Xs = dz < 0 ? Xm : (dz == 0 ? Xc : Xp);
 #pragma unroll
             for (int dx = -1; dx <= 1; ++dx) {
 #pragma unroll
                 for (int t = 0; t < kRY + 2; ++t) {
-                    const float4 uk4 = sU[s][ty * kRY + t][tx + 1 + dx];
-                    const float xk = sX[s][ty * kRY + t][tx + 1 + dx];
-                    const float uk[4] = {uk4.x, uk4.y, uk4.z, uk4.w};
+                    const float4 uk4 = Us[(ty * kRY + t) * kSX + tx + 1 + dx];
+                    const float xk = Xs[(ty * kRY + t) * kSXP + tx + kXOff + dx];
+                    const float2 u01 = make_float2(uk4.x, uk4.y), u23 = make_float2(uk4.z, uk4.w);
 #pragma unroll
                     for (int r = 0; r < kRY; ++r) {
                         const int dy = t - 1 - r;
                         if (dy < -1 || dy > 1) continue;
                         if (dx == 0 && dy == 0 && dz == 0) continue;  // Eq. 9: k != i
-                        const int ncls = (dx != 0) + (dy != 0) + (dz != 0);
-                        const float g = fabsf(xr[r] - xk);         // Eq. 6
-#pragma unroll
-                        for (int j = 0; j < C; ++j) {
-                            hn[r][j] = fmaf(uk[j], g, hn[r][j]);          // Eq. 5 numerator
-                            fa[r][ncls - 1][j] = fmaf(uk[j], uk[j], fa[r][ncls - 1][j]);  // Eq. 7
+                        const int cls = (dx != 0) + (dy != 0) + (dz != 0) - 1;
+                        const float g = fabsf(xr[r] - xk);          // Eq. 6
+                        const float2 g2 = make_float2(g, g);
+                        hn[r][0] = __ffma2_rn(u01, g2, hn[r][0]);            // Eq. 5 numerator
+                        fa[r][cls][0] = __ffma2_rn(u01, u01, fa[r][cls][0]);  // Eq. 7 class sums
+                        if (NP > 1) {
+                            hn[r][NP - 1] = __ffma2_rn(u23, g2, hn[r][NP - 1]);
+                            fa[r][cls][NP - 1] = __ffma2_rn(u23, u23, fa[r][cls][NP - 1]);
                         }
                     }
                 }
             }
         }
 
-        // Eq. 7 denominator from the in-bounds neighbour counts per class.
-        const int gx = x0 + tx;
-        const int px = (gx > 0) + (gx < a.nx - 1);
         const int pz = (z > 0) + (z < a.nz - 1);
+        unsigned band_bits = 0u;
 #pragma unroll
         for (int r = 0; r < kRY; ++r) {
             const int gy = y0 + ty * kRY + r;
             if (gx >= a.nx || gy >= a.ny) continue;
-            const int py = (gy > 0) + (gy < a.ny - 1);
-            const float Qs = w1 * (float)(px + py + pz) + w2 * (float)(px * py + py * pz + pz * px) +
-                             w3 * (float)(px * py * pz);
-            const float invQ = Qs > 0.f ? 1.0f / Qs : 0.f;
-            float G = 0.f;
-#pragma unroll
-            for (int j = 0; j < C; ++j) G += hn[r][j];  // = sum_k g_ik (rows of U sum to 1)
+            float invQ = invQi[r];
+            if (pz != 2) {
+                const int py = (gy > 0) + (gy < a.ny - 1);
+                const float Qs = (float)(px + py + pz) + w2 * (float)(px * py + py * pz + pz * px) +
+                                 w3 * (float)(px * py * pz);
+                invQ = Qs > 0.f ? 1.0f / Qs : 0.f;
+            }
+            float G = hn[r][0].x + hn[r][0].y;
+            if (C > 2) G += hn[r][NP - 1].x;
+            if (C > 3) G += hn[r][NP - 1].y;  // = sum_k g_ik (rows of U sum to 1)
             const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
-            float av[kMaxC] = {1.f, 1.f, 1.f, 1.f};
+            float2 A[2];
             bool band = false;
 #pragma unroll
-            for (int j = 0; j < C; ++j) {
-                const float H = hn[r][j] * invG;                                           // Eq. 5
-                const float F = fmaf(w3, fa[r][2][j], fmaf(w2, fa[r][1][j], w1 * fa[r][0][j])) * invQ;  // Eq. 7
-                const float a1 = fmaf(-lam, H, fmaf(-xi, F, 1.0f));                      // Eq. 4 factor
-                band |= (a1 > -kBandLo) && (a1 < kBandHi);
-                av[j] = fmaxf(a1, kAFloor);                                              // R4
+            for (int q = 0; q < NP; ++q) {
+                const float2 H = __fmul2_rn(hn[r][q], make_float2(invG, invG));                 // Eq. 5
+                const float2 F = __fmul2_rn(__ffma2_rn(fa[r][2][q], w32, __ffma2_rn(fa[r][1][q], w22, fa[r][0][q])),
+                                            make_float2(invQ, invQ));                            // Eq. 7
+                A[q] = __ffma2_rn(H, nlam2, __ffma2_rn(F, nxi2, make_float2(1.f, 1.f)));         // Eq. 4
+                band |= (A[q].x > -kBandLo) && (A[q].x < kBandHi);
+                if (2 * q + 1 < C) band |= (A[q].y > -kBandLo) && (A[q].y < kBandHi);
+                A[q].x = fmaxf(A[q].x, kAFloor);                                                  // R4
+                A[q].y = fmaxf(A[q].y, kAFloor);
             }
-            if (band && (lam > 0.f || xi > 0.f))
-                attraction_fp64(&sU[0][0][0], &sX[0][0][0], kSY * kSX, sm, sc, sp, ty * kRY + 1 + r, tx + 1,
-                                xr[r], gx, gy, z, a.nx, a.ny, a.nz, a.lam_xi[2 * p], a.lam_xi[2 * p + 1], w2, w3,
-                                C, av);
-            const float4 un = membership<C, M2>(xr[r], c, av, a.m, a.inv_m1, num, den, Jacc);
-            const float4 uo = sU[sc][ty * kRY + 1 + r][tx + 1];
-            duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
-                                       fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
+            if (NP == 1) A[1] = make_float2(1.f, 1.f);
+            if (band) {  // deferred to the warp-cooperative fp64 pass below
+                band_bits |= 1u << r;
+                continue;
+            }
+            const float4 un = membership2<C, M2>(xr[r], c2, A, a.m, a.inv_m1, num2, den2, Jacc);
+            if (DU) {
+                const float4 uo = Uc[(ty * kRY + 1 + r) * kSX + tx + 1];
+                duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
+                                           fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
+            }
             Uout[(long long)z * plane + (long long)gy * a.nx + gx] = un;
         }
-        __syncthreads();
-    }
-    cp_async_wait<0>();
 
+        // Ill-conditioned voxels of this warp, one at a time, all lanes together.
+        unsigned lanes = __ballot_sync(0xffffffffu, band_bits != 0u);
+        while (lanes) {
+            const int L = __ffs(lanes) - 1;
+            lanes &= lanes - 1;
+            unsigned bits = __shfl_sync(0xffffffffu, band_bits, L);
+            while (bits) {
+                const int r = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int row = ty * kRY + 1 + r;
+                const int gxL = x0 + L, gy = y0 + ty * kRY + r;
+                const float4 a4 = attraction_coop<C>(Um, Uc, Up, Xm, Xc, Xp, row, L, gxL, gy, z, a.nx, a.ny,
+                                                     a.nz, a.lam_xi[2 * p], a.lam_xi[2 * p + 1], w2, w3);
+                if (tx == L) {
+                    const float2 A[2] = {make_float2(a4.x, a4.y), make_float2(a4.z, a4.w)};
+                    const float xv = Xc[row * kSXP + L + kXOff];
+                    const float4 un = membership2<C, M2>(xv, c2, A, a.m, a.inv_m1, num2, den2, Jacc);
+                    if (DU) {
+                        const float4 uo = Uc[row * kSX + L + 1];
+                        duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
+                                                   fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
+                    }
+                    Uout[(long long)z * plane + (long long)gy * a.nx + gxL] = un;
+                }
+            }
+        }
+        // this warp no longer needs plane z-1
+        __syncwarp();
+        if (tx == 0) mbar_arrive(&empty[sm]);
+    }
+#undef PIFCM_ISSUE_PLANE
+
+    float num[kMaxC] = {num2[0].x, num2[0].y, num2[1].x, num2[1].y};
+    float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
     const int blk = blockIdx.x + gridDim.x * blockIdx.y;
     block_partials<kWarpsY>(num, den, Jacc, duacc, a.partials + ((long long)p * a.nblk + blk) * kNR);
 }
@@ -364,22 +567,60 @@ int step_nblk(int nx, int ny, int nz, bool stencil) {
     return tx * ty * tz;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// U states: 5-D (4 floats, x, y, z, state); x: 3-D (x, y, z) with pitched rows.
+static bool make_maps(const StepArgs &a, CUtensorMap *mU, CUtensorMap *mX) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    const cuuint64_t du[5] = {4, (cuuint64_t)a.nx, (cuuint64_t)a.ny, (cuuint64_t)a.nz, (cuuint64_t)a.n_in_states};
+    const cuuint64_t su[4] = {16, 16ull * a.nx, 16ull * a.nx * a.ny, 16ull * (cuuint64_t)a.nvox};
+    const cuuint32_t bu[5] = {4, kSX, kSY, 1, 1};
+    const cuuint32_t e5[5] = {1, 1, 1, 1, 1};
+    if (enc(mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float4 *>(a.U_in), du, su, bu, e5,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    const cuuint64_t dx[3] = {(cuuint64_t)a.nx, (cuuint64_t)a.ny, (cuuint64_t)a.nz};
+    const cuuint64_t sx[2] = {4ull * a.pitch, 4ull * a.pitch * a.ny};
+    const cuuint32_t bx[3] = {kSXP, kSY, 1};
+    return enc(mX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(a.x), dx, sx, bx, e5,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int C, bool M2, bool DU>
+static cudaError_t launch_stencil(const StepArgs &a, int P, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_step_stencil<C, M2, DU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kStencilSmem);
+        attr = true;
+    }
+    CUtensorMap mU, mX;
+    if (!make_maps(a, &mU, &mX)) return cudaErrorInvalidValue;
+    dim3 grid(a.tiles_x * a.tiles_y, a.zchunks, P);
+    k_step_stencil<C, M2, DU><<<grid, kStepThreads, kStencilSmem, st>>>(mU, mX, a);
+    return cudaGetLastError();
+}
+
 template <int C, bool M2>
 static cudaError_t launch_t(const StepArgs &a, bool stencil, int P, cudaStream_t st) {
     if (stencil) {
-        const size_t smem = (sizeof(float4) + sizeof(float)) * kStages * kSY * kSX;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_step_stencil<C, M2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-            attr = true;
-        }
-        dim3 grid(a.tiles_x * a.tiles_y, a.zchunks, P);
-        k_step_stencil<C, M2><<<grid, kStepThreads, smem, st>>>(a);
-    } else {
-        dim3 grid(a.nblk, P);
-        k_step_pointwise<C, M2><<<grid, kPwThreads, 0, st>>>(a);
+        return a.want_du ? launch_stencil<C, M2, true>(a, P, st) : launch_stencil<C, M2, false>(a, P, st);
     }
+    dim3 grid(a.nblk, P);
+    k_step_pointwise<C, M2><<<grid, kPwThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 
