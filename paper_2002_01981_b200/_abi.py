@@ -89,11 +89,13 @@ SIGNATURES = {
 _lib = None
 
 
-def load(path: str = LIB_PATH) -> ct.CDLL:
-    """Load libpifcm.so; raise if it is missing (no fallback exists)."""
+def load(path: str | None = None) -> ct.CDLL:
+    """Load libpifcm.so; raise if it is missing (no fallback exists).
+    PIFCM_LIB may name a tuning variant built by build.py --out=..."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("PIFCM_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(
             f"libpifcm.so not found at {path}: build it with `python -m paper_2002_01981_b200.build` "

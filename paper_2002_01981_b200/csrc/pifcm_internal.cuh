@@ -13,20 +13,34 @@ constexpr int kMaxC = 4;          // AoS-C4 rows: one float4 per voxel
 constexpr int kNR = 2 * kMaxC + 2; // partial record: num[4], den[4], J, max|du|
 constexpr float kAFloor = 1e-9f;  // R4: floor of 1 - lam H - xi F (Eq. 4)
 constexpr double kDenEps = 1e-12; // R9: keep c_j if sum u^m < 1e-12 (Eq. 3)
-// Ill-conditioned band of the Eq. 4 factor: fp32 a in (-kBandLo, kBandHi) is
-// re-evaluated in fp64 (u is proportional to a there).
-constexpr float kBandLo = 1e-4f;
-constexpr float kBandHi = 2.5e-3f;
+// Ill-conditioned voxels: u_j moves by u_j (1 - u_j) / ((m-1) a_j) per unit
+// relative change of the Eq. 4 factor a_j.  The fp32 factors are accurate to
+// kAErr (absolute; sums of <= 26 positive fp32 terms, a ratio and two FMAs),
+// so a voxel whose sensitivity K = sum_j u_j (1 - u_j) / ((m-1) a_j) exceeds
+// kKMax = kUTol / kAErr is re-evaluated from the definitions in fp64
+// (DESIGN.md §Numerics).  kUTol leaves a 4x margin to the 1e-4 tolerance.
+#ifndef PIFCM_KMAX
+#define PIFCM_KMAX 25.0f
+#endif
+constexpr float kAErr = 1e-6f;
+constexpr float kUTol = 2.5e-5f;
+constexpr float kKMax = PIFCM_KMAX;  // = kUTol / kAErr
 
 // Stencil step tiling (one CTA = TX x TY voxels per plane, marching TZ planes).
 constexpr int kTX = 32;             // one warp along x: 512 B coalesced rows
-constexpr int kWarpsY = 4;          // warps per CTA, stacked in y
-constexpr int kRY = 4;              // consecutive y rows per thread (register blocking)
+#ifndef PIFCM_WARPS_Y
+#define PIFCM_WARPS_Y 4
+#endif
+#ifndef PIFCM_RY
+#define PIFCM_RY 4
+#endif
+constexpr int kWarpsY = PIFCM_WARPS_Y;  // warps per CTA, stacked in y
+constexpr int kRY = PIFCM_RY;           // consecutive y rows per thread (register blocking)
 constexpr int kTY = kWarpsY * kRY;  // 16
 constexpr int kSX = kTX + 2;        // haloed smem row length
 constexpr int kSY = kTY + 2;        // haloed smem rows
 constexpr int kStages = 4;          // plane ring: z-1, z, z+1 resident, z+2 landing
-constexpr int kTZ = 16;             // planes per CTA (z-chunk)
+constexpr int kTZ = 32;             // planes per CTA (z-chunk)
 constexpr int kStepThreads = kTX * kWarpsY;
 
 // Pointwise (FCM, lambda = xi = 0) step.

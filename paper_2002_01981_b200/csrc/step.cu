@@ -151,6 +151,14 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, u
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
                                             int c2) {
     asm volatile(
@@ -171,55 +179,94 @@ constexpr int kUStageBytes = kSY * kSX * 16;  // 9792
 constexpr int kXStageBytes = kSY * kSXP * 4;  // 2592
 constexpr int kUStagePad = (kUStageBytes + 127) / 128 * 128;
 constexpr int kXStagePad = (kXStageBytes + 127) / 128 * 128;
-constexpr int kStencilSmem = kStages * (kUStagePad + kXStagePad) + 128;
+#ifndef PIFCM_STEP_MINBLOCKS
+#define PIFCM_STEP_MINBLOCKS 3
+#endif
+constexpr int kStepMinBlocks = PIFCM_STEP_MINBLOCKS;  // CTAs per SM the register budget targets
+#ifndef PIFCM_RING
+#define PIFCM_RING 5
+#endif
+constexpr int kRing = PIFCM_RING;  // planes in flight: z-1, z, z+1 in use, the rest prefetching
+constexpr int kStencilSmem = kRing * (kUStagePad + kXStagePad) + 128;
 
 // ----------------------------------------------------------------------------
 // Packed (FFMA2) epilogue of one voxel: Eq. 4 distances from the attraction
 // factors A (already floored), Eq. 2 memberships, Eq. 1 / Eq. 3 partial sums.
 // Cluster pairs (0,1), (2,3); for odd C the padded component is masked.
+// Memberships of one voxel (Eq. 4 distances from the floored attraction
+// factors A, Eq. 2), its Eq. 1 cost and its sensitivity to the factors:
+//   K = sum_j |d u / d ln a_j| = sum_j u_j (1 - u_j) / ((m - 1) a_j)
+// (1/a_j = w_j (x - c_j)^2 for m = 2, with w_j = d2_ij^{-1/(m-1)}); the fp32
+// factors carry an absolute error <= kAErr, so K * kAErr bounds the error
+// of u, and voxels with K > kKMax are re-evaluated in fp64.
+struct Memb {
+    float u[4];
+    float Ji, K;
+};
 template <int C, bool M2>
-__device__ __forceinline__ float4 membership2(float xv, const float2 (&c2)[2], const float2 (&A)[2], float m,
-                                              float inv_m1, float2 (&num2)[2], float2 (&den2)[2],
-                                              float &Jacc) {
+__device__ __forceinline__ Memb memb_compute(float xv, const float2 (&c2)[2], const float2 (&A)[2], float m,
+                                             float inv_m1, const float2 (&Ar)[2]) {
     constexpr int NP = (C + 1) / 2;
     const float2 x2 = make_float2(xv, xv);
-    float d2[4];
+    float d2[4], dd[4];
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         const float2 d = __fadd2_rn(x2, make_float2(-c2[q].x, -c2[q].y));
-        const float2 e = __fmul2_rn(__fmul2_rn(d, d), A[q]);  // Eq. 4
+        const float2 s2 = __fmul2_rn(d, d);
+        const float2 e = __fmul2_rn(s2, A[q]);  // Eq. 4
         d2[2 * q] = e.x;
         d2[2 * q + 1] = e.y;
+        dd[2 * q] = s2.x;
+        dd[2 * q + 1] = s2.y;
     }
-    float u[4] = {0.f, 0.f, 0.f, 0.f};
-    int jz = C;
+    float w[4] = {0.f, 0.f, 0.f, 0.f}, S = 0.0f;
 #pragma unroll
-    for (int j = C - 1; j >= 0; --j)
-        if (d2[j] == 0.0f) jz = j;
-    float Ji;
-    if (jz < C) {  // R5: zero distance -> crisp row at the lowest such j
-#pragma unroll
-        for (int j = 0; j < C; ++j) u[j] = (j == jz) ? 1.0f : 0.0f;
-        Ji = 0.0f;
-    } else {
-        float w[4] = {0.f, 0.f, 0.f, 0.f}, S = 0.0f;
-#pragma unroll
-        for (int j = 0; j < C; ++j) {
-            w[j] = M2 ? rcp_approx(d2[j]) : exp2f(-log2f(d2[j]) * inv_m1);
-            S += w[j];
-        }
-        const float invS = rcp_approx(S);
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const float2 uu = __fmul2_rn(make_float2(w[2 * q], w[2 * q + 1]), make_float2(invS, invS));  // Eq. 2
-            u[2 * q] = uu.x;
-            u[2 * q + 1] = uu.y;
-        }
-        Ji = M2 ? invS : exp2f((1.0f - m) * log2f(S));  // Eq. 1 per voxel: S^{1-m}
+    for (int j = 0; j < C; ++j) {
+        w[j] = M2 ? rcp_approx(d2[j]) : exp2f(-log2f(d2[j]) * inv_m1);  // d2 = 0 -> +inf
+        S += w[j];
     }
+    const float invS = rcp_approx(S);
+    Memb r;
+    float Kp[2] = {0.f, 0.f};
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-        const float2 uu = make_float2(u[2 * q], u[2 * q + 1]);
+        const float2 wq = make_float2(w[2 * q], w[2 * q + 1]);
+        const float2 uu = __fmul2_rn(wq, make_float2(invS, invS));  // Eq. 2
+        r.u[2 * q] = uu.x;
+        r.u[2 * q + 1] = uu.y;
+        // u (1 - u) / |a| with the unfloored factor: a clamped factor (a << 0)
+        // contributes little (its u is ~0 or ~1), an uncertain clamp (|a| ~ 0)
+        // makes K huge, an unclamped small factor is weighed by 1/a
+        const float2 ia = make_float2(rcp_approx(fabsf(Ar[q].x)), rcp_approx(fabsf(Ar[q].y)));
+        const float2 t = __fmul2_rn(__fmul2_rn(uu, __fadd2_rn(make_float2(1.f, 1.f), make_float2(-uu.x, -uu.y))), ia);
+        Kp[q] = t.x + ((2 * q + 1 < C) ? t.y : 0.f);
+    }
+    if (NP == 1) { r.u[2] = 0.f; r.u[3] = 0.f; }
+    r.K = M2 ? Kp[0] + Kp[1] : (Kp[0] + Kp[1]) * inv_m1;
+    (void)dd;
+    r.Ji = M2 ? invS : exp2f((1.0f - m) * log2f(S));  // Eq. 1 per voxel: S^{1-m}
+    if (!(S < INFINITY)) {  // R5: a zero distance -> crisp row at the lowest such j (rare)
+        int jz = C - 1;
+#pragma unroll
+        for (int j = C - 1; j >= 0; --j)
+            if (d2[j] == 0.0f) jz = j;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r.u[j] = (j == jz) ? 1.0f : 0.0f;
+        r.Ji = 0.0f;
+        r.K = 0.0f;
+    }
+    return r;
+}
+
+// Eq. 3 / Eq. 1 partial sums of one voxel.
+template <int C, bool M2>
+__device__ __forceinline__ void memb_accumulate(const Memb &r, float xv, float m, float2 (&num2)[2],
+                                                float2 (&den2)[2], float &Jacc) {
+    constexpr int NP = (C + 1) / 2;
+    const float2 x2 = make_float2(xv, xv);
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        const float2 uu = make_float2(r.u[2 * q], r.u[2 * q + 1]);
         float2 um;
         if (M2) {
             um = __fmul2_rn(uu, uu);
@@ -230,8 +277,16 @@ __device__ __forceinline__ float4 membership2(float xv, const float2 (&c2)[2], c
         num2[q] = __ffma2_rn(um, x2, num2[q]);  // Eq. 3 numerator
         den2[q] = __fadd2_rn(den2[q], um);      // Eq. 3 denominator
     }
-    Jacc += Ji;
-    return make_float4(u[0], u[1], u[2], u[3]);
+    Jacc += r.Ji;
+}
+
+template <int C, bool M2>
+__device__ __forceinline__ float4 membership2(float xv, const float2 (&c2)[2], const float2 (&A)[2], float m,
+                                              float inv_m1, float2 (&num2)[2], float2 (&den2)[2],
+                                              float &Jacc) {
+    const Memb r = memb_compute<C, M2>(xv, c2, A, m, inv_m1, A);
+    memb_accumulate<C, M2>(r, xv, m, num2, den2, Jacc);
+    return make_float4(r.u[0], r.u[1], r.u[2], r.u[3]);
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -292,25 +347,79 @@ __device__ __forceinline__ float4 attraction_coop(const float4 *Um, const float4
 }
 
 // ----------------------------------------------------------------------------
+// In-plane parts of the Eq. 7 numerator for the thread's own rows.  The Eq. 7
+// numerator Fn_ij = sum_k q2_ik u_kj^2 is a linear 3x3x3 stencil of v = u^2
+// whose weight depends only on the offset class n = |dX|+|dY|+|dZ| (Eq. 8,
+// R1: q2 = W(n), W(1) = 1, W(2) = w2, W(3) = w3, W(0) = 0 for k = i).  Per
+// plane it therefore splits into two in-plane stencils:
+//   S (the target's own plane):  W(1) E + W(2) K
+//   R (a plane at dZ = +-1):     W(1) v(0,0) + W(2) E + W(3) K
+// with E = edge sum v(+-1,0) + v(0,+-1) and K = corner sum v(+-1,+-1), and
+//   Fn(z) = R(z-1) + S(z) + R(z+1).
+// Here v(x-1) + v(x+1) (d) and v(x) (c) are formed per haloed row and the
+// rows are combined with a 3-row sliding window.
+// MODE 0: S, R <- the sums of this plane.  MODE 1 (steady state, plane z+1 of
+// target plane z): Fn = Pc + R; Pc = Rc + S; Rc = R, row by row.
+template <int NP, int MODE>
+__device__ __forceinline__ void plane_SR(const float4 *Us, int ty, int tx, float2 w22, float2 w32,
+                                         float2 (&S)[kRY][NP], float2 (&R)[kRY][NP],
+                                         float2 (&Fn)[kRY][NP]) {
+    float2 dwin[3][NP], cwin[3][NP];
+#pragma unroll
+    for (int t = 0; t < kRY + 2; ++t) {
+        const int o = (ty * kRY + t) * kSX + tx + 1;
+        const float4 ul = Us[o - 1], uc = Us[o], ur = Us[o + 1];
+        const float2 l2[2] = {make_float2(ul.x, ul.y), make_float2(ul.z, ul.w)};
+        const float2 c2[2] = {make_float2(uc.x, uc.y), make_float2(uc.z, uc.w)};
+        const float2 r2[2] = {make_float2(ur.x, ur.y), make_float2(ur.z, ur.w)};
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const int qq = (NP == 1) ? 0 : q;
+            dwin[t % 3][q] = __ffma2_rn(l2[qq], l2[qq], __fmul2_rn(r2[qq], r2[qq]));
+            cwin[t % 3][q] = __fmul2_rn(c2[qq], c2[qq]);
+        }
+        if (t >= 2) {
+            const int r = t - 2;  // rows t-2, t-1, t = r, r+1, r+2 around target row r+1
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const float2 E = __fadd2_rn(dwin[(t - 1) % 3][q], __fadd2_rn(cwin[(t - 2) % 3][q], cwin[t % 3][q]));
+                const float2 K = __fadd2_rn(dwin[(t - 2) % 3][q], dwin[t % 3][q]);
+                const float2 Sv = __ffma2_rn(K, w22, E);
+                const float2 Rv = __ffma2_rn(K, w32, __ffma2_rn(E, w22, cwin[(t - 1) % 3][q]));
+                if (MODE == 0) {
+                    S[r][q] = Sv;
+                    R[r][q] = Rv;
+                } else {  // S = Pc, R = Rc (carried)
+                    Fn[r][q] = __fadd2_rn(S[r][q], Rv);
+                    S[r][q] = __fadd2_rn(R[r][q], Sv);
+                    R[r][q] = Rv;
+                }
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
 // Stencil step (lambda, xi arbitrary): the hot kernel.
 //   thread (tx, ty): x = x0 + tx, rows y0 + ty*kRY + r (r < kRY) of plane z.
-//   Per plane it streams the 9 (dx, dz) columns of kRY+2 haloed rows from
-//   shared memory; each loaded neighbour row updates up to 3 of the thread's
-//   voxels.  Per (neighbour, voxel) pair: one FADD (g, Eq. 6) and, per cluster
-//   pair, one FFMA2 for the Eq. 5 numerator and one for the Eq. 7 class sum.
+//   Eq. 5: per plane the thread streams the 9 (dx, dz) columns of kRY+2
+//   haloed rows from shared memory; each loaded neighbour row updates up to 3
+//   of its voxels: g (Eq. 6) for two voxels per FADD2, one FFMA2 per cluster
+//   pair for the numerator.  Eq. 7: the separable in-plane sums S, R of the
+//   newest plane (plane_SR), carried across the z march.
 //   Planes arrive by TMA into a 4-stage ring (full barriers); each warp
 //   releases a stage on its empty barrier, so warps are not lock-stepped.
 template <int C, bool M2, bool DU>
-__global__ void __launch_bounds__(kStepThreads, 4)
+__global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     k_step_stencil(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
                    const StepArgs a) {
     constexpr int NP = (C + 1) / 2;  // cluster pairs (FFMA2 lanes)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *base = smem_raw;  // >= 16-byte aligned: enough for non-swizzled TMA boxes
     auto sUst = [&](int s) { return reinterpret_cast<float4 *>(base + s * kUStagePad); };
-    auto sXst = [&](int s) { return reinterpret_cast<float *>(base + kStages * kUStagePad + s * kXStagePad); };
-    __shared__ __align__(8) uint64_t full[kStages];
-    __shared__ __align__(8) uint64_t empty[kStages];
+    auto sXst = [&](int s) { return reinterpret_cast<float *>(base + kRing * kUStagePad + s * kXStagePad); };
+    __shared__ __align__(8) uint64_t full[kRing];
+    __shared__ int released[kRing];
 
     const int p = blockIdx.z;
     if (a.stop && *a.stop) return;
@@ -326,35 +435,33 @@ __global__ void __launch_bounds__(kStepThreads, 4)
     const int slot = a.in_idx ? a.in_idx[p] : p;
 
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kRing; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWarpsY);
+            released[s] = 0;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     // TMA of plane q (q may lie outside [0, nz): the box is zero-filled).  The
-    // tensor maps are used through their kernel-parameter addresses.
+    // tensor maps are used through their kernel-parameter addresses.  A stage
+    // is refilled (with plane q + kRing) by the last warp that releases it.
     const CUtensorMap *pmU = &tmU, *pmX = &tmX;
 #define PIFCM_ISSUE_PLANE(q_)                                                        \
     do {                                                                             \
         const int l_ = (q_) - (zb - 1);                                              \
-        const int s_ = l_ & (kStages - 1);                                           \
-        if (l_ >= kStages) mbar_wait(&empty[s_], ((l_ >> 2) - 1) & 1);               \
+        const int s_ = l_ % kRing;                                                   \
         mbar_expect_tx(&full[s_], kUStageBytes + kXStageBytes);                      \
-        tma_load_5d(sUst(s_), pmU, &full[s_], 0, x0 - 1, y0 - 1, (q_), slot);        \
+        tma_load_4d(sUst(s_), pmU, &full[s_], 4 * (x0 - 1), y0 - 1, (q_), slot);     \
         tma_load_3d(sXst(s_), pmX, &full[s_], x0 - kXOff, y0 - 1, (q_));            \
     } while (0)
     auto wait_plane = [&](int q) {
         const int l = q - (zb - 1);
-        mbar_wait(&full[l & (kStages - 1)], (l >> 2) & 1);
+        mbar_wait(&full[l % kRing], (l / kRing) & 1);
     };
 
     if (tid == 0) {
-        PIFCM_ISSUE_PLANE(zb - 1);
-        PIFCM_ISSUE_PLANE(zb);
-        if (zb + 1 <= ze) PIFCM_ISSUE_PLANE(zb + 1);
+        for (int q = zb - 1; q <= min(zb + kRing - 2, ze); ++q) PIFCM_ISSUE_PLANE(q);
     }
 
     float4 *Uout = a.U_out + (long long)(a.out_idx ? a.out_idx[p] : p) * a.nvox;
@@ -379,17 +486,38 @@ __global__ void __launch_bounds__(kStepThreads, 4)
         invQi[r] = 1.0f / Qs;
     }
 
+    // rows of this thread that lie inside the volume, and their output row base
+    unsigned vmask = 0u;
+#pragma unroll
+    for (int r = 0; r < kRY; ++r)
+        if (gx < a.nx && y0 + ty * kRY + r < a.ny) vmask |= 1u << r;
+    float4 *Urow = Uout + (long long)(y0 + ty * kRY) * a.nx + gx;
+
     float2 num2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     float2 den2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     float Jacc = 0.f, duacc = 0.f;
 
+    // Eq. 7 carried sums: Pc = R(z-1) + S(z), Rc = R(z)
+    float2 Pc[kRY][NP], Rc[kRY][NP];
     wait_plane(zb - 1);
     wait_plane(zb);
+    {
+        float2 S0[kRY][NP], R0[kRY][NP], S1[kRY][NP], R1[kRY][NP], dummy[kRY][NP];
+        plane_SR<NP, 0>(sUst(0), ty, tx, w22, w32, S0, R0, dummy);  // plane zb-1 (local index 0)
+        plane_SR<NP, 0>(sUst(1), ty, tx, w22, w32, S1, R1, dummy);  // plane zb
+#pragma unroll
+        for (int r = 0; r < kRY; ++r)
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                Pc[r][q] = __fadd2_rn(R0[r][q], S1[r][q]);
+                Rc[r][q] = R1[r][q];
+            }
+    }
+
     for (int z = zb; z < ze; ++z) {
-        if (tid == 0 && z + 2 <= ze) PIFCM_ISSUE_PLANE(z + 2);
         wait_plane(z + 1);
         const int lz = z - (zb - 1);
-        const int sm = (lz - 1) & (kStages - 1), sc = lz & (kStages - 1), sp = (lz + 1) & (kStages - 1);
+        const int sm = (lz - 1) % kRing, sc = lz % kRing, sp = (lz + 1) % kRing;
         const float4 *Um = sUst(sm), *Uc = sUst(sc), *Up = sUst(sp);
         const float *Xm = sXst(sm), *Xc = sXst(sc), *Xp = sXst(sp);
 
@@ -397,17 +525,12 @@ __global__ void __launch_bounds__(kStepThreads, 4)
 #pragma unroll
         for (int r = 0; r < kRY; ++r) xr[r] = Xc[(ty * kRY + 1 + r) * kSXP + tx + kXOff];
 
-        float2 hn[kRY][NP], fa[kRY][3][NP];
+        // ---- Eq. 5 numerators
+        float2 hn[kRY][NP];
 #pragma unroll
         for (int r = 0; r < kRY; ++r)
 #pragma unroll
-            for (int q = 0; q < NP; ++q) {
-                hn[r][q] = make_float2(0.f, 0.f);
-                fa[r][0][q] = make_float2(0.f, 0.f);
-                fa[r][1][q] = make_float2(0.f, 0.f);
-                fa[r][2][q] = make_float2(0.f, 0.f);
-            }
-
+            for (int q = 0; q < NP; ++q) hn[r][q] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int dz = -1; dz <= 1; ++dz) {
             const float4 *Us = dz < 0 ? Um : (dz == 0 ? Uc : Up);
@@ -419,67 +542,90 @@ __global__ void __launch_bounds__(kStepThreads, 4)
                     const float4 uk4 = Us[(ty * kRY + t) * kSX + tx + 1 + dx];
                     const float xk = Xs[(ty * kRY + t) * kSXP + tx + kXOff + dx];
                     const float2 u01 = make_float2(uk4.x, uk4.y), u23 = make_float2(uk4.z, uk4.w);
+                    // g_ik (Eq. 6) for the voxels this row touches, two per FADD2
+                    float gv[kRY];
+#pragma unroll
+                    for (int r = 0; r < kRY; r += 2) {
+                        const int dy0 = t - 1 - r, dy1 = t - 2 - r;
+                        const bool v0 = dy0 >= -1 && dy0 <= 1 && !(dx == 0 && dy0 == 0 && dz == 0);
+                        const bool v1 = dy1 >= -1 && dy1 <= 1 && !(dx == 0 && dy1 == 0 && dz == 0);
+                        if (v0 && v1) {
+                            const float2 d = __fadd2_rn(make_float2(xr[r], xr[r + 1]), make_float2(-xk, -xk));
+                            gv[r] = d.x;
+                            gv[r + 1] = d.y;
+                        } else if (v0) {
+                            gv[r] = xr[r] - xk;
+                        } else if (v1) {
+                            gv[r + 1] = xr[r + 1] - xk;
+                        }
+                    }
 #pragma unroll
                     for (int r = 0; r < kRY; ++r) {
                         const int dy = t - 1 - r;
                         if (dy < -1 || dy > 1) continue;
                         if (dx == 0 && dy == 0 && dz == 0) continue;  // Eq. 9: k != i
-                        const int cls = (dx != 0) + (dy != 0) + (dz != 0) - 1;
-                        const float g = fabsf(xr[r] - xk);          // Eq. 6
+                        const float g = fabsf(gv[r]);
                         const float2 g2 = make_float2(g, g);
-                        hn[r][0] = __ffma2_rn(u01, g2, hn[r][0]);            // Eq. 5 numerator
-                        fa[r][cls][0] = __ffma2_rn(u01, u01, fa[r][cls][0]);  // Eq. 7 class sums
-                        if (NP > 1) {
-                            hn[r][NP - 1] = __ffma2_rn(u23, g2, hn[r][NP - 1]);
-                            fa[r][cls][NP - 1] = __ffma2_rn(u23, u23, fa[r][cls][NP - 1]);
-                        }
+                        hn[r][0] = __ffma2_rn(u01, g2, hn[r][0]);                 // Eq. 5 numerator
+                        if (NP > 1) hn[r][NP - 1] = __ffma2_rn(u23, g2, hn[r][NP - 1]);
                     }
                 }
             }
         }
 
+        // ---- Eq. 7 numerators: Fn(z) = Pc + R(z+1); carry Pc = R(z) + S(z+1), Rc = R(z+1)
+        float2 Fn[kRY][NP];
+        plane_SR<NP, 1>(Up, ty, tx, w22, w32, Pc, Rc, Fn);
+
+        // ---- per-voxel epilogue: Eq. 5 / 7 ratios, Eq. 4, Eq. 2, partial sums
+        float invQ[kRY];
         const int pz = (z > 0) + (z < a.nz - 1);
-        unsigned band_bits = 0u;
+        if (pz == 2) {
 #pragma unroll
-        for (int r = 0; r < kRY; ++r) {
-            const int gy = y0 + ty * kRY + r;
-            if (gx >= a.nx || gy >= a.ny) continue;
-            float invQ = invQi[r];
-            if (pz != 2) {
+            for (int r = 0; r < kRY; ++r) invQ[r] = invQi[r];
+        } else {  // first / last plane: fewer in-bounds neighbours (Eq. 7 denominator)
+#pragma unroll
+            for (int r = 0; r < kRY; ++r) {
+                const int gy = y0 + ty * kRY + r;
                 const int py = (gy > 0) + (gy < a.ny - 1);
                 const float Qs = (float)(px + py + pz) + w2 * (float)(px * py + py * pz + pz * px) +
                                  w3 * (float)(px * py * pz);
-                invQ = Qs > 0.f ? 1.0f / Qs : 0.f;
+                invQ[r] = Qs > 0.f ? 1.0f / Qs : 0.f;
             }
+        }
+        float4 *Uz = Urow + (long long)z * plane;
+        unsigned band_bits = 0u;
+#pragma unroll
+        for (int r = 0; r < kRY; ++r) {
             float G = hn[r][0].x + hn[r][0].y;
             if (C > 2) G += hn[r][NP - 1].x;
             if (C > 3) G += hn[r][NP - 1].y;  // = sum_k g_ik (rows of U sum to 1)
             const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
-            float2 A[2];
-            bool band = false;
+            float2 A[2], Ar[2];
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
-                const float2 H = __fmul2_rn(hn[r][q], make_float2(invG, invG));                 // Eq. 5
-                const float2 F = __fmul2_rn(__ffma2_rn(fa[r][2][q], w32, __ffma2_rn(fa[r][1][q], w22, fa[r][0][q])),
-                                            make_float2(invQ, invQ));                            // Eq. 7
-                A[q] = __ffma2_rn(H, nlam2, __ffma2_rn(F, nxi2, make_float2(1.f, 1.f)));         // Eq. 4
-                band |= (A[q].x > -kBandLo) && (A[q].x < kBandHi);
-                if (2 * q + 1 < C) band |= (A[q].y > -kBandLo) && (A[q].y < kBandHi);
-                A[q].x = fmaxf(A[q].x, kAFloor);                                                  // R4
-                A[q].y = fmaxf(A[q].y, kAFloor);
+                const float2 H = __fmul2_rn(hn[r][q], make_float2(invG, invG));          // Eq. 5
+                const float2 F = __fmul2_rn(Fn[r][q], make_float2(invQ[r], invQ[r]));    // Eq. 7
+                Ar[q] = __ffma2_rn(H, nlam2, __ffma2_rn(F, nxi2, make_float2(1.f, 1.f))); // Eq. 4
+                A[q].x = fmaxf(Ar[q].x, kAFloor);                                          // R4
+                A[q].y = fmaxf(Ar[q].y, kAFloor);
             }
-            if (NP == 1) A[1] = make_float2(1.f, 1.f);
-            if (band) {  // deferred to the warp-cooperative fp64 pass below
-                band_bits |= 1u << r;
-                continue;
+            if (NP == 1) { A[1] = make_float2(1.f, 1.f); Ar[1] = A[1]; }
+            const Memb mb = memb_compute<C, M2>(xr[r], c2, A, a.m, a.inv_m1, Ar);
+            const bool valid = (vmask >> r) & 1u;
+            const bool band = valid && !(mb.K <= kKMax);  // ill-conditioned: fp64 pass below
+            band_bits |= band ? (1u << r) : 0u;
+            const bool ok = valid && !band;
+            const float4 un = make_float4(mb.u[0], mb.u[1], mb.u[2], mb.u[3]);
+            if (ok) {
+                memb_accumulate<C, M2>(mb, xr[r], a.m, num2, den2, Jacc);
+                if (DU) {
+                    const float4 uo = Uc[(ty * kRY + 1 + r) * kSX + tx + 1];
+                    duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
+                                               fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
+                }
+                Uz[(long long)r * a.nx] = un;
             }
-            const float4 un = membership2<C, M2>(xr[r], c2, A, a.m, a.inv_m1, num2, den2, Jacc);
-            if (DU) {
-                const float4 uo = Uc[(ty * kRY + 1 + r) * kSX + tx + 1];
-                duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
-                                           fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
-            }
-            Uout[(long long)z * plane + (long long)gy * a.nx + gx] = un;
         }
 
         // Ill-conditioned voxels of this warp, one at a time, all lanes together.
@@ -508,9 +654,16 @@ __global__ void __launch_bounds__(kStepThreads, 4)
                 }
             }
         }
-        // this warp no longer needs plane z-1
+        // this warp no longer needs plane z-1; the last warp to release its
+        // stage refills it with plane z-1+kRing
         __syncwarp();
-        if (tx == 0) mbar_arrive(&empty[sm]);
+        if (tx == 0) {
+            const int old = atomicAdd(&released[sm], 1);
+            if (old == kWarpsY - 1) {
+                released[sm] = 0;
+                if (z - 1 + kRing <= ze) PIFCM_ISSUE_PLANE(z - 1 + kRing);
+            }
+        }
     }
 #undef PIFCM_ISSUE_PLANE
 
@@ -583,11 +736,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 static bool make_maps(const StepArgs &a, CUtensorMap *mU, CUtensorMap *mX) {
     auto enc = encode_fn();
     if (!enc) return false;
-    const cuuint64_t du[5] = {4, (cuuint64_t)a.nx, (cuuint64_t)a.ny, (cuuint64_t)a.nz, (cuuint64_t)a.n_in_states};
-    const cuuint64_t su[4] = {16, 16ull * a.nx, 16ull * a.nx * a.ny, 16ull * (cuuint64_t)a.nvox};
-    const cuuint32_t bu[5] = {4, kSX, kSY, 1, 1};
+    // innermost dimension = whole AoS rows (4 * nx floats) so that every box
+    // row is one contiguous 544-byte burst
+    const cuuint64_t du[4] = {4ull * a.nx, (cuuint64_t)a.ny, (cuuint64_t)a.nz, (cuuint64_t)a.n_in_states};
+    const cuuint64_t su[3] = {16ull * a.nx, 16ull * a.nx * a.ny, 16ull * (cuuint64_t)a.nvox};
+    const cuuint32_t bu[4] = {4 * kSX, kSY, 1, 1};
     const cuuint32_t e5[5] = {1, 1, 1, 1, 1};
-    if (enc(mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float4 *>(a.U_in), du, su, bu, e5,
+    if (enc(mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float4 *>(a.U_in), du, su, bu, e5,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;

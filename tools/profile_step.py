@@ -23,7 +23,7 @@ ws = ctx.workspace(nx, ny, nz, cfg, pso)
 vt = torch.as_tensor(vol, device="cuda:0")
 if mode == "segment":
     ctx.segment(vt, cfg, pso, ws=ws)
-else:
+if mode in ("eval", "time"):
     x, hist = ctx.normalize_u8(vt)
     c0 = ctx.gmm_init(hist, 4)
     U0 = torch.full((nz * ny * nx, 4), 0.25, device="cuda:0")
@@ -33,3 +33,12 @@ else:
         ctx.pso_step(g, cfg, pso, x, ws)
 torch.cuda.synchronize()
 print("done")
+
+if mode == "time":
+    # device time of the fused step at P=32 (C3), CUDA events on the launch stream
+    ctx.timing_enable(True)
+    for _ in range(10):
+        ctx.pso_step(g, cfg, pso, x, ws)
+    ms, n, b = ctx.timing_read()
+    print(f"fused step: {ms / n:.3f} ms/launch, {b / n / 1e9:.3f} GB alg/launch, "
+          f"{(b / n) / (ms / n * 1e-3) / 1e9:.1f} GB/s, {32 * nz * ny * nx / (ms / n * 1e-3) / 1e9:.1f} G vp/s")
