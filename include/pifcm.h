@@ -278,11 +278,14 @@ int64_t pifcm_launch_count(const pifcm_ctx *ctx);
 /* Device timing of the fused step kernel: when enabled (which resets the
  * counters), every launch of the neighbourhood (stencil) step kernel is
  * bracketed by CUDA events on its stream.  pifcm_timing_read synchronises
- * those events and returns the summed kernel time in ms, the number of
- * launches, and their algorithmic bytes (per launch: P * nvox * 32 bytes of
+ * those events and returns, for the batched launches (batched = 1: P > 1
+ * states per launch, i.e. the PSO generations) or the single-state launches
+ * (batched = 0: the final IFCM), the summed kernel time in ms, the number of
+ * launches and their algorithmic bytes (per launch: P * nvox * 32 bytes of
  * AoS-C4 membership read + write, plus nvox * 4 bytes of intensities). */
 int pifcm_timing_enable(pifcm_ctx *ctx, int32_t on);
-int pifcm_timing_read(pifcm_ctx *ctx, double *ms_total, int64_t *launches, double *alg_bytes);
+int pifcm_timing_read(pifcm_ctx *ctx, int32_t batched, double *ms_total, int64_t *launches,
+                      double *alg_bytes);
 
 #ifdef __cplusplus
 }

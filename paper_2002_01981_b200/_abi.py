@@ -61,7 +61,7 @@ SIGNATURES = {
     "pifcm_last_error": (ct.c_char_p, [_vp]),
     "pifcm_launch_count": (ct.c_int64, [_vp]),
     "pifcm_timing_enable": (ct.c_int, [_vp, ct.c_int32]),
-    "pifcm_timing_read": (ct.c_int, [_vp, ct.POINTER(ct.c_double), ct.POINTER(ct.c_int64),
+    "pifcm_timing_read": (ct.c_int, [_vp, ct.c_int32, ct.POINTER(ct.c_double), ct.POINTER(ct.c_int64),
                                      ct.POINTER(ct.c_double)]),
     "pifcm_workspace_size": (ct.c_int, [_G, _C, _P, ct.POINTER(ct.c_size_t)]),
     "pifcm_iterate_workspace_size": (ct.c_int, [_G, _C, ct.c_int32, ct.c_int32, ct.POINTER(ct.c_size_t)]),

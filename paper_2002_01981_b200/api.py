@@ -153,10 +153,12 @@ class Context:
     def timing_enable(self, on: bool = True):
         self._ck(self.lib.pifcm_timing_enable(self._h, 1 if on else 0))
 
-    def timing_read(self):
-        """-> (summed fused-step kernel ms, launches, algorithmic bytes)."""
+    def timing_read(self, batched: bool = True):
+        """-> (summed fused-step kernel ms, launches, algorithmic bytes) of the
+        batched (P > 1, PSO generations) or single-state launches."""
         ms, n, b = ct.c_double(), ct.c_int64(), ct.c_double()
-        self._ck(self.lib.pifcm_timing_read(self._h, ct.byref(ms), ct.byref(n), ct.byref(b)))
+        self._ck(self.lib.pifcm_timing_read(self._h, 1 if batched else 0, ct.byref(ms), ct.byref(n),
+                                            ct.byref(b)))
         return ms.value, n.value, b.value
 
     # ------------------------------------------------------------ workspace

@@ -22,9 +22,10 @@ struct pifcm_ctx {
     // fused-step timing (pifcm_timing_*)
     bool timing = false;
     std::vector<cudaEvent_t> tev;   // pairs (start, stop)
+    std::vector<int> tcls;          // class of each pair: 0 batched (P > 1), 1 single state
     size_t tused = 0;               // events in use
-    double t_ms = 0.0, t_bytes = 0.0, pend_bytes = 0.0;
-    long long t_launches = 0;
+    double t_ms[2] = {0.0, 0.0}, t_bytes[2] = {0.0, 0.0};
+    long long t_launches[2] = {0, 0};
 };
 
 namespace {
@@ -200,9 +201,12 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     LAUNCH(ctx, 1, launch_step(a, cfg->C, stencil, P, st));
     if (timed) {
         CK(ctx, cudaEventRecord(ctx->tev[ctx->tused + 1], st));
+        const int cls = P > 1 ? 0 : 1;
+        if (ctx->tcls.size() < ctx->tused / 2 + 1) ctx->tcls.resize(ctx->tused / 2 + 1);
+        ctx->tcls[ctx->tused / 2] = cls;
         ctx->tused += 2;
-        ctx->pend_bytes += 32.0 * (double)a.nvox * P + 4.0 * (double)a.nvox;
-        ctx->t_launches += 1;
+        ctx->t_bytes[cls] += 32.0 * (double)a.nvox * P + 4.0 * (double)a.nvox;
+        ctx->t_launches[cls] += 1;
     }
     FinalizeArgs f{};
     f.partials = partials;
@@ -262,11 +266,9 @@ static int timing_drain(pifcm_ctx *ctx) {
         CK(ctx, cudaEventSynchronize(ctx->tev[i + 1]));
         float ms = 0.f;
         CK(ctx, cudaEventElapsedTime(&ms, ctx->tev[i], ctx->tev[i + 1]));
-        ctx->t_ms += ms;
+        ctx->t_ms[ctx->tcls[i / 2]] += ms;
     }
     ctx->tused = 0;
-    ctx->t_bytes += ctx->pend_bytes;
-    ctx->pend_bytes = 0.0;
     return PIFCM_OK;
 }
 
@@ -275,19 +277,22 @@ int pifcm_timing_enable(pifcm_ctx *ctx, int32_t on) {
     int r = timing_drain(ctx);
     if (r) return r;
     ctx->timing = on != 0;
-    ctx->t_ms = 0.0;
-    ctx->t_bytes = 0.0;
-    ctx->t_launches = 0;
+    for (int c = 0; c < 2; ++c) {
+        ctx->t_ms[c] = 0.0;
+        ctx->t_bytes[c] = 0.0;
+        ctx->t_launches[c] = 0;
+    }
     return PIFCM_OK;
 }
 
-int pifcm_timing_read(pifcm_ctx *ctx, double *ms_total, int64_t *launches, double *alg_bytes) {
-    if (!ctx) return PIFCM_EINVAL;
+int pifcm_timing_read(pifcm_ctx *ctx, int32_t batched, double *ms_total, int64_t *launches, double *alg_bytes) {
+    if (!ctx || batched < 0 || batched > 1) return PIFCM_EINVAL;
     int r = timing_drain(ctx);
     if (r) return r;
-    if (ms_total) *ms_total = ctx->t_ms;
-    if (launches) *launches = ctx->t_launches;
-    if (alg_bytes) *alg_bytes = ctx->t_bytes;
+    const int c = batched ? 0 : 1;
+    if (ms_total) *ms_total = ctx->t_ms[c];
+    if (launches) *launches = ctx->t_launches[c];
+    if (alg_bytes) *alg_bytes = ctx->t_bytes[c];
     return PIFCM_OK;
 }
 

@@ -1,0 +1,224 @@
+"""Particle-sharded PSO-3DPIFCM across ranks (one process per GPU).
+
+The PSO of Alg. 1 steps 3-9 evaluates every particle
+independently (the fitness of particle p is one IFCM step of its own state at
+its own (lambda, xi), CHAINED reading R11), so the particles are sharded over
+ranks: rank r owns particles [p0, p1) and their membership states.  The only
+exchanges are
+  * an all-gather of the per-particle fitness (P doubles) every generation,
+    after which every rank runs the same deterministic PSO update (so no
+    positions are exchanged), and
+  * a broadcast of the gbest state (its U and centres, Alg. 1 step 10) from
+    the rank that owns the gbest particle, before the final IFCM (step 11).
+The collectives go through torch.distributed (NCCL on GPUs); every compute
+step runs in libpifcm.so.  The PSO loop is written against a small engine
+interface so the sharding logic can be exercised on CPU (gloo) in tests.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+__all__ = ["shard_range", "allgather_fitness", "ShardedPso", "GpuPsoEngine", "ShardedSegmenter"]
+
+
+def shard_range(P: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, as-even-as-possible split of P particles over `world` ranks
+    (20 over 8 -> 3,3,3,3,2,2,2,2)."""
+    base, rem = divmod(P, world)
+    p0 = rank * base + min(rank, rem)
+    return p0, p0 + base + (1 if rank < rem else 0)
+
+
+def allgather_fitness(dist, local: torch.Tensor, P: int, world: int) -> torch.Tensor:
+    """All-gather the fp64 fitness of every rank's particle range into [P]
+    (rank order = particle order).  Uneven ranges are padded to the largest."""
+    if world == 1:
+        return local.clone()
+    maxl = -(-P // world)
+    dev = local.device
+    cpu_coll = dist.get_backend() == "gloo" and dev.type == "cuda"
+    buf = torch.zeros(maxl, dtype=torch.float64, device="cpu" if cpu_coll else dev)
+    buf[: local.numel()] = local.to(buf.device)
+    out = torch.empty(world * maxl, dtype=torch.float64, device=buf.device)
+    dist.all_gather_into_tensor(out, buf)
+    parts = []
+    for r in range(world):
+        a, b = shard_range(P, world, r)
+        parts.append(out[r * maxl: r * maxl + (b - a)])
+    return torch.cat(parts).to(dev)
+
+
+def broadcast_(dist, t: torch.Tensor, src: int):
+    """Broadcast in place (through host memory when gloo carries CUDA tensors)."""
+    if dist.get_backend() == "gloo" and t.device.type == "cuda":
+        h = t.cpu()
+        dist.broadcast(h, src=src)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, src=src)
+
+
+@dataclass
+class PsoOutcome:
+    lam: float
+    xi: float
+    J: float
+    generations: int
+    gbest_particle: int
+
+
+class ShardedPso:
+    """Generation loop of Alg. 1 steps 4-9 over sharded particles.
+
+    engine must provide: init(p0, p1); eval(); local_fitness() -> Tensor[p1-p0];
+    set_fitness(Tensor[P]); update(); summary() -> (PsoOutcome, stopped)."""
+
+    def __init__(self, engine, P: int, dist=None, check_every: int = 4):
+        self.engine = engine
+        self.P = P
+        self.dist = dist
+        self.world = dist.get_world_size() if dist is not None else 1
+        self.rank = dist.get_rank() if dist is not None else 0
+        self.p0, self.p1 = shard_range(P, self.world, self.rank)
+        self.check_every = check_every
+
+    def run(self, max_gen: int, early_stop: bool) -> PsoOutcome:
+        e = self.engine
+        e.init(self.p0, self.p1)
+        for gen in range(max_gen):
+            e.eval()
+            full = allgather_fitness(self.dist, e.local_fitness(), self.P, self.world)
+            e.set_fitness(full)
+            e.update()
+            if early_stop and (gen + 1) % self.check_every == 0:
+                _, stopped = e.summary()
+                if stopped:
+                    break
+        out, _ = e.summary()
+        return out
+
+    def owner_of(self, particle: int) -> int:
+        for r in range(self.world):
+            a, b = shard_range(self.P, self.world, r)
+            if a <= particle < b:
+                return r
+        raise ValueError(particle)
+
+
+class GpuPsoEngine:
+    """ShardedPso engine over libpifcm.so (pifcm_pso_init/eval/update)."""
+
+    def __init__(self, ctx, grid, cfg, pso, x, U0, c0):
+        self.ctx, self.grid, self.cfg, self.pso0 = ctx, grid, cfg, pso
+        self.x, self.U0, self.c0 = x, U0, c0
+        self.ws = None
+
+    def init(self, p0, p1):
+        from dataclasses import replace
+        self.pso = replace(self.pso0, p_begin=p0, p_end=p1)
+        if p0 == 0 and p1 == self.pso.P:
+            self.pso = replace(self.pso, p_begin=0, p_end=0)
+        self.p0, self.p1 = p0, p1
+        g = self.grid
+        n = self.ctx.workspace_size(g.nx, g.ny, g.nz, self.cfg, self.pso)
+        if self.ws is None or self.ws.numel() < n:
+            self.ws = torch.empty(n, dtype=torch.uint8, device=self.x.device)
+        self.ctx.pso_init(g, self.cfg, self.pso, self.U0, self.c0, self.ws)
+        self.fit = self.ctx.pso_fitness(g, self.cfg, self.pso, self.ws)
+
+    def eval(self):
+        self.ctx.pso_eval(self.grid, self.cfg, self.pso, self.x, self.ws)
+
+    def local_fitness(self):
+        return self.fit[self.p0:self.p1]
+
+    def set_fitness(self, full):
+        self.fit.copy_(full)
+
+    def update(self):
+        self.ctx.pso_update(self.grid, self.cfg, self.pso, self.ws)
+
+    def summary(self):
+        s, stopped = self.ctx.pso_result(self.grid, self.cfg, self.pso, self.ws)
+        return PsoOutcome(s.lam, s.xi, s.J, s.generations, s.gbest_particle), stopped
+
+    def gbest_state(self, U_out, c_out):
+        self.ctx.pso_gbest_state(self.grid, self.cfg, self.pso, self.ws, U_out, c_out)
+
+
+class ShardedSegmenter:
+    """pifcm_segment with the PSO particles sharded over the ranks of `dist`.
+
+    Every rank normalises, fits the GMM and runs the FCM start (identical,
+    deterministic), the PSO generations are sharded, the gbest state is
+    broadcast from its owner and every rank runs the final IFCM and argmax.
+    Labels are bit-identical to the single-process pifcm_segment."""
+
+    def __init__(self, ctx, cfg, pso, shape, dist=None):
+        self.ctx, self.cfg, self.pso = ctx, cfg, pso
+        self.nz, self.ny, self.nx = shape
+        self.dist = dist
+        self.dev = torch.device(f"cuda:{ctx.device}")
+        nvox = self.nx * self.ny * self.nz
+        self.Ub = torch.empty((1, nvox, 4), dtype=torch.float32, device=self.dev)
+        self.Ua = torch.zeros((1, nvox, 4), dtype=torch.float32, device=self.dev)
+        self.cen = torch.empty((1, 4), dtype=torch.float32, device=self.dev)
+        self.engine = None
+
+    def segment(self, vol: torch.Tensor) -> dict:
+        from .api import _grid
+        ctx, cfg = self.ctx, self.cfg
+        nz, ny, nx = self.nz, self.ny, self.nx
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record()
+        # Alg. 2 step 1 + Alg. 1 step 2: normalise, GMM, FCM start (lambda = xi = 0)
+        x, hist = ctx.normalize_u8(vol)
+        c0 = ctx.gmm_init(hist, cfg.C)
+        ev[1].record()
+        self.cen.copy_(c0.view(1, 4))
+        self.Ua.zero_()
+        zero = torch.zeros((1, 2), dtype=torch.float64, device=self.dev)
+        stats = torch.zeros((1, 4), dtype=torch.float64, device=self.dev)
+        ctx.iterate(x, self.Ua, self.Ub, self.cen, zero, cfg, iters=cfg.max_iter, stats=stats, nx=nx)
+        fcm_iters = int(stats[0, 2].item())
+        ev[2].record()
+        # Alg. 1 steps 3-10: sharded PSO from (U_fcm, c_fcm)
+        g = _grid(nx, ny, nz)
+        U0 = self.Ub[0]
+        c_fcm = self.cen[0].clone()
+        self.engine = GpuPsoEngine(ctx, g, cfg, self.pso, x, U0, c_fcm)
+        runner = ShardedPso(self.engine, self.pso.P, self.dist)
+        out = runner.run(self.pso.max_gen, early_stop=self.pso.patience > 0)
+        # Alg. 1 step 10: gbest state from its owner
+        owner = runner.owner_of(out.gbest_particle)
+        if runner.rank == owner:
+            self.engine.gbest_state(self.Ua[0], self.cen[0])
+        if self.dist is not None and runner.world > 1:
+            broadcast_(self.dist, self.Ua, owner)
+            broadcast_(self.dist, self.cen, owner)
+        ev[3].record()
+        # Alg. 1 step 11: final IFCM at (lambda*, xi*) until eps, then argmax
+        lx = torch.tensor([[out.lam, out.xi]], dtype=torch.float64, device=self.dev)
+        stats.zero_()
+        ctx.iterate(x, self.Ua, self.Ub, self.cen, lx, cfg, iters=cfg.max_iter, stats=stats, nx=nx)
+        labels = ctx.argmax(self.Ub[0], nx, ny, nz, cfg.C)
+        ev[4].record()
+        final_iters = int(stats[0, 2].item())
+        torch.cuda.synchronize()
+        self.labels = labels
+        return {"lambda": out.lam, "xi": out.xi, "J": out.J, "generations": out.generations,
+                "gbest_particle": out.gbest_particle, "fcm_iters": fcm_iters,
+                "final_iters": final_iters, "centers": self.cen[0, :cfg.C].tolist(),
+                "t_norm": ev[0].elapsed_time(ev[1]) * 1e-3, "t_init": ev[1].elapsed_time(ev[2]) * 1e-3,
+                "t_pso": ev[2].elapsed_time(ev[3]) * 1e-3, "t_final": ev[3].elapsed_time(ev[4]) * 1e-3,
+                "t_total": ev[0].elapsed_time(ev[4]) * 1e-3}
+
+    def segment_host(self, vol_host: torch.Tensor, labels_host: torch.Tensor) -> dict:
+        """Host (pinned) u8 volume in, host labels out (H2D / D2H inside)."""
+        vol = vol_host.to(self.dev, non_blocking=True)
+        rep = self.segment(vol)
+        labels_host.copy_(self.labels, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return rep
