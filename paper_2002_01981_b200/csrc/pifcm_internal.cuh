@@ -40,7 +40,10 @@ constexpr int kTY = kWarpsY * kRY;  // 16
 constexpr int kSX = kTX + 2;        // haloed smem row length
 constexpr int kSY = kTY + 2;        // haloed smem rows
 constexpr int kStages = 4;          // plane ring: z-1, z, z+1 resident, z+2 landing
-constexpr int kTZ = 32;             // planes per CTA (z-chunk)
+#ifndef PIFCM_TZ
+#define PIFCM_TZ 32
+#endif
+constexpr int kTZ = PIFCM_TZ;       // planes per CTA (z-chunk)
 constexpr int kStepThreads = kTX * kWarpsY;
 
 // Pointwise (FCM, lambda = xi = 0) step.

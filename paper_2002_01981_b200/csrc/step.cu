@@ -525,57 +525,92 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
 #pragma unroll
         for (int r = 0; r < kRY; ++r) xr[r] = Xc[(ty * kRY + 1 + r) * kSXP + tx + kXOff];
 
-        // ---- Eq. 5 numerators
+        // ---- Eq. 5 numerators (and, on the z+1 plane, the Eq. 7 plane sums)
         float2 hn[kRY][NP];
 #pragma unroll
         for (int r = 0; r < kRY; ++r)
 #pragma unroll
             for (int q = 0; q < NP; ++q) hn[r][q] = make_float2(0.f, 0.f);
+        // one loaded neighbour row (column dx, plane dz, haloed row t): g_ik
+        // (Eq. 6) for the voxels it touches, two per FADD2, and the Eq. 5
+        // numerators, one FFMA2 per cluster pair
+        auto h_row = [&](const int dx, const int dz, const int t, const float4 uk4, const float xk) {
+            const float2 u01 = make_float2(uk4.x, uk4.y), u23 = make_float2(uk4.z, uk4.w);
+            float gv[kRY];
 #pragma unroll
-        for (int dz = -1; dz <= 1; ++dz) {
-            const float4 *Us = dz < 0 ? Um : (dz == 0 ? Uc : Up);
-            const float *Xs = dz < 0 ? Xm : (dz == 0 ? Xc : Xp);
+            for (int r = 0; r < kRY; r += 2) {
+                const int dy0 = t - 1 - r, dy1 = t - 2 - r;
+                const bool v0 = dy0 >= -1 && dy0 <= 1 && !(dx == 0 && dy0 == 0 && dz == 0);
+                const bool v1 = dy1 >= -1 && dy1 <= 1 && !(dx == 0 && dy1 == 0 && dz == 0);
+                if (v0 && v1) {
+                    const float2 d = __fadd2_rn(make_float2(xr[r], xr[r + 1]), make_float2(-xk, -xk));
+                    gv[r] = d.x;
+                    gv[r + 1] = d.y;
+                } else if (v0) {
+                    gv[r] = xr[r] - xk;
+                } else if (v1) {
+                    gv[r + 1] = xr[r + 1] - xk;
+                }
+            }
 #pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) {
+            for (int r = 0; r < kRY; ++r) {
+                const int dy = t - 1 - r;
+                if (dy < -1 || dy > 1) continue;
+                if (dx == 0 && dy == 0 && dz == 0) continue;  // Eq. 9: k != i
+                const float g = fabsf(gv[r]);
+                const float2 g2 = make_float2(g, g);
+                hn[r][0] = __ffma2_rn(u01, g2, hn[r][0]);                 // Eq. 5 numerator
+                if (NP > 1) hn[r][NP - 1] = __ffma2_rn(u23, g2, hn[r][NP - 1]);
+            }
+        };
 #pragma unroll
-                for (int t = 0; t < kRY + 2; ++t) {
-                    const float4 uk4 = Us[(ty * kRY + t) * kSX + tx + 1 + dx];
-                    const float xk = Xs[(ty * kRY + t) * kSXP + tx + kXOff + dx];
-                    const float2 u01 = make_float2(uk4.x, uk4.y), u23 = make_float2(uk4.z, uk4.w);
-                    // g_ik (Eq. 6) for the voxels this row touches, two per FADD2
-                    float gv[kRY];
+        for (int dz = -1; dz <= 0; ++dz) {
+            const float4 *Us = dz < 0 ? Um : Uc;
+            const float *Xs = dz < 0 ? Xm : Xc;
 #pragma unroll
-                    for (int r = 0; r < kRY; r += 2) {
-                        const int dy0 = t - 1 - r, dy1 = t - 2 - r;
-                        const bool v0 = dy0 >= -1 && dy0 <= 1 && !(dx == 0 && dy0 == 0 && dz == 0);
-                        const bool v1 = dy1 >= -1 && dy1 <= 1 && !(dx == 0 && dy1 == 0 && dz == 0);
-                        if (v0 && v1) {
-                            const float2 d = __fadd2_rn(make_float2(xr[r], xr[r + 1]), make_float2(-xk, -xk));
-                            gv[r] = d.x;
-                            gv[r + 1] = d.y;
-                        } else if (v0) {
-                            gv[r] = xr[r] - xk;
-                        } else if (v1) {
-                            gv[r + 1] = xr[r + 1] - xk;
-                        }
-                    }
+            for (int dx = -1; dx <= 1; ++dx)
 #pragma unroll
-                    for (int r = 0; r < kRY; ++r) {
-                        const int dy = t - 1 - r;
-                        if (dy < -1 || dy > 1) continue;
-                        if (dx == 0 && dy == 0 && dz == 0) continue;  // Eq. 9: k != i
-                        const float g = fabsf(gv[r]);
-                        const float2 g2 = make_float2(g, g);
-                        hn[r][0] = __ffma2_rn(u01, g2, hn[r][0]);                 // Eq. 5 numerator
-                        if (NP > 1) hn[r][NP - 1] = __ffma2_rn(u23, g2, hn[r][NP - 1]);
+                for (int t = 0; t < kRY + 2; ++t)
+                    h_row(dx, dz, t, Us[(ty * kRY + t) * kSX + tx + 1 + dx],
+                          Xs[(ty * kRY + t) * kSXP + tx + kXOff + dx]);
+        }
+        // plane z+1, row-major: the same loads feed Eq. 5 and the separable
+        // Eq. 7 sums of plane_SR (Fn(z) = Pc + R(z+1); Pc = R(z) + S(z+1);
+        // Rc = R(z+1)), so plane z+1 is read from shared memory once
+        float2 Fn[kRY][NP];
+        {
+            float2 dwin[3][NP], cwin[3][NP];
+#pragma unroll
+            for (int t = 0; t < kRY + 2; ++t) {
+                const int o = (ty * kRY + t) * kSX + tx + 1;
+                const int ox = (ty * kRY + t) * kSXP + tx + kXOff;
+                const float4 ul = Up[o - 1], uc = Up[o], ur = Up[o + 1];
+                h_row(-1, 1, t, ul, Xp[ox - 1]);
+                h_row(0, 1, t, uc, Xp[ox]);
+                h_row(1, 1, t, ur, Xp[ox + 1]);
+                const float2 l2[2] = {make_float2(ul.x, ul.y), make_float2(ul.z, ul.w)};
+                const float2 cc[2] = {make_float2(uc.x, uc.y), make_float2(uc.z, uc.w)};
+                const float2 r2[2] = {make_float2(ur.x, ur.y), make_float2(ur.z, ur.w)};
+#pragma unroll
+                for (int q = 0; q < NP; ++q) {
+                    dwin[t % 3][q] = __ffma2_rn(l2[q], l2[q], __fmul2_rn(r2[q], r2[q]));
+                    cwin[t % 3][q] = __fmul2_rn(cc[q], cc[q]);
+                }
+                if (t >= 2) {
+                    const int r = t - 2;
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        const float2 E = __fadd2_rn(dwin[(t - 1) % 3][q], __fadd2_rn(cwin[(t - 2) % 3][q], cwin[t % 3][q]));
+                        const float2 K = __fadd2_rn(dwin[(t - 2) % 3][q], dwin[t % 3][q]);
+                        const float2 Sv = __ffma2_rn(K, w22, E);
+                        const float2 Rv = __ffma2_rn(K, w32, __ffma2_rn(E, w22, cwin[(t - 1) % 3][q]));
+                        Fn[r][q] = __fadd2_rn(Pc[r][q], Rv);
+                        Pc[r][q] = __fadd2_rn(Rc[r][q], Sv);
+                        Rc[r][q] = Rv;
                     }
                 }
             }
         }
-
-        // ---- Eq. 7 numerators: Fn(z) = Pc + R(z+1); carry Pc = R(z) + S(z+1), Rc = R(z+1)
-        float2 Fn[kRY][NP];
-        plane_SR<NP, 1>(Up, ty, tx, w22, w32, Pc, Rc, Fn);
 
         // ---- per-voxel epilogue: Eq. 5 / 7 ratios, Eq. 4, Eq. 2, partial sums
         float invQ[kRY];
