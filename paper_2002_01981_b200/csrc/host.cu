@@ -114,8 +114,7 @@ Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg 
     if (pso) { P = pso->P; prange(pso, &p0, &Pl); }
     L.P = P; L.Pl = Pl; L.p0 = p0;
     L.nslots = 2 * Pl + 1;
-    const int nb_s = step_nblk(g->nx, g->ny, g->nz, true), nb_p = step_nblk(g->nx, g->ny, g->nz, false);
-    L.nblk = nb_s > nb_p ? nb_s : nb_p;
+    L.nblk = step_nblk_max(g->nx, g->ny, g->nz);
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
     L.x = take(sizeof(float) * (size_t)g->pitch * g->ny * g->nz);
@@ -210,7 +209,7 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     }
     FinalizeArgs f{};
     f.partials = partials;
-    f.nblk = step_nblk(g->nx, g->ny, g->nz, stencil);
+    f.nblk = step_nblk(g->nx, g->ny, g->nz, stencil, P);
     f.C = cfg->C; f.P = P; f.centers = centers; f.fitness = fitness; f.stats = stats;
     f.eps = eps; f.status = status; f.stop = stop;
     LAUNCH(ctx, 1, launch_finalize(f, st));
@@ -313,9 +312,7 @@ int pifcm_iterate_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *c
     if ((r = check_grid(nullptr, grid)) || (r = check_cfg(nullptr, cfg))) return r;
     if (P < 1 || iters < 1) return PIFCM_EINVAL;
     const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
-    const int nblk = step_nblk(grid->nx, grid->ny, grid->nz, true) > step_nblk(grid->nx, grid->ny, grid->nz, false)
-                         ? step_nblk(grid->nx, grid->ny, grid->nz, true)
-                         : step_nblk(grid->nx, grid->ny, grid->nz, false);
+    const int nblk = step_nblk_max(grid->nx, grid->ny, grid->nz);
     size_t b = align_up(sizeof(double) * kNR * (size_t)nblk * P, 256) +  // partials
                align_up(sizeof(double) * 4 * P, 256) + 256;              // stats scratch + status
     if (iters > 1) b += align_up(sizeof(float4) * (size_t)nvox * P, 256);
@@ -344,9 +341,7 @@ int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     CK(ctx, cudaSetDevice(ctx->device));
     const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
-    const int nblk = step_nblk(grid->nx, grid->ny, grid->nz, true) > step_nblk(grid->nx, grid->ny, grid->nz, false)
-                         ? step_nblk(grid->nx, grid->ny, grid->nz, true)
-                         : step_nblk(grid->nx, grid->ny, grid->nz, false);
+    const int nblk = step_nblk_max(grid->nx, grid->ny, grid->nz);
     size_t o = 0;
     double *partials = at<double>(ws, o); o = align_up(o + sizeof(double) * kNR * (size_t)nblk * P, 256);
     double *st_scr = at<double>(ws, o); o = align_up(o + sizeof(double) * 4 * P, 256);

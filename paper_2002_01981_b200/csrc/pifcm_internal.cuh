@@ -43,7 +43,8 @@ constexpr int kStages = 4;          // plane ring: z-1, z, z+1 resident, z+2 lan
 #ifndef PIFCM_TZ
 #define PIFCM_TZ 32
 #endif
-constexpr int kTZ = PIFCM_TZ;       // planes per CTA (z-chunk)
+constexpr int kTZ = PIFCM_TZ;       // planes per CTA (z-chunk) for deep grids
+constexpr int kTZMin = 8;           // smallest z-chunk used to fill a wave
 constexpr int kStepThreads = kTX * kWarpsY;
 
 // Pointwise (FCM, lambda = xi = 0) step.
@@ -64,7 +65,7 @@ struct StepArgs {
     int nblk;            // partial records per state
     const double *stats; // nullable: skip state p if stats[4p+3] != 0 (converged)
     const int *stop;     // nullable: skip everything if *stop != 0
-    int tiles_x, tiles_y, zchunks;
+    int tiles_x, tiles_y, zchunks, tz;  // tz = planes per z-chunk
     float m, inv_m1;     // m, 1/(m-1)
     int q_mode;
     int first;           // FCM first iteration: U_in not read, max|du| := 1
@@ -114,7 +115,9 @@ struct PsoUpdateArgs {
 // ---------------------------------------------------------------- launchers
 // All return cudaGetLastError() of the launch.
 cudaError_t launch_step(const StepArgs &a, int C, bool stencil, int P, cudaStream_t st);
-int step_nblk(int nx, int ny, int nz, bool stencil);
+int step_nblk(int nx, int ny, int nz, bool stencil, int P);
+int step_nblk_max(int nx, int ny, int nz);
+int step_zchunks(int nx, int ny, int nz, int P);
 cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_copy(const float4 *scratch, float4 *out, long long nvox, int P,
                               const double *stats, int iters, cudaStream_t st);

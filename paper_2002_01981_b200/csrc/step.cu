@@ -428,8 +428,8 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     const int tile = blockIdx.x;
     const int x0 = (tile % a.tiles_x) * kTX;
     const int y0 = (tile / a.tiles_x) * kTY;
-    const int zb = blockIdx.y * kTZ;
-    const int ze = min(zb + kTZ, a.nz);
+    const int zb = blockIdx.y * a.tz;
+    const int ze = min(zb + a.tz, a.nz);
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
     const int slot = a.in_idx ? a.in_idx[p] : p;
@@ -749,10 +749,44 @@ static int pw_blocks(long long nvox) {
     return (int)b;
 }
 
-int step_nblk(int nx, int ny, int nz, bool stencil) {
+// z-chunks of a stencil launch.  Depends on the volume only (not on the
+// number of states), so the partial-sum decomposition -- and therefore every
+// reduction result -- is the same whether a state is evaluated alone, in a
+// batch, or on any rank of a particle-sharded run.  Chosen to fill whole
+// waves of CTA slots (148 SMs x kStepMinBlocks) for a single state (the
+// final IFCM), weighing the 2 halo planes each chunk re-reads; batched
+// launches are many waves deep either way.
+int step_zchunks(int nx, int ny, int nz, int P) {
+    (void)P;
+    const long long tiles = (long long)((nx + kTX - 1) / kTX) * ((ny + kTY - 1) / kTY);
+    const long long slots = 148LL * kStepMinBlocks;
+    const int zmax = (nz + kTZMin - 1) / kTZMin;
+    int best = (nz + kTZ - 1) / kTZ;
+    double best_eff = -1.0;
+    for (int z = 1; z <= zmax; ++z) {
+        const int tz = (nz + z - 1) / z;
+        const int zz = (nz + tz - 1) / tz;  // chunks actually needed with tz planes each
+        const long long ctas = tiles * zz;
+        const long long waves = (ctas + slots - 1) / slots;
+        const double eff = (double)ctas / (double)(waves * slots) * (double)tz / (double)(tz + 2);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = zz;
+        }
+    }
+    return best;
+}
+
+int step_nblk(int nx, int ny, int nz, bool stencil, int P) {
     if (!stencil) return pw_blocks((long long)nx * ny * nz);
-    const int tx = (nx + kTX - 1) / kTX, ty = (ny + kTY - 1) / kTY, tz = (nz + kTZ - 1) / kTZ;
-    return tx * ty * tz;
+    const int tx = (nx + kTX - 1) / kTX, ty = (ny + kTY - 1) / kTY;
+    return tx * ty * step_zchunks(nx, ny, nz, P);
+}
+
+int step_nblk_max(int nx, int ny, int nz) {
+    const int tx = (nx + kTX - 1) / kTX, ty = (ny + kTY - 1) / kTY;
+    const int s = tx * ty * ((nz + kTZMin - 1) / kTZMin), q = pw_blocks((long long)nx * ny * nz);
+    return s > q ? s : q;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -818,8 +852,9 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
     StepArgs a = a0;
     a.tiles_x = (a.nx + kTX - 1) / kTX;
     a.tiles_y = (a.ny + kTY - 1) / kTY;
-    a.zchunks = (a.nz + kTZ - 1) / kTZ;
-    a.nblk = step_nblk(a.nx, a.ny, a.nz, stencil);
+    a.zchunks = step_zchunks(a.nx, a.ny, a.nz, P);
+    a.tz = (a.nz + a.zchunks - 1) / a.zchunks;
+    a.nblk = step_nblk(a.nx, a.ny, a.nz, stencil, P);
     const bool m2 = (a.m == 2.0f);
     switch (C) {
         case 2: return m2 ? launch_t<2, true>(a, stencil, P, st) : launch_t<2, false>(a, stencil, P, st);
