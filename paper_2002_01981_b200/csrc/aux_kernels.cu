@@ -387,85 +387,100 @@ cudaError_t launch_hist_u8(const uint8_t *vol, long long n, const unsigned int *
 // mu_j = (j+0.5)/C, sigma_j^2 = 1/(4C^2), w_j = 1/C; variance floor 1e-6;
 // stop when no mean moves by 1e-9 or after max_iter; means sorted ascending;
 // fewer than C occupied bins or coincident means -> c_j = j/(C-1).
-// One block, one thread per bin, fp64, fixed-order tree reductions.
-__device__ double block_sum256(double v, double *sh) {
-    sh[threadIdx.x] = v;
+// One block, one thread per bin, fp64; every reduction is a fixed-order
+// xor-shuffle tree inside each warp followed by the 8 warp results in order,
+// all statistics of a pass reduced together (two passes per EM iteration).
+template <int NV>
+__device__ __forceinline__ void block_sum_vec(double (&v)[NV], double (*sh)[NV]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) sh[warp][i] = v[i];
     __syncthreads();
-    for (int s = 128; s > 0; s >>= 1) {
-        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-        __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double t = sh[0][i];
+        for (int w = 1; w < 8; ++w) t += sh[w][i];
+        v[i] = t;
     }
-    const double r = sh[0];
     __syncthreads();
-    return r;
 }
 
 __global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max_iter, float *c0) {
-    __shared__ double sh[256];
-    __shared__ double mu[kMaxC], s2[kMaxC], w[kMaxC];
-    __shared__ int flag;
+    __shared__ double sh1[8][2 * kMaxC + 2];
+    __shared__ double sh2[8][kMaxC];
+    double mu[kMaxC], s2[kMaxC], w[kMaxC];
     const int b = threadIdx.x;
     const double y = (double)b / 255.0;
     const double n = (double)hist[b];
-    const double Ntot = block_sum256(n, sh);
-    const double occ = block_sum256(n > 0.0 ? 1.0 : 0.0, sh);
-    if (threadIdx.x == 0) {
-        flag = (Ntot <= 0.0 || occ < (double)C) ? 1 : 0;
-        for (int j = 0; j < C; ++j) {
-            mu[j] = ((double)j + 0.5) / (double)C;
-            s2[j] = 1.0 / (4.0 * (double)C * (double)C);
-            w[j] = 1.0 / (double)C;
-        }
-    }
-    __syncthreads();
-    if (flag) {
+    double tot[2 * kMaxC + 2];
+#pragma unroll
+    for (int i = 0; i < 2 * kMaxC + 2; ++i) tot[i] = 0.0;
+    tot[0] = n;
+    tot[1] = n > 0.0 ? 1.0 : 0.0;
+    block_sum_vec<2 * kMaxC + 2>(tot, sh1);
+    const double Ntot = tot[0], occ = tot[1];
+    if (Ntot <= 0.0 || occ < (double)C) {
         if (threadIdx.x < C) c0[threadIdx.x] = (float)((double)threadIdx.x / (double)(C - 1));
         return;
     }
+    for (int j = 0; j < kMaxC; ++j) {
+        mu[j] = ((double)j + 0.5) / (double)C;
+        s2[j] = 1.0 / (4.0 * (double)C * (double)C);
+        w[j] = 1.0 / (double)C;
+    }
     const double two_pi = 6.283185307179586476925286766559;
     for (int it = 0; it < max_iter; ++it) {
-        // E step
+        // E step: responsibilities of this bin (R15)
         double r[kMaxC];
-        double s = 0.0;
+        double sum = 0.0;
         for (int j = 0; j < C; ++j) {
             const double d = y - mu[j];
             r[j] = w[j] * exp(-d * d / (2.0 * s2[j])) / sqrt(two_pi * s2[j]);
-            s += r[j];
+            sum += r[j];
         }
-        if (!(s > 0.0)) {
+        if (!(sum > 0.0)) {
             int jb = 0;
             for (int j = 1; j < C; ++j)
                 if (fabs(y - mu[j]) < fabs(y - mu[jb])) jb = j;
             for (int j = 0; j < C; ++j) r[j] = (j == jb) ? 1.0 : 0.0;
-            s = 1.0;
+            sum = 1.0;
         }
-        double Nj[kMaxC], newmu[kMaxC];
+        double v1[2 * kMaxC + 2];
+#pragma unroll
+        for (int i = 0; i < 2 * kMaxC + 2; ++i) v1[i] = 0.0;
         for (int j = 0; j < C; ++j) {
-            const double rr = (n > 0.0) ? r[j] / s : 0.0;
-            Nj[j] = block_sum256(n * rr, sh);
-            const double Sy = block_sum256(n * rr * y, sh);
-            newmu[j] = (Nj[j] > 1e-12) ? Sy / Nj[j] : mu[j];
+            const double rr = (n > 0.0) ? r[j] / sum : 0.0;
+            r[j] = rr;
+            v1[j] = n * rr;              // N_j
+            v1[kMaxC + j] = n * rr * y;  // sum y
         }
-        double Syy[kMaxC];
+        block_sum_vec<2 * kMaxC + 2>(v1, sh1);
+        double newmu[kMaxC];
+        for (int j = 0; j < C; ++j) newmu[j] = (v1[j] > 1e-12) ? v1[kMaxC + j] / v1[j] : mu[j];
+        double v2[kMaxC];
+#pragma unroll
+        for (int j = 0; j < kMaxC; ++j) v2[j] = 0.0;
         for (int j = 0; j < C; ++j) {
-            const double rr = (n > 0.0) ? r[j] / s : 0.0;
             const double d = y - newmu[j];
-            Syy[j] = block_sum256(n * rr * d * d, sh);
+            v2[j] = n * r[j] * d * d;
         }
-        if (threadIdx.x == 0) {
-            double shift = 0.0;
-            for (int j = 0; j < C; ++j) {
-                if (Nj[j] > 1e-12) {
-                    w[j] = Nj[j] / Ntot;
-                    s2[j] = fmax(Syy[j] / Nj[j], 1e-6);
-                }
-                shift = fmax(shift, fabs(newmu[j] - mu[j]));
-                mu[j] = newmu[j];
+        block_sum_vec<kMaxC>(v2, sh2);
+        // M step (every thread holds the same sums, so every thread updates)
+        double shift = 0.0;
+        for (int j = 0; j < C; ++j) {
+            if (v1[j] > 1e-12) {
+                w[j] = v1[j] / Ntot;
+                s2[j] = fmax(v2[j] / v1[j], 1e-6);
             }
-            flag = (shift < 1e-9) ? 1 : 0;
+            shift = fmax(shift, fabs(newmu[j] - mu[j]));
+            mu[j] = newmu[j];
         }
-        __syncthreads();
-        if (flag) break;
+        if (shift < 1e-9) break;
     }
     if (threadIdx.x == 0) {
         double m[kMaxC];

@@ -64,7 +64,9 @@ int check_grid(pifcm_ctx *ctx, const pifcm_grid *g) {
         return fail(ctx, PIFCM_EINVAL, "grid dims must be >= 1 (got %d x %d x %d)", g->nx, g->ny, g->nz);
     if (g->pitch < g->nx) return fail(ctx, PIFCM_EINVAL, "pitch %d < nx %d", g->pitch, g->nx);
     if (g->pitch % 4 != 0) return fail(ctx, PIFCM_EALIGN, "pitch %d is not a multiple of 4", g->pitch);
-    if ((long long)g->ny * g->nz > (1LL << 31)) return fail(ctx, PIFCM_EINVAL, "volume too large");
+    if ((long long)g->nx * g->ny * g->nz >= (1LL << 31))
+        return fail(ctx, PIFCM_EINVAL, "volume of %lld voxels >= 2^31 (use z-slab sharding)",
+                    (long long)g->nx * g->ny * g->nz);
     return PIFCM_OK;
 }
 
@@ -101,7 +103,7 @@ void prange(const pifcm_pso_cfg *p, int *p0, int *pl) {
 // Workspace layout (all offsets 256-byte aligned).
 struct Layout {
     size_t x, vol, lab, hist, mm, c0, slots, hdr, dhdr, pos, vel, pbf, pbx, fit, evalpos, cur, nxt,
-        gbc, cent, part, stats, lamxi, total;
+        gbc, cent, part, stats, lamxi, cnt, total;
     int nslots, P, Pl, p0, nblk;
     long long nvox;
 };
@@ -139,6 +141,7 @@ Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg 
     L.part = take(sizeof(double) * kNR * (size_t)L.nblk * (Pl > 1 ? Pl : 1));
     L.stats = take(sizeof(double) * 4 * (Pl > 1 ? Pl : 1));
     L.lamxi = take(sizeof(double) * 2 * (Pl > 1 ? Pl : 1));
+    L.cnt = take(sizeof(unsigned) * (Pl > 1 ? Pl : 1));
     L.total = o;
     return L;
 }
@@ -176,7 +179,7 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
              const float4 *Uin, float4 *Uout, const int *in_idx, const int *out_idx,
              float *centers, const double *lamxi, bool stencil, int first, int P,
              double *partials, double *fitness, double *stats, float eps, int *status,
-             const int *stop, cudaStream_t st, int n_in_states) {
+             const int *stop, cudaStream_t st, int n_in_states, unsigned *counters) {
     StepArgs a{};
     a.x = x;
     a.nx = g->nx; a.ny = g->ny; a.nz = g->nz; a.pitch = g->pitch;
@@ -188,6 +191,12 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     a.q_mode = cfg->q_mode; a.first = first;
     a.n_in_states = n_in_states;
     a.want_du = (stats != nullptr) ? 1 : 0;
+    a.counters = counters;
+    a.C = cfg->C;
+    a.fitness = fitness;
+    a.stats_out = stats;
+    a.eps = eps;
+    a.status = status;
     const bool timed = ctx->timing && stencil;
     if (timed) {
         while (ctx->tev.size() < ctx->tused + 2) {
@@ -207,12 +216,8 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
         ctx->t_bytes[cls] += 32.0 * (double)a.nvox * P + 4.0 * (double)a.nvox;
         ctx->t_launches[cls] += 1;
     }
-    FinalizeArgs f{};
-    f.partials = partials;
-    f.nblk = step_nblk(g->nx, g->ny, g->nz, stencil, P);
-    f.C = cfg->C; f.P = P; f.centers = centers; f.fitness = fitness; f.stats = stats;
-    f.eps = eps; f.status = status; f.stop = stop;
-    LAUNCH(ctx, 1, launch_finalize(f, st));
+    // Eq. 3 / Eq. 1 finalisation is fused: the last CTA of each state sums the
+    // partial records (finalize_if_last in step.cu)
     return PIFCM_OK;
 }
 
@@ -314,7 +319,8 @@ int pifcm_iterate_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *c
     const long long nvox = (long long)grid->nx * grid->ny * grid->nz;
     const int nblk = step_nblk_max(grid->nx, grid->ny, grid->nz);
     size_t b = align_up(sizeof(double) * kNR * (size_t)nblk * P, 256) +  // partials
-               align_up(sizeof(double) * 4 * P, 256) + 256;              // stats scratch + status
+               align_up(sizeof(double) * 4 * P, 256) + 256 +             // stats scratch + status
+               align_up(sizeof(unsigned) * P, 256);                      // finalisation counters
     if (iters > 1) b += align_up(sizeof(float4) * (size_t)nvox * P, 256);
     *bytes = b;
     return PIFCM_OK;
@@ -346,7 +352,9 @@ int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
     double *partials = at<double>(ws, o); o = align_up(o + sizeof(double) * kNR * (size_t)nblk * P, 256);
     double *st_scr = at<double>(ws, o); o = align_up(o + sizeof(double) * 4 * P, 256);
     int *status = at<int>(ws, o); o += 256;
+    unsigned *counters = at<unsigned>(ws, o); o = align_up(o + sizeof(unsigned) * P, 256);
     float4 *scratch = iters > 1 ? at<float4>(ws, o) : nullptr;
+    CK(ctx, cudaMemsetAsync(counters, 0, sizeof(unsigned) * P, st));
     double *S = stats ? stats : st_scr;
     CK(ctx, cudaMemsetAsync(S, 0, sizeof(double) * 4 * P, st));
     CK(ctx, cudaMemsetAsync(status, 0, sizeof(int), st));
@@ -358,7 +366,7 @@ int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
     for (int t = 1; t <= iters; ++t) {
         float4 *dst = (((iters - t) & 1) == 0) ? reinterpret_cast<float4 *>(U_out) : scratch;
         r = run_step(ctx, grid, cfg, x, src, dst, nullptr, nullptr, centers, lam_xi, !zero, 0, P,
-                     partials, nullptr, S, eps, status, nullptr, st, P);
+                     partials, nullptr, S, eps, status, nullptr, st, P, counters);
         if (r) return r;
         src = dst;
     }
@@ -389,6 +397,7 @@ int pifcm_pso_init(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
     if (reinterpret_cast<const void *>(U0) != slot0)
         CK(ctx, cudaMemcpyAsync(slot0, U0, sizeof(float4) * (size_t)L.nvox, cudaMemcpyDeviceToDevice, st));
     const uint32_t k0 = (uint32_t)(pso->seed & 0xFFFFFFFFu), k1 = (uint32_t)(pso->seed >> 32);
+    CK(ctx, cudaMemsetAsync(at<unsigned>(ws, L.cnt), 0, sizeof(unsigned) * (L.Pl > 1 ? L.Pl : 1), st));
     LAUNCH(ctx, 1, launch_pso_init(swarm_of(ws, L), L.P, L.Pl, L.p0, pso->v0, k0, k1, c0, L.nslots, st));
     return PIFCM_OK;
 }
@@ -413,7 +422,7 @@ int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
     float4 *slots = at<float4>(ws, L.slots);
     return run_step(ctx, grid, cfg, x, slots, slots, s.cur, s.nxt, s.centers, s.pos + 2 * L.p0, true, 0,
                     L.Pl, at<double>(ws, L.part), s.fit + L.p0, nullptr, 0.f, s.hdr + kHStatus,
-                    s.hdr + kHStop, st, L.nslots);
+                    s.hdr + kHStop, st, L.nslots, at<unsigned>(ws, L.cnt));
 }
 
 int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
@@ -546,7 +555,7 @@ int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float 
 // the slot holding the result in *res and the iteration count in *iters.
 static int run_until(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x,
                      float4 *slots, long long nvox, int a, int b, float *centers, const double *lamxi,
-                     bool stencil, bool fcm_first, double *partials, double *stats, int *status,
+                     bool stencil, bool fcm_first, double *partials, double *stats, int *status, unsigned *counters,
                      cudaStream_t st, int *res, int *iters) {
     CK(ctx, cudaMemsetAsync(stats, 0, sizeof(double) * 4, st));
     int src = a, dst = b, t = 0;
@@ -554,7 +563,7 @@ static int run_until(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *
     for (t = 1; t <= cfg->max_iter; ++t) {
         int r = run_step(ctx, g, cfg, x, slots + (long long)src * nvox, slots + (long long)dst * nvox, nullptr,
                          nullptr, centers, lamxi, stencil, (fcm_first && t == 1) ? 1 : 0, 1, partials,
-                         nullptr, stats, cfg->eps, status, nullptr, st, 1);
+                         nullptr, stats, cfg->eps, status, nullptr, st, 1, counters);
         if (r) return r;
         const int tmp = src; src = dst; dst = tmp;
         if (t % check_every == 0 || t == cfg->max_iter) {
@@ -616,9 +625,10 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     CK(ctx, cudaMemcpyAsync(cent, c0, sizeof(float) * 4, cudaMemcpyDeviceToDevice, st));
     CK(ctx, cudaMemsetAsync(lamxi, 0, sizeof(double) * 2, st));
     CK(ctx, cudaMemsetAsync(s.hdr, 0, sizeof(int) * 16, st));
+    CK(ctx, cudaMemsetAsync(at<unsigned>(ws, L.cnt), 0, sizeof(unsigned) * (L.Pl > 1 ? L.Pl : 1), st));
     int fcm_slot = 0, fcm_iters = 0;
-    if ((r = run_until(ctx, &g, cfg, x, slots, L.nvox, 1, 0, cent, lamxi, false, true, partials, stats, status, st,
-                       &fcm_slot, &fcm_iters)))
+    if ((r = run_until(ctx, &g, cfg, x, slots, L.nvox, 1, 0, cent, lamxi, false, true, partials, stats, status,
+                       at<unsigned>(ws, L.cnt), st, &fcm_slot, &fcm_iters)))
         return r;
     // keep the FCM result in slot 0 (the PSO start slot)
     if (fcm_slot != 0)
@@ -642,7 +652,7 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     const bool zero = (pres.lambda == 0.0 && pres.xi == 0.0);
     int fin_slot = gs, fin_iters = 0;
     if ((r = run_until(ctx, &g, cfg, x, slots, L.nvox, gs, other, cent, lamxi, !zero, false, partials, stats, status,
-                       st, &fin_slot, &fin_iters)))
+                       at<unsigned>(ws, L.cnt), st, &fin_slot, &fin_iters)))
         return r;
     CK(ctx, cudaEventRecord(ev[4], st));
     // defuzzify (+ optional U copy)

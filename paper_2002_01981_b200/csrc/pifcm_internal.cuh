@@ -49,6 +49,7 @@ constexpr int kStepThreads = kTX * kWarpsY;
 
 // Pointwise (FCM, lambda = xi = 0) step.
 constexpr int kPwThreads = 256;
+constexpr int kPwSpan = 8;  // voxels per lane per span
 
 // ------------------------------------------------------------ step arguments
 struct StepArgs {
@@ -71,6 +72,13 @@ struct StepArgs {
     int first;           // FCM first iteration: U_in not read, max|du| := 1
     int n_in_states;     // states addressable from U_in (TMA tensor-map extent)
     int want_du;         // accumulate max|u_new - u_old| (convergence tests)
+    // fused finalisation (Eq. 3 / Eq. 1) by the last CTA of each state
+    unsigned *counters;  // [P] arrival counters, 0 between launches
+    int C;
+    double *fitness;     // nullable [P]
+    double *stats_out;   // nullable [P][4] {J, du, iters, converged} (same array as stats)
+    float eps;
+    int *status;         // nullable: PIFCM_ENUMERIC on a non-finite J
 };
 
 struct FinalizeArgs {

@@ -117,6 +117,59 @@ __device__ __forceinline__ void block_partials(const float (&num)[kMaxC], const 
         double t = red[0][r];
         for (int w = 1; w < NW; ++w) t = (r == kNR - 1) ? fmax(t, red[w][r]) : t + red[w][r];
         out[r] = t;
+        __threadfence();  // the record is visible device-wide before this CTA is counted
+    }
+}
+
+// Finalisation by the last CTA of state p (threadFenceReduction pattern):
+// the fixed-order fp64 sum of the nblk partial records, then Eq. 3:
+// c_j = sum u^m x / sum u^m (c_j kept if the sum < 1e-12, R9) and Eq. 1
+// (PAPER:53): J = sum of the per-voxel costs.  The summation order does not
+// depend on which CTA finishes last.
+template <int NT>
+__device__ __forceinline__ void finalize_if_last(const StepArgs &a, int p, int nblk) {
+    __shared__ int is_last;
+    __shared__ double red[NT][kNR];
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(&a.counters[p], 1u) == (unsigned)(nblk - 1));
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const double *src = a.partials + (long long)p * nblk * kNR;
+    double v[kNR];
+#pragma unroll
+    for (int r = 0; r < kNR; ++r) v[r] = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += NT) {
+#pragma unroll
+        for (int r = 0; r < kNR - 1; ++r) v[r] += __ldcg(src + (long long)b * kNR + r);
+        v[kNR - 1] = fmax(v[kNR - 1], __ldcg(src + (long long)b * kNR + kNR - 1));
+    }
+#pragma unroll
+    for (int r = 0; r < kNR; ++r) red[threadIdx.x][r] = v[r];
+    __syncthreads();
+    for (int s = NT / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+#pragma unroll
+            for (int r = 0; r < kNR - 1; ++r) red[threadIdx.x][r] += red[threadIdx.x + s][r];
+            red[threadIdx.x][kNR - 1] = fmax(red[threadIdx.x][kNR - 1], red[threadIdx.x + s][kNR - 1]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double J = red[0][2 * kMaxC], du = red[0][2 * kMaxC + 1];
+        for (int j = 0; j < a.C; ++j) {
+            const double num = red[0][j], den = red[0][kMaxC + j];
+            if (den >= kDenEps) a.centers[4 * p + j] = (float)(num / den);
+        }
+        if (a.fitness) a.fitness[p] = J;
+        if (a.stats_out) {
+            a.stats_out[4 * p + 0] = J;
+            a.stats_out[4 * p + 1] = du;
+            a.stats_out[4 * p + 2] += 1.0;
+            a.stats_out[4 * p + 3] = (a.eps > 0.f && du < (double)a.eps) ? 1.0 : 0.0;
+        }
+        if (!isfinite(J) && a.status) atomicExch(a.status, (int)PIFCM_ENUMERIC);
+        a.counters[p] = 0u;  // ready for the next launch
     }
 }
 
@@ -706,6 +759,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
     const int blk = blockIdx.x + gridDim.x * blockIdx.y;
     block_partials<kWarpsY>(num, den, Jacc, duacc, a.partials + ((long long)p * a.nblk + blk) * kNR);
+    finalize_if_last<kStepThreads>(a, p, a.nblk);
 }
 
 // ----------------------------------------------------------------------------
@@ -724,27 +778,31 @@ __global__ void __launch_bounds__(kPwThreads) k_step_pointwise(const StepArgs a)
     const float av[kMaxC] = {1.f, 1.f, 1.f, 1.f};  // lambda = xi = 0: Eq. 4 factor is 1
     float num[kMaxC] = {0.f, 0.f, 0.f, 0.f}, den[kMaxC] = {0.f, 0.f, 0.f, 0.f};
     float Jacc = 0.f, duacc = a.first ? 1.0f : 0.f;
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.nvox; i += stride) {
-        const int X = (int)(i % a.nx);
-        const long long row = i / a.nx;  // = z*ny + y
-        const float xv = a.x[row * a.pitch + X];
+    // grid-stride over voxels (coalesced); 32-bit index arithmetic (nvox < 2^31
+    // is checked by the host)
+    const unsigned nx = (unsigned)a.nx, nvox = (unsigned)a.nvox;
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nvox; i += stride) {
+        const unsigned row = i / nx;  // = z*ny + y
+        const unsigned X = i - row * nx;
+        const float xv = __ldg(a.x + (size_t)row * a.pitch + X);
         const float4 un = membership<C, M2>(xv, c, av, a.m, a.inv_m1, num, den, Jacc);
         if (!a.first) {
             const float4 uo = Uin[i];
             duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
                                        fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
         }
-        Uout[i] = un;
+        __stcs(Uout + i, un);
     }
     block_partials<kPwThreads / 32>(num, den, Jacc, duacc,
                                    a.partials + ((long long)p * a.nblk + blockIdx.x) * kNR);
+    finalize_if_last<kPwThreads>(a, p, a.nblk);
 }
 
 // ----------------------------------------------------------------------------
 static int pw_blocks(long long nvox) {
-    long long b = (nvox + kPwThreads * 8 - 1) / (kPwThreads * 8);
-    if (b > 148 * 8) b = 148 * 8;
+    long long b = (nvox + kPwThreads * kPwSpan - 1) / (kPwThreads * kPwSpan);
+    if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
     return (int)b;
 }
