@@ -82,10 +82,19 @@ typedef enum { PIFCM_U8 = 0, PIFCM_U16 = 1, PIFCM_F32 = 2 } pifcm_dtype;
 typedef struct pifcm_ctx pifcm_ctx;
 
 /* Volume extent.  Alg. 1 input "img3d - a 3D matrix of pixel intensities"
- * (PAPER:93).  nz == 1 is the 2D case (8-neighbourhood). */
+ * (PAPER:93).  nz == 1 is the 2D case (8-neighbourhood).
+ * z-slab mode (nz_total > 0, only for the pifcm_slab_* calls): this process
+ * holds the planes [z0, z0 + nz) of a volume of nz_total planes; its x and U
+ * arrays then have nz + 2 planes, plane 0 being global z0 - 1 and plane
+ * nz + 1 global z0 + nz (halo planes).  z0 must be a multiple of 16 and every
+ * slab but the last must have a multiple of 16 planes (the slab reductions
+ * use fixed global chunks of 16 planes, which makes them independent of the
+ * number of slabs).  nz_total = 0 (or z0 = 0, nz_total = nz): whole volume. */
 typedef struct {
     int32_t nx, ny, nz;
-    int32_t pitch; /* elements per x row of the intensity volume; >= nx, % 4 == 0 */
+    int32_t pitch;    /* elements per x row of the intensity volume; >= nx, % 4 == 0 */
+    int32_t z0;       /* z-slab: first global plane held (0 otherwise)                 */
+    int32_t nz_total; /* z-slab: planes of the whole volume (0: not a slab)             */
 } pifcm_grid;
 
 /* Method parameters.  Alg. 1 inputs c, v, h, m, epsilon. */
@@ -270,6 +279,47 @@ int pifcm_segment_host(pifcm_ctx *ctx, const uint8_t *vol_host, int32_t nx, int3
                        int32_t nz, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
                        void *ws, size_t ws_bytes, uint8_t *labels_host, pifcm_report *rep,
                        pifcm_stream stream);
+
+/* ------------------------------------------------------------------- z-slab */
+/* The IFCM step of a volume too large for one GPU, partitioned into z-slabs
+ * across processes: per iteration the caller exchanges one halo
+ * plane per neighbour and per state (pifcm_slab_halo + its own collective),
+ * runs pifcm_slab_step, all-gathers the per-chunk partial records of all
+ * ranks in rank order and calls pifcm_slab_finalize, which applies Eq. 3 /
+ * Eq. 1 identically on every rank.  Because the records are
+ * keyed by fixed global 16-plane chunks, centres and J are bit-identical for
+ * any number of slabs. */
+
+/* Partial records per state that pifcm_slab_step writes for this slab. */
+int pifcm_slab_records(const pifcm_grid *grid, int32_t *nrec);
+
+/* One Jacobi IFCM step over the slab's local planes for P
+ * states.  x dev fp32 [nz+2][ny][pitch]; U_in, U_out dev fp32
+ * [P][nz+2][ny][nx][4] (halo planes of U_in filled); centers dev fp32 [P][4]
+ * (read only); lam_xi dev fp64 [P][2]; stats dev fp64 [P][4] nullable (states
+ * with stats[p][3] != 0 are skipped); records dev fp64 [P][nrec][10] out:
+ * per chunk and tile {sum u^m x (4), sum u^m (4), J, max|du|}.  Async. */
+int pifcm_slab_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                    const float *x, const float *U_in, float *U_out, const float *centers,
+                    const double *lam_xi, int32_t P, const double *stats, double *records,
+                    pifcm_stream stream);
+
+/* Eq. 3 / Eq. 1 from the gathered records [world][P][nrec][10] (rank order,
+ * zero-padded to nrec per rank): centres (kept where sum u^m < 1e-12, R9),
+ * stats {J, max|du|, iterations += 1, converged = max|du| < eps} and fitness
+ * (nullable).  Async. */
+int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int32_t nrec,
+                        const double *records, float *centers, double *stats, double *fitness,
+                        float eps, pifcm_stream stream);
+
+/* Halo planes of P slab states U [P][nz+2][ny][nx][4]:
+ *   op 0: pack the first local plane (array plane 1) into buf [P][ny][nx][4]
+ *   op 1: pack the last local plane (array plane nz) into buf
+ *   op 2: unpack buf into the lower halo (array plane 0); zeros when z0 == 0
+ *   op 3: unpack buf into the upper halo (plane nz+1); zeros at the volume end
+ * (buf may be NULL for a zero fill).  Async. */
+int pifcm_slab_halo(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t P, int32_t op, float *U,
+                    float *buf, pifcm_stream stream);
 
 /* Number of kernels this context has launched so far (for the bench's
  * gpu_launches count). */

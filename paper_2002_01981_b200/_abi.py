@@ -20,7 +20,8 @@ U8 = 0
 
 
 class Grid(ct.Structure):
-    _fields_ = [("nx", ct.c_int32), ("ny", ct.c_int32), ("nz", ct.c_int32), ("pitch", ct.c_int32)]
+    _fields_ = [("nx", ct.c_int32), ("ny", ct.c_int32), ("nz", ct.c_int32), ("pitch", ct.c_int32),
+                ("z0", ct.c_int32), ("nz_total", ct.c_int32)]
 
 
 class IfcmCfg(ct.Structure):
@@ -84,6 +85,11 @@ SIGNATURES = {
                                  ct.c_int32, _vp, ct.c_size_t, _vp, _vp, ct.POINTER(Report), _vp]),
     "pifcm_segment_host": (ct.c_int, [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int32, _C, _P, _vp,
                                       ct.c_size_t, _vp, ct.POINTER(Report), _vp]),
+    "pifcm_slab_records": (ct.c_int, [_G, ct.POINTER(ct.c_int32)]),
+    "pifcm_slab_step": (ct.c_int, [_vp, _G, _C, _vp, _vp, _vp, _vp, _vp, ct.c_int32, _vp, _vp, _vp]),
+    "pifcm_slab_finalize": (ct.c_int, [_vp, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, _vp, _vp, _vp,
+                                       _vp, ct.c_float, _vp]),
+    "pifcm_slab_halo": (ct.c_int, [_vp, _G, ct.c_int32, ct.c_int32, _vp, _vp, _vp]),
 }
 
 _lib = None

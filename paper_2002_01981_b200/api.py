@@ -98,8 +98,8 @@ def _stream(stream) -> int | None:
     return stream.cuda_stream or None
 
 
-def _grid(nx, ny, nz, pitch=None) -> _abi.Grid:
-    return _abi.Grid(nx, ny, nz, pitch if pitch is not None else pitch_of(nx))
+def _grid(nx, ny, nz, pitch=None, z0=0, nz_total=0) -> _abi.Grid:
+    return _abi.Grid(nx, ny, nz, pitch if pitch is not None else pitch_of(nx), z0, nz_total)
 
 
 @dataclass
@@ -295,6 +295,27 @@ class Context:
                                              ct.byref(pso.c()), _ptr(ws), ws.numel(), _ptr(labels_host),
                                              ct.byref(rep), _stream(stream)))
         return report_dict(rep, cfg.C)
+
+
+    # ------------------------------------------------------------ z-slab
+    def slab_records(self, grid) -> int:
+        n = ct.c_int32()
+        self._ck(self.lib.pifcm_slab_records(ct.byref(grid), ct.byref(n)))
+        return n.value
+
+    def slab_step(self, grid, cfg, x, U_in, U_out, centers, lam_xi, records, stats=None, stream=None):
+        P = U_in.shape[0]
+        self._ck(self.lib.pifcm_slab_step(self._h, ct.byref(grid), ct.byref(cfg.c()), _ptr(x), _ptr(U_in),
+                                          _ptr(U_out), _ptr(centers), _ptr(lam_xi), P, _ptr(stats),
+                                          _ptr(records), _stream(stream)))
+
+    def slab_finalize(self, C, P, world, nrec, records, centers, stats=None, fitness=None, eps=0.0,
+                      stream=None):
+        self._ck(self.lib.pifcm_slab_finalize(self._h, C, P, world, nrec, _ptr(records), _ptr(centers),
+                                              _ptr(stats), _ptr(fitness), eps, _stream(stream)))
+
+    def slab_halo(self, grid, P, op, U, buf=None, stream=None):
+        self._ck(self.lib.pifcm_slab_halo(self._h, ct.byref(grid), P, op, _ptr(U), _ptr(buf), _stream(stream)))
 
 
 def report_dict(rep: _abi.Report, C: int) -> dict:

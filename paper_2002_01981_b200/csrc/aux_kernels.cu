@@ -83,6 +83,81 @@ cudaError_t launch_fixup_copy(const float4 *scratch, float4 *out, long long nvox
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- z-slab
+// Records of all ranks, gathered [world][P][nrec][kNR] (zero-padded to nrec
+// per rank), summed for state p in (rank, record) order -- i.e. in global
+// z-chunk order, the same order for any number of slabs -- then Eq. 3 / Eq. 1.
+__global__ void __launch_bounds__(kFinThreads) k_slab_finalize(int C, int P, int world, int nrec,
+                                                             const double *rec, float *centers,
+                                                             double *stats, double *fitness, float eps,
+                                                             int *status) {
+    __shared__ double red[kFinThreads][kNR];
+    const int p = blockIdx.x;
+    if (stats && stats[4 * p + 3] != 0.0) return;
+    const long long total = (long long)world * nrec;
+    double v[kNR];
+#pragma unroll
+    for (int r = 0; r < kNR; ++r) v[r] = 0.0;
+    for (long long b = threadIdx.x; b < total; b += kFinThreads) {
+        const long long w = b / nrec, k = b - w * nrec;
+        const double *src = rec + ((w * P + p) * nrec + k) * kNR;
+#pragma unroll
+        for (int r = 0; r < kNR - 1; ++r) v[r] += src[r];
+        v[kNR - 1] = fmax(v[kNR - 1], src[kNR - 1]);
+    }
+#pragma unroll
+    for (int r = 0; r < kNR; ++r) red[threadIdx.x][r] = v[r];
+    __syncthreads();
+    for (int s = kFinThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+#pragma unroll
+            for (int r = 0; r < kNR - 1; ++r) red[threadIdx.x][r] += red[threadIdx.x + s][r];
+            red[threadIdx.x][kNR - 1] = fmax(red[threadIdx.x][kNR - 1], red[threadIdx.x + s][kNR - 1]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double J = red[0][2 * kMaxC], du = red[0][2 * kMaxC + 1];
+        for (int j = 0; j < C; ++j) {
+            const double num = red[0][j], den = red[0][kMaxC + j];
+            if (den >= kDenEps) centers[4 * p + j] = (float)(num / den);
+        }
+        if (fitness) fitness[p] = J;
+        if (stats) {
+            stats[4 * p + 0] = J;
+            stats[4 * p + 1] = du;
+            stats[4 * p + 2] += 1.0;
+            stats[4 * p + 3] = (eps > 0.f && du < (double)eps) ? 1.0 : 0.0;
+        }
+        if (!isfinite(J) && status) atomicExch(status, (int)PIFCM_ENUMERIC);
+    }
+}
+
+cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const double *records, float *centers,
+                                 double *stats, double *fitness, float eps, int *status, cudaStream_t st) {
+    k_slab_finalize<<<P, kFinThreads, 0, st>>>(C, P, world, nrec, records, centers, stats, fitness, eps, status);
+    return cudaGetLastError();
+}
+
+// Copy one plane of every state between a slab array and a packed buffer
+// (halo pack / unpack), or zero it (a halo outside the volume).
+__global__ void k_halo_copy(const float4 *src, long long src_state, float4 *dst, long long dst_state,
+                            long long plane, bool zero) {
+    const int p = blockIdx.y;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < plane;
+         i += (long long)gridDim.x * blockDim.x)
+        dst[p * dst_state + i] = zero ? make_float4(0.f, 0.f, 0.f, 0.f) : src[p * src_state + i];
+}
+
+cudaError_t launch_halo_copy(const float4 *src, long long src_state, float4 *dst, long long dst_state,
+                             long long plane, int P, bool zero, cudaStream_t st) {
+    long long b = (plane + 255) / 256;
+    if (b > 148 * 4) b = 148 * 4;
+    dim3 grid((unsigned)(b < 1 ? 1 : b), P);
+    k_halo_copy<<<grid, 256, 0, st>>>(src, src_state, dst, dst_state, plane, zero);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- Philox
 // Philox4x32-10 (Salmon et al. SC'11), the counter-based generator shared by
 // specification (not code) with the oracle so both see the same draws (R12).

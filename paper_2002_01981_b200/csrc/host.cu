@@ -64,6 +64,8 @@ int check_grid(pifcm_ctx *ctx, const pifcm_grid *g) {
         return fail(ctx, PIFCM_EINVAL, "grid dims must be >= 1 (got %d x %d x %d)", g->nx, g->ny, g->nz);
     if (g->pitch < g->nx) return fail(ctx, PIFCM_EINVAL, "pitch %d < nx %d", g->pitch, g->nx);
     if (g->pitch % 4 != 0) return fail(ctx, PIFCM_EALIGN, "pitch %d is not a multiple of 4", g->pitch);
+    const bool slab = g->nz_total > 0 && !(g->z0 == 0 && g->nz_total == g->nz);
+    if (slab) return fail(ctx, PIFCM_EINVAL, "z-slab grids (nz_total > 0) are only for the pifcm_slab_* calls");
     if ((long long)g->nx * g->ny * g->nz >= (1LL << 31))
         return fail(ctx, PIFCM_EINVAL, "volume of %lld voxels >= 2^31 (use z-slab sharding)",
                     (long long)g->nx * g->ny * g->nz);
@@ -705,6 +707,89 @@ int pifcm_segment_host(pifcm_ctx *ctx, const uint8_t *vol_host, int32_t nx, int3
         return r;
     CK(ctx, cudaMemcpyAsync(labels_host, dlab, (size_t)L.nvox, cudaMemcpyDeviceToHost, st));
     CK(ctx, cudaStreamSynchronize(st));
+    return PIFCM_OK;
+}
+
+// ============================================================== ABI: z-slab
+static int check_slab(pifcm_ctx *ctx, const pifcm_grid *g) {
+    if (!g) return fail(ctx, PIFCM_EINVAL, "grid is NULL");
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1) return fail(ctx, PIFCM_EINVAL, "grid dims must be >= 1");
+    if (g->pitch < g->nx || g->pitch % 4 != 0) return fail(ctx, PIFCM_EALIGN, "pitch must be >= nx and % 4 == 0");
+    if (g->nz_total < 1) return fail(ctx, PIFCM_EINVAL, "slab calls need nz_total >= 1");
+    if (g->z0 < 0 || g->z0 + g->nz > g->nz_total)
+        return fail(ctx, PIFCM_EINVAL, "slab [%d, %d) outside [0, %d)", g->z0, g->z0 + g->nz, g->nz_total);
+    if (g->z0 % kSlabTZ != 0) return fail(ctx, PIFCM_EINVAL, "slab z0 = %d is not a multiple of %d", g->z0, kSlabTZ);
+    if (g->z0 + g->nz != g->nz_total && g->nz % kSlabTZ != 0)
+        return fail(ctx, PIFCM_EINVAL, "a slab other than the last must hold a multiple of %d planes", kSlabTZ);
+    if ((long long)g->nx * g->ny * (g->nz + 2) >= (1LL << 31)) return fail(ctx, PIFCM_EINVAL, "slab too large");
+    return PIFCM_OK;
+}
+
+int pifcm_slab_records(const pifcm_grid *grid, int32_t *nrec) {
+    if (!nrec) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_slab(nullptr, grid))) return r;
+    *nrec = ((grid->nx + kTX - 1) / kTX) * ((grid->ny + kTY - 1) / kTY) * ((grid->nz + kSlabTZ - 1) / kSlabTZ);
+    return PIFCM_OK;
+}
+
+int pifcm_slab_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const float *x,
+                    const float *U_in, float *U_out, const float *centers, const double *lam_xi, int32_t P,
+                    const double *stats, double *records, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_slab(ctx, grid)) || (r = check_cfg(ctx, cfg))) return r;
+    if (P < 1 || P > 65535) return fail(ctx, PIFCM_EINVAL, "P = %d outside [1, 65535]", P);
+    if (!x || !U_in || !U_out || !centers || !lam_xi || !records)
+        return fail(ctx, PIFCM_EINVAL, "x, U_in, U_out, centers, lam_xi and records must be non-NULL");
+    if (U_in == U_out) return fail(ctx, PIFCM_EINVAL, "U_in and U_out must not alias");
+    StepArgs a{};
+    a.x = x;
+    a.nx = grid->nx; a.ny = grid->ny; a.nz = grid->nz + 2; a.pitch = grid->pitch;
+    a.nvox = (long long)grid->nx * grid->ny * (grid->nz + 2);
+    a.z_lo = 1; a.nz_t = grid->nz; a.goff = grid->z0 - 1; a.nz_g = grid->nz_total;
+    a.U_in = reinterpret_cast<const float4 *>(U_in); a.U_out = reinterpret_cast<float4 *>(U_out);
+    a.centers = const_cast<float *>(centers); a.lam_xi = lam_xi; a.partials = records;
+    a.stats = stats;
+    a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f); a.q_mode = cfg->q_mode;
+    a.n_in_states = P;
+    a.want_du = 1;
+    a.counters = nullptr;  // records are combined across ranks by pifcm_slab_finalize
+    a.C = cfg->C;
+    LAUNCH(ctx, 1, launch_step(a, cfg->C, true, P, reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int32_t nrec, const double *records,
+                        float *centers, double *stats, double *fitness, float eps, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    if (C < 2 || C > kMaxC || P < 1 || world < 1 || nrec < 1 || !records || !centers)
+        return fail(ctx, PIFCM_EINVAL, "invalid slab finalize arguments");
+    LAUNCH(ctx, 1, launch_slab_finalize(C, P, world, nrec, records, centers, stats, fitness, eps, nullptr,
+                                        reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_slab_halo(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t P, int32_t op, float *U, float *buf,
+                    pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_slab(ctx, grid))) return r;
+    if (P < 1 || op < 0 || op > 3 || !U) return fail(ctx, PIFCM_EINVAL, "invalid halo arguments");
+    const long long plane = (long long)grid->nx * grid->ny;
+    const long long state = plane * (grid->nz + 2);
+    float4 *U4 = reinterpret_cast<float4 *>(U), *B4 = reinterpret_cast<float4 *>(buf);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (op <= 1) {
+        if (!buf) return fail(ctx, PIFCM_EINVAL, "pack needs a buffer");
+        const long long src_plane = op == 0 ? 1 : grid->nz;
+        LAUNCH(ctx, 1, launch_halo_copy(U4 + src_plane * plane, state, B4, plane, plane, P, false, st));
+    } else {
+        const long long dst_plane = op == 2 ? 0 : grid->nz + 1;
+        const bool outside = op == 2 ? grid->z0 == 0 : grid->z0 + grid->nz == grid->nz_total;
+        if (!outside && !buf) return fail(ctx, PIFCM_EINVAL, "unpack of an interior halo needs a buffer");
+        LAUNCH(ctx, 1, launch_halo_copy(B4, plane, U4 + dst_plane * plane, state, plane, P, outside, st));
+    }
     return PIFCM_OK;
 }
 

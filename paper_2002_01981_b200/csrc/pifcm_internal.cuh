@@ -45,6 +45,7 @@ constexpr int kStages = 4;          // plane ring: z-1, z, z+1 resident, z+2 lan
 #endif
 constexpr int kTZ = PIFCM_TZ;       // planes per CTA (z-chunk) for deep grids
 constexpr int kTZMin = 8;           // smallest z-chunk used to fill a wave
+constexpr int kSlabTZ = 16;         // z-chunk of the z-slab mode (global, G-invariant)
 constexpr int kStepThreads = kTX * kWarpsY;
 
 // Pointwise (FCM, lambda = xi = 0) step.
@@ -54,8 +55,10 @@ constexpr int kPwSpan = 8;  // voxels per lane per span
 // ------------------------------------------------------------ step arguments
 struct StepArgs {
     const float *x;      // [nz][ny][pitch]
-    int nx, ny, nz, pitch;
+    int nx, ny, nz, pitch;  // nz = planes in the arrays (slab mode: local planes + 2 halos)
     long long nvox;      // nx*ny*nz  (float4 rows per state)
+    int z_lo, nz_t;      // target planes [z_lo, z_lo + nz_t) in array coordinates
+    int goff, nz_g;      // global z of array plane 0; planes of the whole volume
     const float4 *U_in;  // base of input states
     float4 *U_out;       // base of output states
     const int *in_idx;   // nullable: state p reads U_in + in_idx[p]*nvox (else p*nvox)
@@ -144,5 +147,9 @@ cudaError_t launch_gather_gbest(const float4 *slots, long long nvox, const int *
                                 const float *gbest_c, float4 *U_out, float *c_out,
                                 cudaStream_t st);
 cudaError_t launch_set_lamxi(double *dst, const double *dhdr, cudaStream_t st);
+cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const double *records, float *centers,
+                                 double *stats, double *fitness, float eps, int *status, cudaStream_t st);
+cudaError_t launch_halo_copy(const float4 *src, long long src_state, float4 *dst, long long dst_state,
+                             long long plane, int P, bool zero, cudaStream_t st);
 
 }  // namespace pifcm

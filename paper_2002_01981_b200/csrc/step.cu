@@ -130,6 +130,7 @@ template <int NT>
 __device__ __forceinline__ void finalize_if_last(const StepArgs &a, int p, int nblk) {
     __shared__ int is_last;
     __shared__ double red[NT][kNR];
+    if (a.counters == nullptr) return;  // z-slab mode: records are combined across ranks
     __syncthreads();
     if (threadIdx.x == 0) is_last = (atomicAdd(&a.counters[p], 1u) == (unsigned)(nblk - 1));
     __syncthreads();
@@ -481,8 +482,8 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     const int tile = blockIdx.x;
     const int x0 = (tile % a.tiles_x) * kTX;
     const int y0 = (tile / a.tiles_x) * kTY;
-    const int zb = blockIdx.y * a.tz;
-    const int ze = min(zb + a.tz, a.nz);
+    const int zb = a.z_lo + blockIdx.y * a.tz;
+    const int ze = min(zb + a.tz, a.z_lo + a.nz_t);
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
     const int slot = a.in_idx ? a.in_idx[p] : p;
@@ -667,7 +668,8 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
 
         // ---- per-voxel epilogue: Eq. 5 / 7 ratios, Eq. 4, Eq. 2, partial sums
         float invQ[kRY];
-        const int pz = (z > 0) + (z < a.nz - 1);
+        const int gz = z + a.goff;  // global plane (z-slab mode: z counts from the lower halo)
+        const int pz = (gz > 0) + (gz < a.nz_g - 1);
         if (pz == 2) {
 #pragma unroll
             for (int r = 0; r < kRY; ++r) invQ[r] = invQi[r];
@@ -727,8 +729,8 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
                 bits &= bits - 1;
                 const int row = ty * kRY + 1 + r;
                 const int gxL = x0 + L, gy = y0 + ty * kRY + r;
-                const float4 a4 = attraction_coop<C>(Um, Uc, Up, Xm, Xc, Xp, row, L, gxL, gy, z, a.nx, a.ny,
-                                                     a.nz, a.lam_xi[2 * p], a.lam_xi[2 * p + 1], w2, w3);
+                const float4 a4 = attraction_coop<C>(Um, Uc, Up, Xm, Xc, Xp, row, L, gxL, gy, gz, a.nx, a.ny,
+                                                     a.nz_g, a.lam_xi[2 * p], a.lam_xi[2 * p + 1], w2, w3);
                 if (tx == L) {
                     const float2 A[2] = {make_float2(a4.x, a4.y), make_float2(a4.z, a4.w)};
                     const float xv = Xc[row * kSXP + L + kXOff];
@@ -910,9 +912,20 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
     StepArgs a = a0;
     a.tiles_x = (a.nx + kTX - 1) / kTX;
     a.tiles_y = (a.ny + kTY - 1) / kTY;
-    a.zchunks = step_zchunks(a.nx, a.ny, a.nz, P);
-    a.tz = (a.nz + a.zchunks - 1) / a.zchunks;
-    a.nblk = step_nblk(a.nx, a.ny, a.nz, stencil, P);
+    if (a.nz_g <= 0) {  // whole volume: targets are all planes
+        a.z_lo = 0;
+        a.nz_t = a.nz;
+        a.goff = 0;
+        a.nz_g = a.nz;
+        a.zchunks = step_zchunks(a.nx, a.ny, a.nz, P);
+        a.tz = (a.nz + a.zchunks - 1) / a.zchunks;
+        a.nblk = step_nblk(a.nx, a.ny, a.nz, stencil, P);
+    } else {  // z-slab: fixed global chunks of kSlabTZ planes
+        if (!stencil) return cudaErrorInvalidValue;
+        a.tz = kSlabTZ;
+        a.zchunks = (a.nz_t + kSlabTZ - 1) / kSlabTZ;
+        a.nblk = a.tiles_x * a.tiles_y * a.zchunks;
+    }
     const bool m2 = (a.m == 2.0f);
     switch (C) {
         case 2: return m2 ? launch_t<2, true>(a, stencil, P, st) : launch_t<2, false>(a, stencil, P, st);

@@ -20,7 +20,8 @@ from dataclasses import dataclass
 
 import torch
 
-__all__ = ["shard_range", "allgather_fitness", "ShardedPso", "GpuPsoEngine", "ShardedSegmenter"]
+__all__ = ["shard_range", "allgather_fitness", "ShardedPso", "GpuPsoEngine", "ShardedSegmenter",
+           "slab_range", "SlabIfcm"]
 
 
 def shard_range(P: int, world: int, rank: int) -> tuple[int, int]:
@@ -222,3 +223,141 @@ class ShardedSegmenter:
         labels_host.copy_(self.labels, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return rep
+
+
+# ----------------------------------------------------------------------------
+# z-slab sharding of the IFCM iteration (volumes too large for one GPU)
+SLAB_TZ = 16  # global z-chunk of the slab reductions (kSlabTZ in the library)
+
+
+def slab_range(nz_total: int, world: int, rank: int, tz: int = SLAB_TZ) -> tuple[int, int]:
+    """(z0, nz) of rank's slab: whole 16-plane chunks, split as evenly as possible."""
+    chunks = -(-nz_total // tz)
+    c0, c1 = shard_range(chunks, world, rank)
+    z0 = c0 * tz
+    return z0, min(c1 * tz, nz_total) - z0
+
+
+def _coll_tensor(dist, t):
+    return t.cpu() if dist.get_backend() == "gloo" and t.device.type == "cuda" else t
+
+
+class SlabIfcm:
+    """Jacobi IFCM iterations of P states over a volume split into z-slabs, one
+    per rank.  Per iteration: halo exchange of one U plane per neighbour and
+    state (pack / unpack kernels, send / recv), pifcm_slab_step on the local
+    planes, an all-gather of the per-chunk partial records, pifcm_slab_finalize
+    (Eq. 3 / Eq. 1 in global chunk order: identical on every rank and for any
+    number of slabs)."""
+
+    def __init__(self, ctx, cfg, nx, ny, nz_total, P, dist=None):
+        from .api import _grid
+        self.ctx, self.cfg, self.P, self.dist = ctx, cfg, P, dist
+        self.world = dist.get_world_size() if dist is not None else 1
+        self.rank = dist.get_rank() if dist is not None else 0
+        self.nx, self.ny, self.nz_total = nx, ny, nz_total
+        self.z0, self.nz = slab_range(nz_total, self.world, self.rank)
+        self.grid = _grid(nx, ny, self.nz, z0=self.z0, nz_total=nz_total)
+        self.nrec = ctx.slab_records(self.grid)
+        nrecs = []
+        for r in range(self.world):
+            z0, nz = slab_range(nz_total, self.world, r)
+            nrecs.append(ctx.slab_records(_grid(nx, ny, nz, z0=z0, nz_total=nz_total)))
+        self.nrec_max = max(nrecs)
+        dev = torch.device(f"cuda:{ctx.device}")
+        self.dev = dev
+        plane = nx * ny
+        self.plane = plane
+        self.Ua = torch.zeros((P, (self.nz + 2) * plane, 4), dtype=torch.float32, device=dev)
+        self.Ub = torch.zeros_like(self.Ua)
+        self.rec = torch.zeros((P, self.nrec, 10), dtype=torch.float64, device=dev)
+        self.rec_pad = torch.zeros((P, self.nrec_max, 10), dtype=torch.float64, device=dev)
+        self.gathered = torch.zeros((self.world, P, self.nrec_max, 10), dtype=torch.float64, device=dev)
+        self.halo = {k: torch.zeros((P, plane, 4), dtype=torch.float32, device=dev)
+                     for k in ("send_lo", "send_hi", "recv_lo", "recv_hi")}
+        self.centers = torch.zeros((P, 4), dtype=torch.float32, device=dev)
+        self.stats = torch.zeros((P, 4), dtype=torch.float64, device=dev)
+
+    # -- data in / out
+    def load_x(self, x_full: torch.Tensor):
+        """x_full [nz_total][ny][pitch] (any device) -> the slab with its halo
+        planes (zero outside the volume)."""
+        from .api import pitch_of
+        pitch = pitch_of(self.nx)
+        xs = torch.zeros((self.nz + 2, self.ny, pitch), dtype=torch.float32, device=self.dev)
+        lo, hi = max(self.z0 - 1, 0), min(self.z0 + self.nz + 1, self.nz_total)
+        xs[lo - (self.z0 - 1): hi - (self.z0 - 1)] = x_full[lo:hi].to(self.dev)
+        self.x = xs
+        return xs
+
+    def load_state(self, U_full: torch.Tensor, centers: torch.Tensor):
+        """U_full [P][nz_total*ny*nx][4]: this slab's planes (halos exchanged later)."""
+        pl = self.plane
+        self.Ua[:, pl: pl * (self.nz + 1)] = U_full[:, self.z0 * pl:(self.z0 + self.nz) * pl].to(self.dev)
+        self.centers.copy_(centers.view(self.P, 4))
+        self.stats.zero_()
+
+    def local_U(self) -> torch.Tensor:
+        return self.Ua[:, self.plane: self.plane * (self.nz + 1)]
+
+    # -- one iteration
+    def exchange(self, U):
+        ctx, g, P, h = self.ctx, self.grid, self.P, self.halo
+        up, down = self.rank + 1, self.rank - 1
+        if self.world > 1:
+            ops = []
+            d = self.dist
+            if down >= 0:
+                ctx.slab_halo(g, P, 0, U, h["send_lo"])
+                ops += [("send", h["send_lo"], down), ("recv", h["recv_lo"], down)]
+            if up < self.world:
+                ctx.slab_halo(g, P, 1, U, h["send_hi"])
+                ops += [("send", h["send_hi"], up), ("recv", h["recv_hi"], up)]
+            gloo = d.get_backend() == "gloo"
+            bufs = [(kind, _coll_tensor(d, t), t, peer) for kind, t, peer in ops]
+            if gloo:
+                torch.cuda.current_stream().synchronize()
+            reqs = d.batch_isend_irecv([d.P2POp(d.isend if k == "send" else d.irecv, b, peer)
+                                        for k, b, _, peer in bufs])
+            for r in reqs:
+                r.wait()
+            for k, b, t, _ in bufs:
+                if k == "recv" and b is not t:
+                    t.copy_(b)
+        # halos outside the volume are zero-filled by the library
+        ctx.slab_halo(g, P, 2, U, h["recv_lo"] if self.rank > 0 else None)
+        ctx.slab_halo(g, P, 3, U, h["recv_hi"] if self.rank < self.world - 1 else None)
+
+    def step(self, lam_xi: torch.Tensor, eps: float = 0.0):
+        skipped = self.stats[:, 3] != 0  # converged states are skipped by the step kernel
+        self.exchange(self.Ua)
+        self.ctx.slab_step(self.grid, self.cfg, self.x, self.Ua, self.Ub, self.centers, lam_xi, self.rec,
+                           stats=self.stats)
+        self.rec_pad[:, : self.nrec] = self.rec
+        if self.world > 1:
+            d = self.dist
+            src = _coll_tensor(d, self.rec_pad)
+            out = _coll_tensor(d, self.gathered)
+            if src is not self.rec_pad:
+                torch.cuda.current_stream().synchronize()
+            d.all_gather_into_tensor(out.view(self.world * self.P, self.nrec_max, 10), src)
+            if out is not self.gathered:
+                self.gathered.copy_(out)
+            recs = self.gathered
+        else:
+            recs = self.rec_pad
+        self.ctx.slab_finalize(self.cfg.C, self.P, self.world, self.nrec_max, recs, self.centers,
+                               stats=self.stats, eps=eps)
+        # converged states keep their U (the step kernel skipped them)
+        if bool(skipped.any()):
+            self.Ub[skipped] = self.Ua[skipped]
+        self.Ua, self.Ub = self.Ub, self.Ua
+
+    def run(self, lam_xi: torch.Tensor, iters: int, eps: float = 0.0, check_every: int = 4) -> int:
+        done = 0
+        for it in range(iters):
+            self.step(lam_xi, eps)
+            done = it + 1
+            if eps > 0 and (it + 1) % check_every == 0 and bool((self.stats[:, 3] != 0).all()):
+                break
+        return done

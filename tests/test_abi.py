@@ -42,7 +42,7 @@ def test_version_and_validation_without_gpu(lib):
     from paper_2002_01981_b200 import _abi
     L = _abi.load()
     assert b"sm_100a" in L.pifcm_version()
-    g = _abi.Grid(181, 217, 181, 184)
+    g = _abi.Grid(181, 217, 181, 184, 0, 0)
     cfg = _abi.IfcmCfg(4, 2.0, 1, 1.0, 0, 1e-5, 100)
     pso = _abi.PsoCfg(32, 1, 30, 0, 1e-4, 0.1, 0.5, 1, 0, 0, 0)
     n = ct.c_size_t()
@@ -51,7 +51,7 @@ def test_version_and_validation_without_gpu(lib):
     assert n.value >= 16 * nvox * 65  # 2P+1 slots of AoS-C4 states
     bad = _abi.IfcmCfg(5, 2.0, 1, 1.0, 0, 1e-5, 100)
     assert L.pifcm_workspace_size(ct.byref(g), ct.byref(bad), None, ct.byref(n)) == -1
-    badg = _abi.Grid(181, 217, 181, 181)
+    badg = _abi.Grid(181, 217, 181, 181, 0, 0)
     assert L.pifcm_workspace_size(ct.byref(badg), ct.byref(cfg), None, ct.byref(n)) == -2
     badm = _abi.IfcmCfg(4, 1.0, 1, 1.0, 0, 1e-5, 100)
     assert L.pifcm_workspace_size(ct.byref(g), ct.byref(badm), None, ct.byref(n)) == -1
@@ -59,7 +59,7 @@ def test_version_and_validation_without_gpu(lib):
 
 def test_struct_sizes_match_c():
     from paper_2002_01981_b200 import _abi
-    assert ct.sizeof(_abi.Grid) == 16
+    assert ct.sizeof(_abi.Grid) == 24
     assert ct.sizeof(_abi.IfcmCfg) == 28
     assert ct.sizeof(_abi.PsoCfg) == 64
     assert ct.sizeof(_abi.PsoResult) == 48

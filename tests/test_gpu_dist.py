@@ -67,7 +67,7 @@ def test_sharded_equals_single():
     procs = [cm.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(2)]
+    res = [q.get(timeout=180) for _ in range(2)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
