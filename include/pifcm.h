@@ -305,12 +305,14 @@ int pifcm_slab_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg
                     pifcm_stream stream);
 
 /* Eq. 3 / Eq. 1 from the gathered records [world][P][nrec][10] (rank order,
- * zero-padded to nrec per rank): centres (kept where sum u^m < 1e-12, R9),
- * stats {J, max|du|, iterations += 1, converged = max|du| < eps} and fitness
+ * rank w's counts[w] <= nrec real records first, padding after; counts dev
+ * int32 [world], nullable = all nrec; world <= 64): summed in canonical
+ * (global chunk) order, then centres (kept where sum u^m < 1e-12, R9), stats
+ * {J, max|du|, iterations += 1, converged = max|du| < eps} and fitness
  * (nullable).  Async. */
 int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int32_t nrec,
-                        const double *records, float *centers, double *stats, double *fitness,
-                        float eps, pifcm_stream stream);
+                        const int32_t *counts, const double *records, float *centers, double *stats,
+                        double *fitness, float eps, pifcm_stream stream);
 
 /* Halo planes of P slab states U [P][nz+2][ny][nx][4]:
  *   op 0: pack the first local plane (array plane 1) into buf [P][ny][nx][4]

@@ -88,7 +88,7 @@ SIGNATURES = {
     "pifcm_slab_records": (ct.c_int, [_G, ct.POINTER(ct.c_int32)]),
     "pifcm_slab_step": (ct.c_int, [_vp, _G, _C, _vp, _vp, _vp, _vp, _vp, ct.c_int32, _vp, _vp, _vp]),
     "pifcm_slab_finalize": (ct.c_int, [_vp, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, _vp, _vp, _vp,
-                                       _vp, ct.c_float, _vp]),
+                                       _vp, _vp, ct.c_float, _vp]),
     "pifcm_slab_halo": (ct.c_int, [_vp, _G, ct.c_int32, ct.c_int32, _vp, _vp, _vp]),
 }
 

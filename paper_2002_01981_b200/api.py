@@ -310,9 +310,10 @@ class Context:
                                           _ptr(records), _stream(stream)))
 
     def slab_finalize(self, C, P, world, nrec, records, centers, stats=None, fitness=None, eps=0.0,
-                      stream=None):
-        self._ck(self.lib.pifcm_slab_finalize(self._h, C, P, world, nrec, _ptr(records), _ptr(centers),
-                                              _ptr(stats), _ptr(fitness), eps, _stream(stream)))
+                      counts=None, stream=None):
+        """counts: device int32 [world] real records per rank (None: all nrec)."""
+        self._ck(self.lib.pifcm_slab_finalize(self._h, C, P, world, nrec, _ptr(counts), _ptr(records),
+                                              _ptr(centers), _ptr(stats), _ptr(fitness), eps, _stream(stream)))
 
     def slab_halo(self, grid, P, op, U, buf=None, stream=None):
         self._ck(self.lib.pifcm_slab_halo(self._h, ct.byref(grid), P, op, _ptr(U), _ptr(buf), _stream(stream)))

@@ -84,23 +84,35 @@ cudaError_t launch_fixup_copy(const float4 *scratch, float4 *out, long long nvox
 }
 
 // ---------------------------------------------------------------- z-slab
-// Records of all ranks, gathered [world][P][nrec][kNR] (zero-padded to nrec
-// per rank), summed for state p in (rank, record) order -- i.e. in global
-// z-chunk order, the same order for any number of slabs -- then Eq. 3 / Eq. 1.
+// Records of all ranks, gathered [world][P][nrec][kNR] (rank w holds
+// counts[w] <= nrec real records, the rest is padding), summed for state p in
+// canonical order -- rank-major, record-minor over the real records only,
+// which is the global z-chunk order and the same sequence for any number of
+// slabs -- then Eq. 3 / Eq. 1.  The thread assignment depends only on the
+// canonical index, so the fp64 result is identical for any slab count.
 __global__ void __launch_bounds__(kFinThreads) k_slab_finalize(int C, int P, int world, int nrec,
-                                                             const double *rec, float *centers,
-                                                             double *stats, double *fitness, float eps,
-                                                             int *status) {
+                                                             const int *counts, const double *rec,
+                                                             float *centers, double *stats, double *fitness,
+                                                             float eps, int *status) {
     __shared__ double red[kFinThreads][kNR];
+    __shared__ int cnt[64];
     const int p = blockIdx.x;
     if (stats && stats[4 * p + 3] != 0.0) return;
-    const long long total = (long long)world * nrec;
+    for (int w = threadIdx.x; w < world && w < 64; w += blockDim.x) cnt[w] = counts ? counts[w] : nrec;
+    __syncthreads();
+    long long total = 0;
+    for (int w = 0; w < world; ++w) total += cnt[w];
     double v[kNR];
 #pragma unroll
     for (int r = 0; r < kNR; ++r) v[r] = 0.0;
-    for (long long b = threadIdx.x; b < total; b += kFinThreads) {
-        const long long w = b / nrec, k = b - w * nrec;
-        const double *src = rec + ((w * P + p) * nrec + k) * kNR;
+    int w = 0;
+    long long base = 0;  // canonical index of rank w's first record
+    for (long long c = threadIdx.x; c < total; c += kFinThreads) {
+        while (c >= base + cnt[w]) {
+            base += cnt[w];
+            ++w;
+        }
+        const double *src = rec + (((long long)w * P + p) * nrec + (c - base)) * kNR;
 #pragma unroll
         for (int r = 0; r < kNR - 1; ++r) v[r] += src[r];
         v[kNR - 1] = fmax(v[kNR - 1], src[kNR - 1]);
@@ -133,9 +145,12 @@ __global__ void __launch_bounds__(kFinThreads) k_slab_finalize(int C, int P, int
     }
 }
 
-cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const double *records, float *centers,
-                                 double *stats, double *fitness, float eps, int *status, cudaStream_t st) {
-    k_slab_finalize<<<P, kFinThreads, 0, st>>>(C, P, world, nrec, records, centers, stats, fitness, eps, status);
+cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const int *counts, const double *records,
+                                 float *centers, double *stats, double *fitness, float eps, int *status,
+                                 cudaStream_t st) {
+    if (world > 64) return cudaErrorInvalidValue;
+    k_slab_finalize<<<P, kFinThreads, 0, st>>>(C, P, world, nrec, counts, records, centers, stats, fitness, eps,
+                                               status);
     return cudaGetLastError();
 }
 

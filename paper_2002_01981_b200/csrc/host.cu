@@ -181,7 +181,7 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
              const float4 *Uin, float4 *Uout, const int *in_idx, const int *out_idx,
              float *centers, const double *lamxi, bool stencil, int first, int P,
              double *partials, double *fitness, double *stats, float eps, int *status,
-             const int *stop, cudaStream_t st, int n_in_states, unsigned *counters) {
+             const int *stop, cudaStream_t st, int n_in_states, unsigned *counters, bool canonical = false) {
     StepArgs a{};
     a.x = x;
     a.nx = g->nx; a.ny = g->ny; a.nz = g->nz; a.pitch = g->pitch;
@@ -193,7 +193,8 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     a.q_mode = cfg->q_mode; a.first = first;
     a.n_in_states = n_in_states;
     a.want_du = (stats != nullptr) ? 1 : 0;
-    a.counters = counters;
+    a.counters = canonical ? nullptr : counters;
+    a.canonical = canonical ? 1 : 0;
     a.C = cfg->C;
     a.fitness = fitness;
     a.stats_out = stats;
@@ -219,7 +220,13 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
         ctx->t_launches[cls] += 1;
     }
     // Eq. 3 / Eq. 1 finalisation is fused: the last CTA of each state sums the
-    // partial records (finalize_if_last in step.cu)
+    // partial records (finalize_if_last in step.cu); in the canonical
+    // decomposition the records are summed by the slab finaliser instead
+    if (canonical) {
+        const int nrec = ((g->nx + kTX - 1) / kTX) * ((g->ny + kTY - 1) / kTY) * ((g->nz + kSlabTZ - 1) / kSlabTZ);
+        LAUNCH(ctx, 1, launch_slab_finalize(cfg->C, P, 1, nrec, nullptr, partials, centers, stats, fitness, eps,
+                                            status, st));
+    }
     return PIFCM_OK;
 }
 
@@ -565,7 +572,8 @@ static int run_until(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *
     for (t = 1; t <= cfg->max_iter; ++t) {
         int r = run_step(ctx, g, cfg, x, slots + (long long)src * nvox, slots + (long long)dst * nvox, nullptr,
                          nullptr, centers, lamxi, stencil, (fcm_first && t == 1) ? 1 : 0, 1, partials,
-                         nullptr, stats, cfg->eps, status, nullptr, st, 1, counters);
+                         nullptr, stats, cfg->eps, status, nullptr, st, 1, counters,
+                         /*canonical: identical to the z-slab sharded final IFCM*/ stencil);
         if (r) return r;
         const int tmp = src; src = dst; dst = tmp;
         if (t % check_every == 0 || t == cfg->max_iter) {
@@ -760,12 +768,13 @@ int pifcm_slab_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg
     return PIFCM_OK;
 }
 
-int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int32_t nrec, const double *records,
-                        float *centers, double *stats, double *fitness, float eps, pifcm_stream stream) {
+int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int32_t nrec, const int32_t *counts,
+                        const double *records, float *centers, double *stats, double *fitness, float eps,
+                        pifcm_stream stream) {
     if (!ctx) return PIFCM_EINVAL;
-    if (C < 2 || C > kMaxC || P < 1 || world < 1 || nrec < 1 || !records || !centers)
+    if (C < 2 || C > kMaxC || P < 1 || world < 1 || world > 64 || nrec < 1 || !records || !centers)
         return fail(ctx, PIFCM_EINVAL, "invalid slab finalize arguments");
-    LAUNCH(ctx, 1, launch_slab_finalize(C, P, world, nrec, records, centers, stats, fitness, eps, nullptr,
+    LAUNCH(ctx, 1, launch_slab_finalize(C, P, world, nrec, counts, records, centers, stats, fitness, eps, nullptr,
                                         reinterpret_cast<cudaStream_t>(stream)));
     return PIFCM_OK;
 }

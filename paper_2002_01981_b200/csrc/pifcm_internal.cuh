@@ -59,6 +59,7 @@ struct StepArgs {
     long long nvox;      // nx*ny*nz  (float4 rows per state)
     int z_lo, nz_t;      // target planes [z_lo, z_lo + nz_t) in array coordinates
     int goff, nz_g;      // global z of array plane 0; planes of the whole volume
+    int canonical;       // whole volume with the fixed global 16-plane chunks of the slab mode
     const float4 *U_in;  // base of input states
     float4 *U_out;       // base of output states
     const int *in_idx;   // nullable: state p reads U_in + in_idx[p]*nvox (else p*nvox)
@@ -147,8 +148,9 @@ cudaError_t launch_gather_gbest(const float4 *slots, long long nvox, const int *
                                 const float *gbest_c, float4 *U_out, float *c_out,
                                 cudaStream_t st);
 cudaError_t launch_set_lamxi(double *dst, const double *dhdr, cudaStream_t st);
-cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const double *records, float *centers,
-                                 double *stats, double *fitness, float eps, int *status, cudaStream_t st);
+cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const int *counts, const double *records,
+                                 float *centers, double *stats, double *fitness, float eps, int *status,
+                                 cudaStream_t st);
 cudaError_t launch_halo_copy(const float4 *src, long long src_state, float4 *dst, long long dst_state,
                              long long plane, int P, bool zero, cudaStream_t st);
 

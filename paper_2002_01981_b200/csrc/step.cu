@@ -912,7 +912,15 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
     StepArgs a = a0;
     a.tiles_x = (a.nx + kTX - 1) / kTX;
     a.tiles_y = (a.ny + kTY - 1) / kTY;
-    if (a.nz_g <= 0) {  // whole volume: targets are all planes
+    if (a.canonical) {  // whole volume in the slab mode's canonical decomposition
+        a.z_lo = 0;
+        a.nz_t = a.nz;
+        a.goff = 0;
+        a.nz_g = a.nz;
+        a.tz = kSlabTZ;
+        a.zchunks = (a.nz + kSlabTZ - 1) / kSlabTZ;
+        a.nblk = a.tiles_x * a.tiles_y * a.zchunks;
+    } else if (a.nz_g <= 0) {  // whole volume: targets are all planes
         a.z_lo = 0;
         a.nz_t = a.nz;
         a.goff = 0;

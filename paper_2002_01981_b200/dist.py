@@ -154,8 +154,10 @@ class ShardedSegmenter:
 
     Every rank normalises, fits the GMM and runs the FCM start (identical,
     deterministic), the PSO generations are sharded, the gbest state is
-    broadcast from its owner and every rank runs the final IFCM and argmax.
-    Labels are bit-identical to the single-process pifcm_segment."""
+    broadcast from its owner, the final IFCM runs z-slab sharded (SlabIfcm)
+    and each rank's slab labels are all-gathered.  pifcm_segment runs its
+    final IFCM in the same canonical 16-plane decomposition, so labels are
+    bit-identical to the single-process pifcm_segment for any world size."""
 
     def __init__(self, ctx, cfg, pso, shape, dist=None):
         self.ctx, self.cfg, self.pso = ctx, cfg, pso
@@ -167,6 +169,13 @@ class ShardedSegmenter:
         self.Ua = torch.zeros((1, nvox, 4), dtype=torch.float32, device=self.dev)
         self.cen = torch.empty((1, 4), dtype=torch.float32, device=self.dev)
         self.engine = None
+        world = dist.get_world_size() if dist is not None else 1
+        # fewer 16-plane chunks than ranks: every rank runs the whole volume
+        self.slab = SlabIfcm(ctx, cfg, self.nx, self.ny, self.nz, 1,
+                             dist if -(-self.nz // SLAB_TZ) >= world else None)
+        w = self.slab.world
+        self.lab_counts = [slab_range(self.nz, w, r)[1] * self.nx * self.ny for r in range(w)]
+        self.lab_pad = torch.zeros((w, max(self.lab_counts)), dtype=torch.uint8, device=self.dev)
 
     def segment(self, vol: torch.Tensor) -> dict:
         from .api import _grid
@@ -202,11 +211,15 @@ class ShardedSegmenter:
         ev[3].record()
         # Alg. 1 step 11: final IFCM at (lambda*, xi*) until eps, then argmax
         lx = torch.tensor([[out.lam, out.xi]], dtype=torch.float64, device=self.dev)
-        stats.zero_()
-        ctx.iterate(x, self.Ua, self.Ub, self.cen, lx, cfg, iters=cfg.max_iter, stats=stats, nx=nx)
-        labels = ctx.argmax(self.Ub[0], nx, ny, nz, cfg.C)
+        sl = self.slab
+        sl.load_x(x)
+        sl.load_state(self.Ua, self.cen)
+        sl.run(lx, cfg.max_iter, eps=cfg.eps)
+        self.cen.copy_(sl.centers)
+        loc = ctx.argmax(sl.local_U()[0], nx, ny, sl.nz, cfg.C)
+        labels = self._gather_labels(loc)
         ev[4].record()
-        final_iters = int(stats[0, 2].item())
+        final_iters = int(sl.stats[0, 2].item())
         torch.cuda.synchronize()
         self.labels = labels
         return {"lambda": out.lam, "xi": out.xi, "J": out.J, "generations": out.generations,
@@ -215,6 +228,22 @@ class ShardedSegmenter:
                 "t_norm": ev[0].elapsed_time(ev[1]) * 1e-3, "t_init": ev[1].elapsed_time(ev[2]) * 1e-3,
                 "t_pso": ev[2].elapsed_time(ev[3]) * 1e-3, "t_final": ev[3].elapsed_time(ev[4]) * 1e-3,
                 "t_total": ev[0].elapsed_time(ev[4]) * 1e-3}
+
+    def _gather_labels(self, loc: torch.Tensor) -> torch.Tensor:
+        sl = self.slab
+        if sl.world == 1:
+            return loc
+        d = sl.dist
+        self.lab_pad[sl.rank, : loc.numel()] = loc.view(-1)
+        src = _coll_tensor(d, self.lab_pad[sl.rank].contiguous())
+        out = _coll_tensor(d, self.lab_pad)
+        if src.device.type == "cpu":
+            torch.cuda.current_stream().synchronize()
+        d.all_gather_into_tensor(out.view(-1), src)
+        if out is not self.lab_pad:
+            self.lab_pad.copy_(out)
+        return torch.cat([self.lab_pad[r, :n] for r, n in enumerate(self.lab_counts)]).view(
+            self.nz, self.ny, self.nx)
 
     def segment_host(self, vol_host: torch.Tensor, labels_host: torch.Tensor) -> dict:
         """Host (pinned) u8 volume in, host labels out (H2D / D2H inside)."""
@@ -264,6 +293,7 @@ class SlabIfcm:
             z0, nz = slab_range(nz_total, self.world, r)
             nrecs.append(ctx.slab_records(_grid(nx, ny, nz, z0=z0, nz_total=nz_total)))
         self.nrec_max = max(nrecs)
+        self.counts = torch.tensor(nrecs, dtype=torch.int32, device=torch.device(f"cuda:{ctx.device}"))
         dev = torch.device(f"cuda:{ctx.device}")
         self.dev = dev
         plane = nx * ny
@@ -296,6 +326,7 @@ class SlabIfcm:
         self.Ua[:, pl: pl * (self.nz + 1)] = U_full[:, self.z0 * pl:(self.z0 + self.nz) * pl].to(self.dev)
         self.centers.copy_(centers.view(self.P, 4))
         self.stats.zero_()
+        self.swaps = 0
 
     def local_U(self) -> torch.Tensor:
         return self.Ua[:, self.plane: self.plane * (self.nz + 1)]
@@ -329,7 +360,9 @@ class SlabIfcm:
         ctx.slab_halo(g, P, 3, U, h["recv_hi"] if self.rank < self.world - 1 else None)
 
     def step(self, lam_xi: torch.Tensor, eps: float = 0.0):
-        skipped = self.stats[:, 3] != 0  # converged states are skipped by the step kernel
+        """One iteration (no host synchronisation).  A converged state is
+        skipped by the step kernel, so its latest U stays in the buffer its
+        last real step wrote: sync_states() moves it back into Ua."""
         self.exchange(self.Ua)
         self.ctx.slab_step(self.grid, self.cfg, self.x, self.Ua, self.Ub, self.centers, lam_xi, self.rec,
                            stats=self.stats)
@@ -347,11 +380,18 @@ class SlabIfcm:
         else:
             recs = self.rec_pad
         self.ctx.slab_finalize(self.cfg.C, self.P, self.world, self.nrec_max, recs, self.centers,
-                               stats=self.stats, eps=eps)
-        # converged states keep their U (the step kernel skipped them)
-        if bool(skipped.any()):
-            self.Ub[skipped] = self.Ua[skipped]
+                               stats=self.stats, eps=eps, counts=self.counts)
         self.Ua, self.Ub = self.Ub, self.Ua
+        self.swaps += 1
+
+    def sync_states(self):
+        """After steps that skipped converged states: state p's latest U was
+        written by its stats[p, 2]-th step, into the buffer that was current
+        after that many swaps; copy it into Ua where that is the other one."""
+        done = self.stats[:, 2].to(torch.int64).cpu()
+        for p in range(self.P):
+            if (int(done[p]) - self.swaps) % 2:
+                self.Ua[p].copy_(self.Ub[p])
 
     def run(self, lam_xi: torch.Tensor, iters: int, eps: float = 0.0, check_every: int = 4) -> int:
         done = 0
@@ -360,4 +400,5 @@ class SlabIfcm:
             done = it + 1
             if eps > 0 and (it + 1) % check_every == 0 and bool((self.stats[:, 3] != 0).all()):
                 break
+        self.sync_states()
         return done

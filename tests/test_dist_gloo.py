@@ -133,3 +133,18 @@ def test_sharded_pso_equals_single_process(orc, P, world):
         assert (log == r.trace_f).all()       # identical fitness vectors every generation
         assert (full == np.arange(P)).all()   # uneven ranges gathered in particle order
         assert has == (rank == owner)
+
+
+def test_slab_range():
+    from paper_2002_01981_b200.dist import SLAB_TZ, slab_range
+    assert SLAB_TZ == 16
+    assert [slab_range(181, 4, r) for r in range(4)] == [(0, 48), (48, 48), (96, 48), (144, 37)]
+    for nz in (1, 15, 16, 17, 40, 181, 512):
+        chunks = -(-nz // 16)
+        for w in range(1, min(chunks, 8) + 1):
+            rs = [slab_range(nz, w, r) for r in range(w)]
+            assert rs[0][0] == 0 and sum(n for _, n in rs) == nz
+            assert all(z0 % 16 == 0 and n > 0 for z0, n in rs)            # whole global chunks
+            assert all(rs[i][0] + rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+            ch = [-(-n // 16) for _, n in rs]
+            assert max(ch) - min(ch) <= 1

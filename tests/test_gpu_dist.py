@@ -12,9 +12,9 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _case():
+def _case(nz):
     from inputs import add_noise_u8, cube_phantom
-    img, _ = cube_phantom(30, 26, 12, (0.1, 0.35, 0.65, 0.9))
+    img, _ = cube_phantom(30, 26, nz, (0.1, 0.35, 0.65, 0.9))
     return add_noise_u8(img, 7.0, 6)
 
 
@@ -22,7 +22,7 @@ CFG = dict(C=4)
 PSO = dict(P=5, max_gen=4, patience=0, seed=31)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, nz, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -30,10 +30,10 @@ def _worker(rank, world, port, q):
     from paper_2002_01981_b200 import Context, IfcmConfig, PsoConfig
     from paper_2002_01981_b200.dist import ShardedSegmenter
     ctx = Context(0)
-    vol = _case()
+    vol = _case(nz)
     seg = ShardedSegmenter(ctx, IfcmConfig(**CFG), PsoConfig(**PSO), vol.shape, dist)
     rep = seg.segment(torch.as_tensor(vol, device="cuda:0"))
-    q.put((rank, seg.labels.cpu().numpy(), rep["lambda"], rep["xi"], rep["final_iters"]))
+    q.put((rank, seg.labels.cpu().numpy(), rep["lambda"], rep["xi"], rep["final_iters"], rep["centers"]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -46,11 +46,14 @@ def _port():
     return p
 
 
-def test_sharded_equals_single():
+# nz = 12: one 16-plane chunk, the final IFCM runs replicated; nz = 40: three
+# chunks, z-slab sharded 2 + 1 (uneven record counts)
+@pytest.mark.parametrize("nz", [12, 40])
+def test_sharded_equals_single(nz):
     from paper_2002_01981_b200 import Context, IfcmConfig, PsoConfig
     from paper_2002_01981_b200.dist import ShardedSegmenter
     ctx = Context(0)
-    vol = _case()
+    vol = _case(nz)
     vt = torch.as_tensor(vol, device="cuda:0")
     lab, _, rep = ctx.segment(vt, IfcmConfig(**CFG), PsoConfig(**PSO))
     ref = lab.cpu().numpy()
@@ -60,17 +63,19 @@ def test_sharded_equals_single():
     assert (seg.labels.cpu().numpy() == ref).all()
     assert (r1["lambda"], r1["xi"]) == (rep["lambda"], rep["xi"])
     assert r1["final_iters"] == rep["final_iters"] and r1["fcm_iters"] == rep["fcm_iters"]
+    assert r1["centers"] == rep["centers"]
     # two ranks on the same GPU (gloo collectives through host memory)
     cm = mp.get_context("spawn")
     q = cm.Queue()
     port = _port()
-    procs = [cm.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [cm.Process(target=_worker, args=(r, 2, port, nz, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=180) for _ in range(2)]
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    for rank, labels, lam, xi, fi in res:
+    for rank, labels, lam, xi, fi, cen in res:
         assert (labels == ref).all()
         assert (lam, xi) == (rep["lambda"], rep["xi"])
+        assert fi == rep["final_iters"] and cen == rep["centers"]

@@ -55,9 +55,10 @@ def _virtual_slabs(ctx, world, iters, lx):
         s.z0, s.nz = slab_range(NZ, world, r)
         s.grid = _grid(NX, NY, s.nz, z0=s.z0, nz_total=NZ)
         s.nrec = ctx.slab_records(s.grid)
-        s.nrec_max = max(ctx.slab_records(_grid(NX, NY, slab_range(NZ, world, q)[1],
-                                                z0=slab_range(NZ, world, q)[0], nz_total=NZ))
-                         for q in range(world))
+        nrecs = [ctx.slab_records(_grid(NX, NY, slab_range(NZ, world, q)[1],
+                                        z0=slab_range(NZ, world, q)[0], nz_total=NZ)) for q in range(world)]
+        s.nrec_max = max(nrecs)
+        s.counts = torch.tensor(nrecs, dtype=torch.int32, device=dev)
         pl = NX * NY
         s.Ua = torch.zeros((P, (s.nz + 2) * pl, 4), device=dev)
         s.Ub = torch.zeros_like(s.Ua)
@@ -84,7 +85,7 @@ def _virtual_slabs(ctx, world, iters, lx):
             s.rec_pad[:, : s.nrec] = s.rec
         gathered = torch.stack([s.rec_pad for s in slabs])
         for s in slabs:
-            s.ctx.slab_finalize(C, P, world, s.nrec_max, gathered, s.centers, stats=s.stats)
+            s.ctx.slab_finalize(C, P, world, s.nrec_max, gathered, s.centers, stats=s.stats, counts=s.counts)
             s.Ua, s.Ub = s.Ub, s.Ua
     U_full = torch.cat([s.local_U() for s in slabs], dim=1)
     return U_full, slabs[0].centers.clone(), slabs[0].stats.clone(), [s.centers for s in slabs]
