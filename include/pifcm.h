@@ -86,10 +86,11 @@ typedef struct pifcm_ctx pifcm_ctx;
  * z-slab mode (nz_total > 0, only for the pifcm_slab_* calls): this process
  * holds the planes [z0, z0 + nz) of a volume of nz_total planes; its x and U
  * arrays then have nz + 2 planes, plane 0 being global z0 - 1 and plane
- * nz + 1 global z0 + nz (halo planes).  z0 must be a multiple of 16 and every
- * slab but the last must have a multiple of 16 planes (the slab reductions
- * use fixed global chunks of 16 planes, which makes them independent of the
- * number of slabs).  nz_total = 0 (or z0 = 0, nz_total = nz): whole volume. */
+ * nz + 1 global z0 + nz (halo planes).  With tz = pifcm_slab_chunk(nx, ny,
+ * nz_total), z0 must be a multiple of tz and every slab but the last must
+ * have a multiple of tz planes (the slab reductions use global chunks of tz
+ * planes, which makes them independent of the number of slabs).
+ * nz_total = 0 (or z0 = 0, nz_total = nz): whole volume. */
 typedef struct {
     int32_t nx, ny, nz;
     int32_t pitch;    /* elements per x row of the intensity volume; >= nx, % 4 == 0 */
@@ -287,8 +288,15 @@ int pifcm_segment_host(pifcm_ctx *ctx, const uint8_t *vol_host, int32_t nx, int3
  * runs pifcm_slab_step, all-gathers the per-chunk partial records of all
  * ranks in rank order and calls pifcm_slab_finalize, which applies Eq. 3 /
  * Eq. 1 identically on every rank.  Because the records are
- * keyed by fixed global 16-plane chunks, centres and J are bit-identical for
- * any number of slabs. */
+ * keyed by global z-chunks whose size depends on the volume alone
+ * (pifcm_slab_chunk), centres and J are bit-identical for any number of
+ * slabs, and equal to the single-GPU final IFCM of pifcm_segment, which runs
+ * in the same decomposition. */
+
+/* Planes per global z-chunk for a volume nx x ny x nz_total (host-only, no
+ * GPU needed): every slab but the last holds a multiple of *tz planes and
+ * starts at a multiple of *tz.  PIFCM_EINVAL on NULL / non-positive dims. */
+int pifcm_slab_chunk(int32_t nx, int32_t ny, int32_t nz_total, int32_t *tz);
 
 /* Partial records per state that pifcm_slab_step writes for this slab. */
 int pifcm_slab_records(const pifcm_grid *grid, int32_t *nrec);

@@ -298,6 +298,10 @@ class Context:
 
 
     # ------------------------------------------------------------ z-slab
+    def slab_chunk(self, nx, ny, nz_total) -> int:
+        """Planes per global z-chunk of the slab / canonical decomposition."""
+        return slab_chunk(nx, ny, nz_total, self.lib)
+
     def slab_records(self, grid) -> int:
         n = ct.c_int32()
         self._ck(self.lib.pifcm_slab_records(ct.byref(grid), ct.byref(n)))
@@ -317,6 +321,16 @@ class Context:
 
     def slab_halo(self, grid, P, op, U, buf=None, stream=None):
         self._ck(self.lib.pifcm_slab_halo(self._h, ct.byref(grid), P, op, _ptr(U), _ptr(buf), _stream(stream)))
+
+
+def slab_chunk(nx, ny, nz_total, lib=None) -> int:
+    """pifcm_slab_chunk (host-only query, no GPU needed)."""
+    lib = lib or _abi.load()
+    tz = ct.c_int32()
+    rc = lib.pifcm_slab_chunk(nx, ny, nz_total, ct.byref(tz))
+    if rc != 0:
+        raise PifcmError(rc, "pifcm_slab_chunk: invalid dimensions")
+    return tz.value
 
 
 def report_dict(rep: _abi.Report, C: int) -> dict:

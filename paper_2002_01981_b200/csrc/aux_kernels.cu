@@ -9,57 +9,13 @@
 namespace pifcm {
 
 // ---------------------------------------------------------------- finalize
-// Fixed-order fp64 sum of the per-block partial records of state p, then
-// Eq. 3: c_j = sum u^m x / sum u^m (keep c_j if the sum < 1e-12,
-// R9) and Eq. 1: J = sum of the per-voxel costs.
-constexpr int kFinThreads = 256;
-
-__global__ void __launch_bounds__(kFinThreads) k_finalize(const FinalizeArgs a) {
-    __shared__ double red[kFinThreads][kNR];
-    const int p = blockIdx.x;
-    if (a.stop && *a.stop) return;
-    if (a.stats && a.stats[4 * p + 3] != 0.0) return;
-    const double *src = a.partials + (long long)p * a.nblk * kNR;
-    double v[kNR];
-#pragma unroll
-    for (int r = 0; r < kNR; ++r) v[r] = 0.0;
-    for (int b = threadIdx.x; b < a.nblk; b += kFinThreads) {
-#pragma unroll
-        for (int r = 0; r < kNR - 1; ++r) v[r] += src[(long long)b * kNR + r];
-        v[kNR - 1] = fmax(v[kNR - 1], src[(long long)b * kNR + kNR - 1]);
-    }
-#pragma unroll
-    for (int r = 0; r < kNR; ++r) red[threadIdx.x][r] = v[r];
-    __syncthreads();
-    for (int s = kFinThreads / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-#pragma unroll
-            for (int r = 0; r < kNR - 1; ++r) red[threadIdx.x][r] += red[threadIdx.x + s][r];
-            red[threadIdx.x][kNR - 1] = fmax(red[threadIdx.x][kNR - 1], red[threadIdx.x + s][kNR - 1]);
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        const double J = red[0][2 * kMaxC], du = red[0][2 * kMaxC + 1];
-        for (int j = 0; j < a.C; ++j) {
-            const double num = red[0][j], den = red[0][kMaxC + j];
-            if (den >= kDenEps) a.centers[4 * p + j] = (float)(num / den);
-        }
-        if (a.fitness) a.fitness[p] = J;
-        if (a.stats) {
-            a.stats[4 * p + 0] = J;
-            a.stats[4 * p + 1] = du;
-            a.stats[4 * p + 2] += 1.0;
-            a.stats[4 * p + 3] = (a.eps > 0.f && du < (double)a.eps) ? 1.0 : 0.0;
-        }
-        if (!isfinite(J) && a.status) atomicExch(a.status, (int)PIFCM_ENUMERIC);
-    }
-}
-
-cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st) {
-    k_finalize<<<a.P, kFinThreads, 0, st>>>(a);
-    return cudaGetLastError();
-}
+// Eq. 3 c_j = sum u^m x / sum u^m (keep c_j if the sum < 1e-12,
+// R9) and Eq. 1 J from per-chunk fp64 partial records.  One CTA
+// is finalised by the last step CTA itself (finalize_if_last in step.cu);
+// the z-slab records gathered across ranks by k_slab_finalize below, with
+// the same thread count and summation order, so the single-GPU canonical
+// run and any slab split give bit-identical centres and J.
+constexpr int kFinThreads = kStepThreads;
 
 // After an early-converged pifcm_iterate: the last U of state p was written
 // by iteration stats[p][2]; iterations t with (iters - t) odd wrote to the

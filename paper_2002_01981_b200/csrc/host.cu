@@ -193,7 +193,7 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     a.q_mode = cfg->q_mode; a.first = first;
     a.n_in_states = n_in_states;
     a.want_du = (stats != nullptr) ? 1 : 0;
-    a.counters = canonical ? nullptr : counters;
+    a.counters = counters;
     a.canonical = canonical ? 1 : 0;
     a.C = cfg->C;
     a.fitness = fitness;
@@ -220,13 +220,8 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
         ctx->t_launches[cls] += 1;
     }
     // Eq. 3 / Eq. 1 finalisation is fused: the last CTA of each state sums the
-    // partial records (finalize_if_last in step.cu); in the canonical
-    // decomposition the records are summed by the slab finaliser instead
-    if (canonical) {
-        const int nrec = ((g->nx + kTX - 1) / kTX) * ((g->ny + kTY - 1) / kTY) * ((g->nz + kSlabTZ - 1) / kSlabTZ);
-        LAUNCH(ctx, 1, launch_slab_finalize(cfg->C, P, 1, nrec, nullptr, partials, centers, stats, fitness, eps,
-                                            status, st));
-    }
+    // partial records (finalize_if_last in step.cu) -- in the canonical
+    // decomposition exactly as k_slab_finalize sums the records of a slab split
     return PIFCM_OK;
 }
 
@@ -726,9 +721,10 @@ static int check_slab(pifcm_ctx *ctx, const pifcm_grid *g) {
     if (g->nz_total < 1) return fail(ctx, PIFCM_EINVAL, "slab calls need nz_total >= 1");
     if (g->z0 < 0 || g->z0 + g->nz > g->nz_total)
         return fail(ctx, PIFCM_EINVAL, "slab [%d, %d) outside [0, %d)", g->z0, g->z0 + g->nz, g->nz_total);
-    if (g->z0 % kSlabTZ != 0) return fail(ctx, PIFCM_EINVAL, "slab z0 = %d is not a multiple of %d", g->z0, kSlabTZ);
-    if (g->z0 + g->nz != g->nz_total && g->nz % kSlabTZ != 0)
-        return fail(ctx, PIFCM_EINVAL, "a slab other than the last must hold a multiple of %d planes", kSlabTZ);
+    const int tz = slab_tz(g->nx, g->ny, g->nz_total);
+    if (g->z0 % tz != 0) return fail(ctx, PIFCM_EINVAL, "slab z0 = %d is not a multiple of %d", g->z0, tz);
+    if (g->z0 + g->nz != g->nz_total && g->nz % tz != 0)
+        return fail(ctx, PIFCM_EINVAL, "a slab other than the last must hold a multiple of %d planes", tz);
     if ((long long)g->nx * g->ny * (g->nz + 2) >= (1LL << 31)) return fail(ctx, PIFCM_EINVAL, "slab too large");
     return PIFCM_OK;
 }
@@ -737,7 +733,14 @@ int pifcm_slab_records(const pifcm_grid *grid, int32_t *nrec) {
     if (!nrec) return PIFCM_EINVAL;
     int r;
     if ((r = check_slab(nullptr, grid))) return r;
-    *nrec = ((grid->nx + kTX - 1) / kTX) * ((grid->ny + kTY - 1) / kTY) * ((grid->nz + kSlabTZ - 1) / kSlabTZ);
+    const int tz = slab_tz(grid->nx, grid->ny, grid->nz_total);
+    *nrec = ((grid->nx + kTX - 1) / kTX) * ((grid->ny + kTY - 1) / kTY) * ((grid->nz + tz - 1) / tz);
+    return PIFCM_OK;
+}
+
+int pifcm_slab_chunk(int32_t nx, int32_t ny, int32_t nz_total, int32_t *tz) {
+    if (!tz || nx < 1 || ny < 1 || nz_total < 1) return PIFCM_EINVAL;
+    *tz = slab_tz(nx, ny, nz_total);
     return PIFCM_OK;
 }
 

@@ -45,7 +45,6 @@ constexpr int kStages = 4;          // plane ring: z-1, z, z+1 resident, z+2 lan
 #endif
 constexpr int kTZ = PIFCM_TZ;       // planes per CTA (z-chunk) for deep grids
 constexpr int kTZMin = 8;           // smallest z-chunk used to fill a wave
-constexpr int kSlabTZ = 16;         // z-chunk of the z-slab mode (global, G-invariant)
 constexpr int kStepThreads = kTX * kWarpsY;
 
 // Pointwise (FCM, lambda = xi = 0) step.
@@ -85,17 +84,6 @@ struct StepArgs {
     int *status;         // nullable: PIFCM_ENUMERIC on a non-finite J
 };
 
-struct FinalizeArgs {
-    const double *partials; // [P][nblk][kNR]
-    int nblk, C, P;
-    float *centers;         // [P][4] in/out
-    double *fitness;        // nullable [P] (offset to this process's first particle)
-    double *stats;          // nullable [P][4] {J, du, iters, converged}
-    float eps;              // convergence threshold on max|du| (<=0: never)
-    int *status;            // nullable: set to PIFCM_ENUMERIC on non-finite J
-    const int *stop;        // nullable
-};
-
 // Swarm state in the workspace (all device pointers).
 struct SwarmDev {
     int *hdr;        // [16] ints: see kH* below
@@ -128,9 +116,9 @@ struct PsoUpdateArgs {
 // All return cudaGetLastError() of the launch.
 cudaError_t launch_step(const StepArgs &a, int C, bool stencil, int P, cudaStream_t st);
 int step_nblk(int nx, int ny, int nz, bool stencil, int P);
+int slab_tz(int nx, int ny, int nz_total);
 int step_nblk_max(int nx, int ny, int nz);
 int step_zchunks(int nx, int ny, int nz, int P);
-cudaError_t launch_finalize(const FinalizeArgs &a, cudaStream_t st);
 cudaError_t launch_fixup_copy(const float4 *scratch, float4 *out, long long nvox, int P,
                               const double *stats, int iters, cudaStream_t st);
 cudaError_t launch_pso_init(SwarmDev s, int P, int Pl, int p0, double v0, uint32_t k0,

@@ -837,6 +837,33 @@ int step_zchunks(int nx, int ny, int nz, int P) {
     return best;
 }
 
+// Planes per z-chunk of the canonical / z-slab decomposition: a function of
+// the volume alone (never of the slab count), so the chunk records -- and with
+// them centres and J -- are the same for any number of slabs.  Chosen like
+// step_zchunks for one state on one GPU (wave fill x halo overhead), subject
+// to at least 8 chunks (up to 8 slabs get work).
+int slab_tz(int nx, int ny, int nz) {
+    const long long tiles = (long long)((nx + kTX - 1) / kTX) * ((ny + kTY - 1) / kTY);
+    const long long slots = 148LL * kStepMinBlocks;
+    const int zmax = (nz + kTZMin - 1) / kTZMin;
+    const int zmin = zmax < 8 ? zmax : 8;
+    int best = (nz + zmin - 1) / zmin;
+    double best_eff = -1.0;
+    for (int z = zmin; z <= zmax; ++z) {
+        const int tz = (nz + z - 1) / z;
+        const int zz = (nz + tz - 1) / tz;
+        if (zz < zmin) continue;
+        const long long ctas = tiles * zz;
+        const long long waves = (ctas + slots - 1) / slots;
+        const double eff = (double)ctas / (double)(waves * slots) * (double)tz / (double)(tz + 2);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = tz;
+        }
+    }
+    return best;
+}
+
 int step_nblk(int nx, int ny, int nz, bool stencil, int P) {
     if (!stencil) return pw_blocks((long long)nx * ny * nz);
     const int tx = (nx + kTX - 1) / kTX, ty = (ny + kTY - 1) / kTY;
@@ -917,8 +944,8 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
         a.nz_t = a.nz;
         a.goff = 0;
         a.nz_g = a.nz;
-        a.tz = kSlabTZ;
-        a.zchunks = (a.nz + kSlabTZ - 1) / kSlabTZ;
+        a.tz = slab_tz(a.nx, a.ny, a.nz);
+        a.zchunks = (a.nz + a.tz - 1) / a.tz;
         a.nblk = a.tiles_x * a.tiles_y * a.zchunks;
     } else if (a.nz_g <= 0) {  // whole volume: targets are all planes
         a.z_lo = 0;
@@ -928,10 +955,10 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
         a.zchunks = step_zchunks(a.nx, a.ny, a.nz, P);
         a.tz = (a.nz + a.zchunks - 1) / a.zchunks;
         a.nblk = step_nblk(a.nx, a.ny, a.nz, stencil, P);
-    } else {  // z-slab: fixed global chunks of kSlabTZ planes
+    } else {  // z-slab: global chunks of slab_tz planes
         if (!stencil) return cudaErrorInvalidValue;
-        a.tz = kSlabTZ;
-        a.zchunks = (a.nz_t + kSlabTZ - 1) / kSlabTZ;
+        a.tz = slab_tz(a.nx, a.ny, a.nz_g);
+        a.zchunks = (a.nz_t + a.tz - 1) / a.tz;
         a.nblk = a.tiles_x * a.tiles_y * a.zchunks;
     }
     const bool m2 = (a.m == 2.0f);

@@ -170,11 +170,12 @@ class ShardedSegmenter:
         self.cen = torch.empty((1, 4), dtype=torch.float32, device=self.dev)
         self.engine = None
         world = dist.get_world_size() if dist is not None else 1
-        # fewer 16-plane chunks than ranks: every rank runs the whole volume
+        tz = ctx.slab_chunk(self.nx, self.ny, self.nz)
+        # fewer z-chunks than ranks: every rank runs the whole volume
         self.slab = SlabIfcm(ctx, cfg, self.nx, self.ny, self.nz, 1,
-                             dist if -(-self.nz // SLAB_TZ) >= world else None)
+                             dist if -(-self.nz // tz) >= world else None)
         w = self.slab.world
-        self.lab_counts = [slab_range(self.nz, w, r)[1] * self.nx * self.ny for r in range(w)]
+        self.lab_counts = [slab_range(self.nz, w, r, tz)[1] * self.nx * self.ny for r in range(w)]
         self.lab_pad = torch.zeros((w, max(self.lab_counts)), dtype=torch.uint8, device=self.dev)
 
     def segment(self, vol: torch.Tensor) -> dict:
@@ -256,11 +257,9 @@ class ShardedSegmenter:
 
 # ----------------------------------------------------------------------------
 # z-slab sharding of the IFCM iteration (volumes too large for one GPU)
-SLAB_TZ = 16  # global z-chunk of the slab reductions (kSlabTZ in the library)
-
-
-def slab_range(nz_total: int, world: int, rank: int, tz: int = SLAB_TZ) -> tuple[int, int]:
-    """(z0, nz) of rank's slab: whole 16-plane chunks, split as evenly as possible."""
+def slab_range(nz_total: int, world: int, rank: int, tz: int) -> tuple[int, int]:
+    """(z0, nz) of rank's slab: whole tz-plane global chunks (tz =
+    pifcm_slab_chunk of the volume), split as evenly as possible."""
     chunks = -(-nz_total // tz)
     c0, c1 = shard_range(chunks, world, rank)
     z0 = c0 * tz
@@ -285,12 +284,13 @@ class SlabIfcm:
         self.world = dist.get_world_size() if dist is not None else 1
         self.rank = dist.get_rank() if dist is not None else 0
         self.nx, self.ny, self.nz_total = nx, ny, nz_total
-        self.z0, self.nz = slab_range(nz_total, self.world, self.rank)
+        self.tz = ctx.slab_chunk(nx, ny, nz_total)
+        self.z0, self.nz = slab_range(nz_total, self.world, self.rank, self.tz)
         self.grid = _grid(nx, ny, self.nz, z0=self.z0, nz_total=nz_total)
         self.nrec = ctx.slab_records(self.grid)
         nrecs = []
         for r in range(self.world):
-            z0, nz = slab_range(nz_total, self.world, r)
+            z0, nz = slab_range(nz_total, self.world, r, self.tz)
             nrecs.append(ctx.slab_records(_grid(nx, ny, nz, z0=z0, nz_total=nz_total)))
         self.nrec_max = max(nrecs)
         self.counts = torch.tensor(nrecs, dtype=torch.int32, device=torch.device(f"cuda:{ctx.device}"))

@@ -136,15 +136,30 @@ def test_sharded_pso_equals_single_process(orc, P, world):
 
 
 def test_slab_range():
-    from paper_2002_01981_b200.dist import SLAB_TZ, slab_range
-    assert SLAB_TZ == 16
-    assert [slab_range(181, 4, r) for r in range(4)] == [(0, 48), (48, 48), (96, 48), (144, 37)]
+    from paper_2002_01981_b200.dist import slab_range
+    assert [slab_range(181, 4, r, 16) for r in range(4)] == [(0, 48), (48, 48), (96, 48), (144, 37)]
     for nz in (1, 15, 16, 17, 40, 181, 512):
-        chunks = -(-nz // 16)
-        for w in range(1, min(chunks, 8) + 1):
-            rs = [slab_range(nz, w, r) for r in range(w)]
-            assert rs[0][0] == 0 and sum(n for _, n in rs) == nz
-            assert all(z0 % 16 == 0 and n > 0 for z0, n in rs)            # whole global chunks
-            assert all(rs[i][0] + rs[i][1] == rs[i + 1][0] for i in range(w - 1))
-            ch = [-(-n // 16) for _, n in rs]
-            assert max(ch) - min(ch) <= 1
+        for tz in (8, 16, 19):
+            chunks = -(-nz // tz)
+            for w in range(1, min(chunks, 8) + 1):
+                rs = [slab_range(nz, w, r, tz) for r in range(w)]
+                assert rs[0][0] == 0 and sum(n for _, n in rs) == nz
+                assert all(z0 % tz == 0 and n > 0 for z0, n in rs)            # whole global chunks
+                assert all(rs[i][0] + rs[i][1] == rs[i + 1][0] for i in range(w - 1))
+                ch = [-(-n // tz) for _, n in rs]
+                assert max(ch) - min(ch) <= 1
+
+
+def test_slab_chunk_depends_on_the_volume_only():
+    """pifcm_slab_chunk (host-only ABI query): >= 8 chunks where the volume
+    allows (8 slabs get work), >= 8 planes per chunk, deterministic."""
+    from paper_2002_01981_b200.api import PifcmError, slab_chunk
+    for nx, ny, nz in [(181, 217, 181), (512, 512, 512), (37, 40, 50), (854, 854, 1), (30, 26, 12), (8, 8, 7)]:
+        tz = slab_chunk(nx, ny, nz)
+        chunks = -(-nz // tz)
+        assert 1 <= tz <= nz
+        assert chunks >= min(8, -(-nz // 8))
+        assert tz >= 8 or chunks == 1 or tz * (chunks - 1) < nz
+        assert slab_chunk(nx, ny, nz) == tz
+    with pytest.raises(PifcmError):
+        slab_chunk(0, 5, 5)

@@ -1,7 +1,7 @@
 """z-slab sharding of the IFCM iteration: a volume split into
 slabs with one halo plane per side gives memberships bit-identical to the
 whole-volume step and centres / J bit-identical for any number of slabs (the
-reductions use fixed global 16-plane chunks); across processes (gloo, two
+reductions use global z-chunks fixed by the volume, pifcm_slab_chunk); across processes (gloo, two
 ranks on one GPU) through the SlabIfcm driver."""
 import os
 import socket
@@ -52,11 +52,12 @@ def _virtual_slabs(ctx, world, iters, lx):
         from paper_2002_01981_b200.api import _grid
         from paper_2002_01981_b200.dist import slab_range
         s.world, s.rank = world, r
-        s.z0, s.nz = slab_range(NZ, world, r)
+        tz = ctx.slab_chunk(NX, NY, NZ)
+        s.z0, s.nz = slab_range(NZ, world, r, tz)
         s.grid = _grid(NX, NY, s.nz, z0=s.z0, nz_total=NZ)
         s.nrec = ctx.slab_records(s.grid)
-        nrecs = [ctx.slab_records(_grid(NX, NY, slab_range(NZ, world, q)[1],
-                                        z0=slab_range(NZ, world, q)[0], nz_total=NZ)) for q in range(world)]
+        nrecs = [ctx.slab_records(_grid(NX, NY, slab_range(NZ, world, q, tz)[1],
+                                        z0=slab_range(NZ, world, q, tz)[0], nz_total=NZ)) for q in range(world)]
         s.nrec_max = max(nrecs)
         s.counts = torch.tensor(nrecs, dtype=torch.int32, device=dev)
         pl = NX * NY

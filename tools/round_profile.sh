@@ -1,0 +1,15 @@
+# One GPU call: bench line, reference arm, launch list of one bench step and a
+# full ncu capture of the fused step kernel (P=32 launch).  Outputs in gpurun_out/.
+set -x
+TAG=${TAG:-r01}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 600 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
+tail -c 3000 gpurun_out/bench_${TAG}.json
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_${TAG}.json 2>&1
+tail -c 1500 gpurun_out/bench_ref_${TAG}.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launches_${TAG}.csv python tools/profile_step.py segment > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step_stencil -s 1 -c 1 \
+    -f -o gpurun_out/kstep_${TAG} python tools/profile_step.py eval 2 > gpurun_out/ncu_full_${TAG}.log 2>&1
+tail -3 gpurun_out/ncu_full_${TAG}.log
