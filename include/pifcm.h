@@ -331,6 +331,69 @@ int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int
 int pifcm_slab_halo(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t P, int32_t op, float *U,
                     float *buf, pifcm_stream stream);
 
+/* ------------------------------------------- pipeline parts for z-slab ranks
+ * Alg. 2 step 1 when the volume is split into slabs: each
+ * rank reduces min / max over its own planes (pifcm_minmax_u8), the caller
+ * combines them across ranks (min of mins, max of maxes), normalises its
+ * slab arrays with the global range (pifcm_normalize_u8_range) and builds the
+ * R15 histogram of its own planes (pifcm_hist_u8), which the caller sums
+ * across ranks before pifcm_gmm_init.  All async. */
+/* mm dev uint32 [2] out: {min, max} of the n u8 values at vol (dev). */
+int pifcm_minmax_u8(pifcm_ctx *ctx, const uint8_t *vol, int64_t n, uint32_t *mm, pifcm_stream stream);
+/* x = (v - mm[0]) / (mm[1] - mm[0]) (0 when mm[1] == mm[0], R16) for the
+ * plain grid (nz_total = 0) vol [nz][ny][nx] -> x [nz][ny][pitch]. */
+int pifcm_normalize_u8_range(pifcm_ctx *ctx, const pifcm_grid *grid, const uint8_t *vol, const uint32_t *mm,
+                             float *x, pifcm_stream stream);
+/* hist dev int64 [256] out: R15 bins b = round((v - min) * 255 / (max - min))
+ * of the n values at vol, with the global range mm. */
+int pifcm_hist_u8(pifcm_ctx *ctx, const uint8_t *vol, int64_t n, const uint32_t *mm, int64_t *hist,
+                  pifcm_stream stream);
+
+/* ------------------------------------------------- PSO over z-slab ranks
+ * Alg. 1 steps 3-10 for a volume split into z-slabs (SURVEY
+ * 8(e), the 512^3 C5 workload): every rank holds ALL particles' states for
+ * its slab (a slot pool like pifcm_pso_*, each slot [nz+2][ny][nx][4] with
+ * the halo planes) and the identical swarm.  Per generation the caller runs
+ *   pifcm_slab_pso_halo (pack, op 0/1) -> send/recv -> pifcm_slab_pso_halo
+ *   (unpack, op 2/3) -> pifcm_slab_pso_eval (records of every particle) ->
+ *   all-gather of the records in rank order -> pifcm_slab_pso_finalize
+ *   (centres and fitness of every particle, identical on every rank) ->
+ *   pifcm_slab_pso_update (the device PSO update of pifcm_pso_update)
+ * so every rank takes the same PSO decisions; fitness and trajectories are
+ * bit-identical for any number of slabs (global z-chunk records).  `slab` is
+ * the rank's slab grid (see pifcm_grid); pso->p_begin = p_end = 0 (all
+ * particles).  The workspace holds the slots, the swarm and scratch. */
+int pifcm_slab_workspace_size(const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                              size_t *bytes);
+/* U0 dev fp32 [nz+2][ny][nx][4] (the slab's start state, halos included),
+ * c0 dev fp32 [4].  Positions / velocities from Philox (R12).  Async. */
+int pifcm_slab_pso_init(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                        const float *U0, const float *c0, void *ws, size_t ws_bytes, pifcm_stream stream);
+/* Halo planes of every particle's current state, ops as pifcm_slab_halo with
+ * buf [P][ny][nx][4].  Async. */
+int pifcm_slab_pso_halo(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                        void *ws, size_t ws_bytes, int32_t op, float *buf, pifcm_stream stream);
+/* One IFCM step of every particle at its own (lambda, xi) on the slab's
+ * planes (Alg. 1 step 4, CHAINED R11); records dev fp64 [P][nrec][10] out
+ * (nrec = pifcm_slab_records).  x dev fp32 [nz+2][ny][pitch].  Async. */
+int pifcm_slab_pso_eval(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                        const float *x, void *ws, size_t ws_bytes, double *records, pifcm_stream stream);
+/* Eq. 3 / Eq. 1 of every particle from the gathered records [world][P][nrec][10]
+ * (as pifcm_slab_finalize) into the swarm's centres and fitness.  Async. */
+int pifcm_slab_pso_finalize(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                            const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, int32_t world, int32_t nrec,
+                            const int32_t *counts, const double *records, pifcm_stream stream);
+/* Alg. 1 steps 5-8 (as pifcm_pso_update).  Async. */
+int pifcm_slab_pso_update(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                          const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, pifcm_stream stream);
+/* As pifcm_pso_result_get / pifcm_pso_gbest_state (U_out: the slab part of
+ * the gbest state, [nz+2][ny][nx][4]; every rank holds it).  Sync. */
+int pifcm_slab_pso_result_get(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                              const pifcm_pso_cfg *pso, void *ws, pifcm_pso_result *out, int32_t *stopped,
+                              pifcm_stream stream);
+int pifcm_slab_pso_gbest_state(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                               const pifcm_pso_cfg *pso, void *ws, float *U_out, float *c_out, pifcm_stream stream);
+
 /* Number of kernels this context has launched so far (for the bench's
  * gpu_launches count). */
 int64_t pifcm_launch_count(const pifcm_ctx *ctx);

@@ -85,6 +85,18 @@ SIGNATURES = {
                                  ct.c_int32, _vp, ct.c_size_t, _vp, _vp, ct.POINTER(Report), _vp]),
     "pifcm_segment_host": (ct.c_int, [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int32, _C, _P, _vp,
                                       ct.c_size_t, _vp, ct.POINTER(Report), _vp]),
+    "pifcm_minmax_u8": (ct.c_int, [_vp, _vp, ct.c_int64, _vp, _vp]),
+    "pifcm_normalize_u8_range": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pifcm_hist_u8": (ct.c_int, [_vp, _vp, ct.c_int64, _vp, _vp, _vp]),
+    "pifcm_slab_workspace_size": (ct.c_int, [_vp, _vp, _vp, _vp]),
+    "pifcm_slab_pso_init": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, ct.c_size_t, _vp]),
+    "pifcm_slab_pso_halo": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, ct.c_size_t, ct.c_int32, _vp, _vp]),
+    "pifcm_slab_pso_eval": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, ct.c_size_t, _vp, _vp]),
+    "pifcm_slab_pso_finalize": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, ct.c_size_t, ct.c_int32, ct.c_int32, _vp, _vp,
+                                           _vp]),
+    "pifcm_slab_pso_update": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, ct.c_size_t, _vp]),
+    "pifcm_slab_pso_result_get": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pifcm_slab_pso_gbest_state": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "pifcm_slab_chunk": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32, _vp]),
     "pifcm_slab_records": (ct.c_int, [_G, ct.POINTER(ct.c_int32)]),
     "pifcm_slab_step": (ct.c_int, [_vp, _G, _C, _vp, _vp, _vp, _vp, _vp, ct.c_int32, _vp, _vp, _vp]),

@@ -322,6 +322,71 @@ class Context:
     def slab_halo(self, grid, P, op, U, buf=None, stream=None):
         self._ck(self.lib.pifcm_slab_halo(self._h, ct.byref(grid), P, op, _ptr(U), _ptr(buf), _stream(stream)))
 
+    # -------------------------------------------- pipeline parts for slab ranks
+    def minmax_u8(self, vol: torch.Tensor, mm: torch.Tensor, stream=None):
+        """mm: device int32 [2] <- {min, max} of vol (uint32 bits; values <= 255)."""
+        self._ck(self.lib.pifcm_minmax_u8(self._h, _ptr(vol), vol.numel(), _ptr(mm), _stream(stream)))
+
+    def normalize_u8_range(self, vol: torch.Tensor, mm: torch.Tensor, stream=None) -> torch.Tensor:
+        nz, ny, nx = vol.shape
+        g = _grid(nx, ny, nz)
+        x = torch.zeros((nz, ny, g.pitch), dtype=torch.float32, device=vol.device)
+        self._ck(self.lib.pifcm_normalize_u8_range(self._h, ct.byref(g), _ptr(vol), _ptr(mm), _ptr(x),
+                                                   _stream(stream)))
+        return x
+
+    def hist_u8(self, vol: torch.Tensor, mm: torch.Tensor, stream=None) -> torch.Tensor:
+        hist = torch.empty(256, dtype=torch.int64, device=vol.device)
+        self._ck(self.lib.pifcm_hist_u8(self._h, _ptr(vol), vol.numel(), _ptr(mm), _ptr(hist), _stream(stream)))
+        return hist
+
+    # ------------------------------------------------- PSO over z-slab ranks
+    def slab_workspace(self, grid, cfg, pso) -> torch.Tensor:
+        n = ct.c_size_t()
+        self._ck(self.lib.pifcm_slab_workspace_size(ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                                    ct.byref(n)))
+        return torch.empty(n.value, dtype=torch.uint8, device=f"cuda:{self.device}")
+
+    def slab_pso_init(self, grid, cfg, pso, U0, c0, ws, stream=None):
+        self._ck(self.lib.pifcm_slab_pso_init(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                              _ptr(U0), _ptr(c0), _ptr(ws), ws.numel(), _stream(stream)))
+
+    def slab_pso_halo(self, grid, cfg, pso, ws, op, buf=None, stream=None):
+        self._ck(self.lib.pifcm_slab_pso_halo(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                              _ptr(ws), ws.numel(), op, _ptr(buf), _stream(stream)))
+
+    def slab_pso_eval(self, grid, cfg, pso, x, ws, records, stream=None):
+        self._ck(self.lib.pifcm_slab_pso_eval(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                              _ptr(x), _ptr(ws), ws.numel(), _ptr(records), _stream(stream)))
+
+    def slab_pso_finalize(self, grid, cfg, pso, ws, world, nrec, records, counts=None, stream=None):
+        self._ck(self.lib.pifcm_slab_pso_finalize(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                                  _ptr(ws), ws.numel(), world, nrec, _ptr(counts),
+                                                  _ptr(records), _stream(stream)))
+
+    def slab_pso_update(self, grid, cfg, pso, ws, stream=None):
+        self._ck(self.lib.pifcm_slab_pso_update(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
+                                                _ptr(ws), ws.numel(), _stream(stream)))
+
+    def slab_pso_result(self, grid, cfg, pso, ws, stream=None):
+        r = _abi.PsoResult()
+        stopped = ct.c_int32()
+        self._ck(self.lib.pifcm_slab_pso_result_get(self._h, ct.byref(grid), ct.byref(cfg.c()),
+                                                    ct.byref(pso.c()), _ptr(ws), ct.byref(r),
+                                                    ct.byref(stopped), _stream(stream)))
+        return PsoSummary(r.lambda_, r.xi, r.J, r.generations, r.gbest_particle,
+                          list(r.centers)[:cfg.C]), bool(stopped.value)
+
+    def slab_pso_gbest_state(self, grid, cfg, pso, ws, U_out, c_out, stream=None):
+        self._ck(self.lib.pifcm_slab_pso_gbest_state(self._h, ct.byref(grid), ct.byref(cfg.c()),
+                                                     ct.byref(pso.c()), _ptr(ws), _ptr(U_out), _ptr(c_out),
+                                                     _stream(stream)))
+
+    def slab_pso_fitness(self, grid, cfg, pso, ws) -> torch.Tensor:
+        """Fitness vector of the slab swarm (a view into ws)."""
+        pg = _grid(grid.nx, grid.ny, grid.nz + 2, grid.pitch)
+        return self.pso_fitness(pg, cfg, pso, ws)
+
 
 def slab_chunk(nx, ny, nz_total, lib=None) -> int:
     """pifcm_slab_chunk (host-only query, no GPU needed)."""

@@ -113,19 +113,22 @@ cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const int *c
 // Copy one plane of every state between a slab array and a packed buffer
 // (halo pack / unpack), or zero it (a halo outside the volume).
 __global__ void k_halo_copy(const float4 *src, long long src_state, float4 *dst, long long dst_state,
-                            long long plane, bool zero) {
+                            long long plane, bool zero, const int *src_idx, const int *dst_idx) {
     const int p = blockIdx.y;
+    const long long so = (long long)(src_idx ? src_idx[p] : p) * src_state;
+    const long long dof = (long long)(dst_idx ? dst_idx[p] : p) * dst_state;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < plane;
          i += (long long)gridDim.x * blockDim.x)
-        dst[p * dst_state + i] = zero ? make_float4(0.f, 0.f, 0.f, 0.f) : src[p * src_state + i];
+        dst[dof + i] = zero ? make_float4(0.f, 0.f, 0.f, 0.f) : src[so + i];
 }
 
 cudaError_t launch_halo_copy(const float4 *src, long long src_state, float4 *dst, long long dst_state,
-                             long long plane, int P, bool zero, cudaStream_t st) {
+                             long long plane, int P, bool zero, cudaStream_t st, const int *src_idx,
+                             const int *dst_idx) {
     long long b = (plane + 255) / 256;
     if (b > 148 * 4) b = 148 * 4;
     dim3 grid((unsigned)(b < 1 ? 1 : b), P);
-    k_halo_copy<<<grid, 256, 0, st>>>(src, src_state, dst, dst_state, plane, zero);
+    k_halo_copy<<<grid, 256, 0, st>>>(src, src_state, dst, dst_state, plane, zero, src_idx, dst_idx);
     return cudaGetLastError();
 }
 

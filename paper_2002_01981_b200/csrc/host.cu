@@ -805,4 +805,171 @@ int pifcm_slab_halo(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t P, int32_t o
     return PIFCM_OK;
 }
 
+
+// ============================================================== ABI: pipeline parts for slabs
+int pifcm_minmax_u8(pifcm_ctx *ctx, const uint8_t *vol, int64_t n, uint32_t *mm, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    if (!vol || !mm || n < 1) return fail(ctx, PIFCM_EINVAL, "vol, mm non-NULL and n >= 1 required");
+    LAUNCH(ctx, 2, launch_minmax_u8(vol, n, reinterpret_cast<unsigned int *>(mm),
+                                    reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_normalize_u8_range(pifcm_ctx *ctx, const pifcm_grid *grid, const uint8_t *vol, const uint32_t *mm,
+                             float *x, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(ctx, grid))) return r;
+    if (!vol || !mm || !x) return fail(ctx, PIFCM_EINVAL, "vol, mm and x must be non-NULL");
+    LAUNCH(ctx, 1, launch_normalize_u8(vol, grid->nx, grid->ny, grid->nz, grid->pitch,
+                                       reinterpret_cast<const unsigned int *>(mm), x,
+                                       reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_hist_u8(pifcm_ctx *ctx, const uint8_t *vol, int64_t n, const uint32_t *mm, int64_t *hist,
+                  pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    if (!vol || !mm || !hist || n < 1) return fail(ctx, PIFCM_EINVAL, "vol, mm, hist non-NULL and n >= 1 required");
+    LAUNCH(ctx, 2, launch_hist_u8(vol, n, reinterpret_cast<const unsigned int *>(mm), hist,
+                                  reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+// ============================================================== ABI: PSO over z-slabs
+// The swarm of a slab rank lives in a pifcm workspace laid out for the slab's
+// arrays (nz + 2 planes with the halos); every rank holds all particles.
+static pifcm_grid plain_of(const pifcm_grid *s) { return pifcm_grid{s->nx, s->ny, s->nz + 2, s->pitch, 0, 0}; }
+
+static int slab_pso_common(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                           const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, Layout *L, pifcm_grid *pg) {
+    int r;
+    if ((r = check_slab(ctx, slab)) || (r = check_cfg(ctx, cfg)) || (r = check_pso(ctx, pso))) return r;
+    if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
+        return fail(ctx, PIFCM_EINVAL, "slab ranks hold every particle (p_begin = p_end = 0)");
+    *pg = plain_of(slab);
+    *L = layout(pg, cfg, pso);
+    return ws ? check_ws(ctx, ws, ws_bytes, L->total) : PIFCM_OK;
+}
+
+int pifcm_slab_workspace_size(const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                              size_t *bytes) {
+    if (!bytes) return PIFCM_EINVAL;
+    Layout L;
+    pifcm_grid pg;
+    int r = slab_pso_common(nullptr, slab, cfg, pso, nullptr, 0, &L, &pg);
+    if (r) return r;
+    *bytes = L.total;
+    return PIFCM_OK;
+}
+
+int pifcm_slab_pso_init(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                        const float *U0, const float *c0, void *ws, size_t ws_bytes, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    Layout L;
+    pifcm_grid pg;
+    int r = slab_pso_common(ctx, slab, cfg, pso, ws, ws_bytes, &L, &pg);
+    if (r) return r;
+    return pifcm_pso_init(ctx, &pg, cfg, pso, U0, c0, ws, ws_bytes, stream);
+}
+
+int pifcm_slab_pso_halo(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                        void *ws, size_t ws_bytes, int32_t op, float *buf, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    Layout L;
+    pifcm_grid pg;
+    int r = slab_pso_common(ctx, slab, cfg, pso, ws, ws_bytes, &L, &pg);
+    if (r) return r;
+    if (op < 0 || op > 3) return fail(ctx, PIFCM_EINVAL, "halo op %d outside [0, 3]", op);
+    const long long plane = (long long)slab->nx * slab->ny;
+    SwarmDev s = swarm_of(ws, L);
+    float4 *slots = at<float4>(ws, L.slots), *B4 = reinterpret_cast<float4 *>(buf);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (op <= 1) {
+        if (!buf) return fail(ctx, PIFCM_EINVAL, "pack needs a buffer");
+        const long long src_plane = op == 0 ? 1 : slab->nz;
+        LAUNCH(ctx, 1, launch_halo_copy(slots + src_plane * plane, L.nvox, B4, plane, plane, L.Pl, false, st, s.cur,
+                                        nullptr));
+    } else {
+        const long long dst_plane = op == 2 ? 0 : slab->nz + 1;
+        const bool outside = op == 2 ? slab->z0 == 0 : slab->z0 + slab->nz == slab->nz_total;
+        if (!outside && !buf) return fail(ctx, PIFCM_EINVAL, "unpack of an interior halo needs a buffer");
+        LAUNCH(ctx, 1, launch_halo_copy(B4, plane, slots + dst_plane * plane, L.nvox, plane, L.Pl, outside, st,
+                                        nullptr, s.cur));
+    }
+    return PIFCM_OK;
+}
+
+int pifcm_slab_pso_eval(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
+                        const float *x, void *ws, size_t ws_bytes, double *records, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    Layout L;
+    pifcm_grid pg;
+    int r = slab_pso_common(ctx, slab, cfg, pso, ws, ws_bytes, &L, &pg);
+    if (r) return r;
+    if (!x || !records) return fail(ctx, PIFCM_EINVAL, "x and records must be non-NULL");
+    SwarmDev s = swarm_of(ws, L);
+    float4 *slots = at<float4>(ws, L.slots);
+    StepArgs a{};
+    a.x = x;
+    a.nx = slab->nx; a.ny = slab->ny; a.nz = slab->nz + 2; a.pitch = slab->pitch;
+    a.nvox = L.nvox;
+    a.z_lo = 1; a.nz_t = slab->nz; a.goff = slab->z0 - 1; a.nz_g = slab->nz_total;
+    a.U_in = slots; a.U_out = slots; a.in_idx = s.cur; a.out_idx = s.nxt;
+    a.centers = s.centers; a.lam_xi = s.pos; a.partials = records;
+    a.stop = s.hdr + kHStop;
+    a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f); a.q_mode = cfg->q_mode;
+    a.n_in_states = L.nslots;
+    a.counters = nullptr;  // records are combined across ranks by pifcm_slab_pso_finalize
+    a.C = cfg->C;
+    LAUNCH(ctx, 1, launch_step(a, cfg->C, true, L.Pl, reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_slab_pso_finalize(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                            const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, int32_t world, int32_t nrec,
+                            const int32_t *counts, const double *records, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    Layout L;
+    pifcm_grid pg;
+    int r = slab_pso_common(ctx, slab, cfg, pso, ws, ws_bytes, &L, &pg);
+    if (r) return r;
+    if (world < 1 || world > 64 || nrec < 1 || !records) return fail(ctx, PIFCM_EINVAL, "invalid records");
+    SwarmDev s = swarm_of(ws, L);
+    LAUNCH(ctx, 1, launch_slab_finalize(cfg->C, L.Pl, world, nrec, counts, records, s.centers, nullptr, s.fit, 0.f,
+                                        s.hdr + kHStatus, reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_slab_pso_update(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                          const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    Layout L;
+    pifcm_grid pg;
+    int r = slab_pso_common(ctx, slab, cfg, pso, ws, ws_bytes, &L, &pg);
+    if (r) return r;
+    return pifcm_pso_update(ctx, &pg, cfg, pso, ws, ws_bytes, stream);
+}
+
+int pifcm_slab_pso_result_get(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                              const pifcm_pso_cfg *pso, void *ws, pifcm_pso_result *out, int32_t *stopped,
+                              pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    Layout L;
+    pifcm_grid pg;
+    int r = slab_pso_common(ctx, slab, cfg, pso, nullptr, 0, &L, &pg);
+    if (r) return r;
+    return pifcm_pso_result_get(ctx, &pg, cfg, pso, ws, out, stopped, stream);
+}
+
+int pifcm_slab_pso_gbest_state(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
+                               const pifcm_pso_cfg *pso, void *ws, float *U_out, float *c_out, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    Layout L;
+    pifcm_grid pg;
+    int r = slab_pso_common(ctx, slab, cfg, pso, nullptr, 0, &L, &pg);
+    if (r) return r;
+    return pifcm_pso_gbest_state(ctx, &pg, cfg, pso, ws, U_out, c_out, stream);
+}
+
 }  // extern "C"

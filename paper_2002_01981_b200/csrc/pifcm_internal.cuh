@@ -140,6 +140,7 @@ cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const int *c
                                  float *centers, double *stats, double *fitness, float eps, int *status,
                                  cudaStream_t st);
 cudaError_t launch_halo_copy(const float4 *src, long long src_state, float4 *dst, long long dst_state,
-                             long long plane, int P, bool zero, cudaStream_t st);
+                             long long plane, int P, bool zero, cudaStream_t st, const int *src_idx = nullptr,
+                             const int *dst_idx = nullptr);
 
 }  // namespace pifcm

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import torch
 
 __all__ = ["shard_range", "allgather_fitness", "ShardedPso", "GpuPsoEngine", "ShardedSegmenter",
-           "slab_range", "SlabIfcm"]
+           "slab_range", "SlabIfcm", "SlabPso", "SlabSegmenter"]
 
 
 def shard_range(P: int, world: int, rank: int) -> tuple[int, int]:
@@ -256,7 +256,7 @@ class ShardedSegmenter:
 
 
 # ----------------------------------------------------------------------------
-# z-slab sharding of the IFCM iteration (volumes too large for one GPU)
+# z-slab sharding (volumes too large for one GPU: SURVEY 8(e), the C5 workload)
 def slab_range(nz_total: int, world: int, rank: int, tz: int) -> tuple[int, int]:
     """(z0, nz) of rank's slab: whole tz-plane global chunks (tz =
     pifcm_slab_chunk of the volume), split as evenly as possible."""
@@ -270,6 +270,96 @@ def _coll_tensor(dist, t):
     return t.cpu() if dist.get_backend() == "gloo" and t.device.type == "cuda" else t
 
 
+def _halo_sendrecv(dist, rank, world, send_lo, send_hi, recv_lo, recv_hi):
+    """Boundary planes to / from the neighbouring slabs (one batched send/recv;
+    gloo carries CUDA tensors through host copies)."""
+    ops = []
+    if rank > 0:
+        ops += [("send", send_lo, rank - 1), ("recv", recv_lo, rank - 1)]
+    if rank < world - 1:
+        ops += [("send", send_hi, rank + 1), ("recv", recv_hi, rank + 1)]
+    if not ops:
+        return
+    if dist.get_backend() == "gloo":
+        torch.cuda.current_stream().synchronize()
+    bufs = [(k, _coll_tensor(dist, t), t, peer) for k, t, peer in ops]
+    reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend if k == "send" else dist.irecv, b, peer)
+                                   for k, b, _, peer in bufs])
+    for r in reqs:
+        r.wait()
+    for k, b, t, _ in bufs:
+        if k == "recv" and b is not t:
+            t.copy_(b)
+
+
+class _SlabGeometry:
+    """This rank's slab of a volume and the record bookkeeping shared by the
+    slab drivers: global chunk size, slab grid, per-rank record counts, the
+    local / padded / gathered record buffers and their all-gather."""
+
+    def __init__(self, ctx, nx, ny, nz_total, P, dist):
+        from .api import _grid
+        self.ctx, self.dist, self.P = ctx, dist, P
+        self.world = dist.get_world_size() if dist is not None else 1
+        self.rank = dist.get_rank() if dist is not None else 0
+        self.nx, self.ny, self.nz_total = nx, ny, nz_total
+        self.tz = ctx.slab_chunk(nx, ny, nz_total)
+        self.z0, self.nz = slab_range(nz_total, self.world, self.rank, self.tz)
+        self.grid = _grid(nx, ny, self.nz, z0=self.z0, nz_total=nz_total)
+        self.plane = nx * ny
+        nrecs = []
+        for r in range(self.world):
+            z0, nz = slab_range(nz_total, self.world, r, self.tz)
+            nrecs.append(ctx.slab_records(_grid(nx, ny, nz, z0=z0, nz_total=nz_total)))
+        self.nrec = nrecs[self.rank]
+        self.nrec_max = max(nrecs)
+        self.dev = torch.device(f"cuda:{ctx.device}")
+        self.counts = torch.tensor(nrecs, dtype=torch.int32, device=self.dev)
+        self.rec = torch.zeros((P, self.nrec, 10), dtype=torch.float64, device=self.dev)
+        self.rec_pad = torch.zeros((P, self.nrec_max, 10), dtype=torch.float64, device=self.dev)
+        self.gathered = torch.zeros((self.world, P, self.nrec_max, 10), dtype=torch.float64, device=self.dev)
+        self.halo = {k: torch.zeros((P, self.plane, 4), dtype=torch.float32, device=self.dev)
+                     for k in ("send_lo", "send_hi", "recv_lo", "recv_hi")}
+
+    def gather_records(self) -> torch.Tensor:
+        """Records of every rank in rank order, [world][P][nrec_max][10]."""
+        self.rec_pad[:, : self.nrec] = self.rec
+        if self.world == 1:
+            return self.rec_pad
+        d = self.dist
+        src = _coll_tensor(d, self.rec_pad)
+        out = _coll_tensor(d, self.gathered)
+        if src is not self.rec_pad:
+            torch.cuda.current_stream().synchronize()
+        d.all_gather_into_tensor(out.view(self.world * self.P, self.nrec_max, 10), src)
+        if out is not self.gathered:
+            self.gathered.copy_(out)
+        return self.gathered
+
+    def exchange(self, pack, unpack):
+        """pack(op, buf) fills buf with boundary plane op (0 lower, 1 upper);
+        unpack(op, buf or None) writes the halo (2 lower, 3 upper; None at the
+        volume ends = zero fill)."""
+        h = self.halo
+        if self.world > 1:
+            if self.rank > 0:
+                pack(0, h["send_lo"])
+            if self.rank < self.world - 1:
+                pack(1, h["send_hi"])
+            _halo_sendrecv(self.dist, self.rank, self.world, h["send_lo"], h["send_hi"], h["recv_lo"],
+                           h["recv_hi"])
+        unpack(2, h["recv_lo"] if self.rank > 0 else None)
+        unpack(3, h["recv_hi"] if self.rank < self.world - 1 else None)
+
+    def slab_planes(self, t: torch.Tensor) -> torch.Tensor:
+        """Planes [z0 - 1, z0 + nz + 1) of a full-volume [nz_total][...] tensor,
+        zero where they fall outside the volume."""
+        out = torch.zeros((self.nz + 2,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.dev)
+        lo, hi = max(self.z0 - 1, 0), min(self.z0 + self.nz + 1, self.nz_total)
+        out[lo - (self.z0 - 1): hi - (self.z0 - 1)] = t[lo:hi].to(self.dev)
+        return out
+
+
 class SlabIfcm:
     """Jacobi IFCM iterations of P states over a volume split into z-slabs, one
     per rank.  Per iteration: halo exchange of one U plane per neighbour and
@@ -279,46 +369,29 @@ class SlabIfcm:
     number of slabs)."""
 
     def __init__(self, ctx, cfg, nx, ny, nz_total, P, dist=None):
-        from .api import _grid
         self.ctx, self.cfg, self.P, self.dist = ctx, cfg, P, dist
-        self.world = dist.get_world_size() if dist is not None else 1
-        self.rank = dist.get_rank() if dist is not None else 0
+        self.geo = _SlabGeometry(ctx, nx, ny, nz_total, P, dist)
+        g = self.geo
+        self.world, self.rank, self.tz = g.world, g.rank, g.tz
         self.nx, self.ny, self.nz_total = nx, ny, nz_total
-        self.tz = ctx.slab_chunk(nx, ny, nz_total)
-        self.z0, self.nz = slab_range(nz_total, self.world, self.rank, self.tz)
-        self.grid = _grid(nx, ny, self.nz, z0=self.z0, nz_total=nz_total)
-        self.nrec = ctx.slab_records(self.grid)
-        nrecs = []
-        for r in range(self.world):
-            z0, nz = slab_range(nz_total, self.world, r, self.tz)
-            nrecs.append(ctx.slab_records(_grid(nx, ny, nz, z0=z0, nz_total=nz_total)))
-        self.nrec_max = max(nrecs)
-        self.counts = torch.tensor(nrecs, dtype=torch.int32, device=torch.device(f"cuda:{ctx.device}"))
-        dev = torch.device(f"cuda:{ctx.device}")
-        self.dev = dev
-        plane = nx * ny
-        self.plane = plane
-        self.Ua = torch.zeros((P, (self.nz + 2) * plane, 4), dtype=torch.float32, device=dev)
+        self.z0, self.nz, self.grid, self.plane = g.z0, g.nz, g.grid, g.plane
+        self.dev = g.dev
+        self.Ua = torch.zeros((P, (self.nz + 2) * self.plane, 4), dtype=torch.float32, device=self.dev)
         self.Ub = torch.zeros_like(self.Ua)
-        self.rec = torch.zeros((P, self.nrec, 10), dtype=torch.float64, device=dev)
-        self.rec_pad = torch.zeros((P, self.nrec_max, 10), dtype=torch.float64, device=dev)
-        self.gathered = torch.zeros((self.world, P, self.nrec_max, 10), dtype=torch.float64, device=dev)
-        self.halo = {k: torch.zeros((P, plane, 4), dtype=torch.float32, device=dev)
-                     for k in ("send_lo", "send_hi", "recv_lo", "recv_hi")}
-        self.centers = torch.zeros((P, 4), dtype=torch.float32, device=dev)
-        self.stats = torch.zeros((P, 4), dtype=torch.float64, device=dev)
+        self.centers = torch.zeros((P, 4), dtype=torch.float32, device=self.dev)
+        self.stats = torch.zeros((P, 4), dtype=torch.float64, device=self.dev)
+        self.swaps = 0
 
     # -- data in / out
     def load_x(self, x_full: torch.Tensor):
         """x_full [nz_total][ny][pitch] (any device) -> the slab with its halo
         planes (zero outside the volume)."""
-        from .api import pitch_of
-        pitch = pitch_of(self.nx)
-        xs = torch.zeros((self.nz + 2, self.ny, pitch), dtype=torch.float32, device=self.dev)
-        lo, hi = max(self.z0 - 1, 0), min(self.z0 + self.nz + 1, self.nz_total)
-        xs[lo - (self.z0 - 1): hi - (self.z0 - 1)] = x_full[lo:hi].to(self.dev)
-        self.x = xs
-        return xs
+        self.x = self.geo.slab_planes(x_full)
+        return self.x
+
+    def set_x(self, x_slab: torch.Tensor):
+        """x of the slab's arrays [nz + 2][ny][pitch] (halo planes included)."""
+        self.x = x_slab
 
     def load_state(self, U_full: torch.Tensor, centers: torch.Tensor):
         """U_full [P][nz_total*ny*nx][4]: this slab's planes (halos exchanged later)."""
@@ -328,59 +401,32 @@ class SlabIfcm:
         self.stats.zero_()
         self.swaps = 0
 
+    def load_local(self, U_slab: torch.Tensor, centers: torch.Tensor):
+        """U_slab [P][(nz+2)*ny*nx][4] already in the slab layout."""
+        self.Ua.copy_(U_slab.view_as(self.Ua))
+        self.centers.copy_(centers.view(self.P, 4))
+        self.stats.zero_()
+        self.swaps = 0
+
     def local_U(self) -> torch.Tensor:
         return self.Ua[:, self.plane: self.plane * (self.nz + 1)]
 
     # -- one iteration
     def exchange(self, U):
-        ctx, g, P, h = self.ctx, self.grid, self.P, self.halo
-        up, down = self.rank + 1, self.rank - 1
-        if self.world > 1:
-            ops = []
-            d = self.dist
-            if down >= 0:
-                ctx.slab_halo(g, P, 0, U, h["send_lo"])
-                ops += [("send", h["send_lo"], down), ("recv", h["recv_lo"], down)]
-            if up < self.world:
-                ctx.slab_halo(g, P, 1, U, h["send_hi"])
-                ops += [("send", h["send_hi"], up), ("recv", h["recv_hi"], up)]
-            gloo = d.get_backend() == "gloo"
-            bufs = [(kind, _coll_tensor(d, t), t, peer) for kind, t, peer in ops]
-            if gloo:
-                torch.cuda.current_stream().synchronize()
-            reqs = d.batch_isend_irecv([d.P2POp(d.isend if k == "send" else d.irecv, b, peer)
-                                        for k, b, _, peer in bufs])
-            for r in reqs:
-                r.wait()
-            for k, b, t, _ in bufs:
-                if k == "recv" and b is not t:
-                    t.copy_(b)
-        # halos outside the volume are zero-filled by the library
-        ctx.slab_halo(g, P, 2, U, h["recv_lo"] if self.rank > 0 else None)
-        ctx.slab_halo(g, P, 3, U, h["recv_hi"] if self.rank < self.world - 1 else None)
+        ctx, g, P = self.ctx, self.grid, self.P
+        self.geo.exchange(lambda op, buf: ctx.slab_halo(g, P, op, U, buf),
+                          lambda op, buf: ctx.slab_halo(g, P, op, U, buf))
 
     def step(self, lam_xi: torch.Tensor, eps: float = 0.0):
         """One iteration (no host synchronisation).  A converged state is
         skipped by the step kernel, so its latest U stays in the buffer its
         last real step wrote: sync_states() moves it back into Ua."""
         self.exchange(self.Ua)
-        self.ctx.slab_step(self.grid, self.cfg, self.x, self.Ua, self.Ub, self.centers, lam_xi, self.rec,
+        self.ctx.slab_step(self.grid, self.cfg, self.x, self.Ua, self.Ub, self.centers, lam_xi, self.geo.rec,
                            stats=self.stats)
-        self.rec_pad[:, : self.nrec] = self.rec
-        if self.world > 1:
-            d = self.dist
-            src = _coll_tensor(d, self.rec_pad)
-            out = _coll_tensor(d, self.gathered)
-            if src is not self.rec_pad:
-                torch.cuda.current_stream().synchronize()
-            d.all_gather_into_tensor(out.view(self.world * self.P, self.nrec_max, 10), src)
-            if out is not self.gathered:
-                self.gathered.copy_(out)
-            recs = self.gathered
-        else:
-            recs = self.rec_pad
-        self.ctx.slab_finalize(self.cfg.C, self.P, self.world, self.nrec_max, recs, self.centers,
-                               stats=self.stats, eps=eps, counts=self.counts)
+        recs = self.geo.gather_records()
+        self.ctx.slab_finalize(self.cfg.C, self.P, self.world, self.geo.nrec_max, recs, self.centers,
+                               stats=self.stats, eps=eps, counts=self.geo.counts)
         self.Ua, self.Ub = self.Ub, self.Ua
         self.swaps += 1
 
@@ -402,3 +448,162 @@ class SlabIfcm:
                 break
         self.sync_states()
         return done
+
+
+class SlabPso:
+    """Alg. 1 steps 3-10 over z-slab ranks (pifcm_slab_pso_*): every rank holds
+    all P particles' states for its slab and the identical swarm; per
+    generation a halo exchange of every particle's current state, the slab
+    step of all particles, an all-gather of their records, the fitness /
+    centres finalisation and the device PSO update -- the same on every rank,
+    so fitness vectors and trajectories are bit-identical for any number of
+    slabs."""
+
+    def __init__(self, ctx, cfg, pso, nx, ny, nz_total, dist=None, check_every: int = 4):
+        from dataclasses import replace
+        self.ctx, self.cfg, self.dist = ctx, cfg, dist
+        self.pso = replace(pso, p_begin=0, p_end=0)
+        self.geo = _SlabGeometry(ctx, nx, ny, nz_total, pso.P, dist)
+        self.grid = self.geo.grid
+        self.ws = ctx.slab_workspace(self.grid, cfg, self.pso)
+        self.check_every = check_every
+
+    def init(self, U0_slab: torch.Tensor, c0: torch.Tensor):
+        """U0_slab [(nz+2)*ny*nx][4] (slab layout), c0 [4]."""
+        self.ctx.slab_pso_init(self.grid, self.cfg, self.pso, U0_slab, c0, self.ws)
+
+    def generation(self, x_slab: torch.Tensor):
+        c, g, cfg, pso, ws = self.ctx, self.grid, self.cfg, self.pso, self.ws
+        self.geo.exchange(lambda op, buf: c.slab_pso_halo(g, cfg, pso, ws, op, buf),
+                          lambda op, buf: c.slab_pso_halo(g, cfg, pso, ws, op, buf))
+        c.slab_pso_eval(g, cfg, pso, x_slab, ws, self.geo.rec)
+        recs = self.geo.gather_records()
+        c.slab_pso_finalize(g, cfg, pso, ws, self.geo.world, self.geo.nrec_max, recs, counts=self.geo.counts)
+        c.slab_pso_update(g, cfg, pso, ws)
+
+    def fitness(self) -> torch.Tensor:
+        return self.ctx.slab_pso_fitness(self.grid, self.cfg, self.pso, self.ws)
+
+    def run(self, x_slab: torch.Tensor, max_gen: int, early_stop: bool, trace=None) -> PsoOutcome:
+        for gen in range(max_gen):
+            self.generation(x_slab)
+            if trace is not None:
+                trace.append(self.fitness().cpu().clone())
+            if early_stop and (gen + 1) % self.check_every == 0:
+                _, stopped = self.ctx.slab_pso_result(self.grid, self.cfg, self.pso, self.ws)
+                if stopped:
+                    break
+        s, _ = self.ctx.slab_pso_result(self.grid, self.cfg, self.pso, self.ws)
+        return PsoOutcome(s.lam, s.xi, s.J, s.generations, s.gbest_particle)
+
+    def gbest_state(self, U_out: torch.Tensor, c_out: torch.Tensor):
+        """The gbest particle's slab state (every rank holds its own part)."""
+        self.ctx.slab_pso_gbest_state(self.grid, self.cfg, self.pso, self.ws, U_out, c_out)
+
+
+class SlabSegmenter:
+    """The whole method (Alg. 1 / Alg. 2) on a volume split into z-slabs, one
+    per rank: global min-max (all-reduce) and histogram (all-reduce) for the
+    GMM start, the FCM start (lambda = xi = 0) as slab iterations, the PSO
+    over slabs (SlabPso), the final IFCM over slabs (SlabIfcm) and the argmax
+    of each slab, gathered.  Every reduction is over global z-chunk records in
+    a fixed order, so all results are bit-identical for any number of ranks."""
+
+    def __init__(self, ctx, cfg, pso, shape, dist=None):
+        self.ctx, self.cfg, self.pso, self.dist = ctx, cfg, pso, dist
+        self.nz, self.ny, self.nx = shape
+        self.ifcm = SlabIfcm(ctx, cfg, self.nx, self.ny, self.nz, 1, dist)
+        self.swarm = SlabPso(ctx, cfg, pso, self.nx, self.ny, self.nz, dist)
+        self.geo = self.ifcm.geo
+        self.dev = self.geo.dev
+        g = self.geo
+        self.lab_counts = [slab_range(self.nz, g.world, r, g.tz)[1] * self.nx * self.ny for r in range(g.world)]
+        self.lab_pad = torch.zeros((g.world, max(self.lab_counts)), dtype=torch.uint8, device=self.dev)
+        self.trace = None
+
+    def _allreduce(self, t, op):
+        if self.geo.world == 1:
+            return t
+        d = self.dist
+        h = _coll_tensor(d, t)
+        d.all_reduce(h, op=op)
+        if h is not t:
+            t.copy_(h)
+        return t
+
+    def segment(self, vol: torch.Tensor) -> dict:
+        """vol: the whole u8 volume [nz][ny][nx] (any device); each rank reads
+        its slab planes."""
+        ctx, cfg, g, d = self.ctx, self.cfg, self.geo, self.dist
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record()
+        # Alg. 2 step 1: global min-max (all-reduce) and the R15 histogram
+        v = g.slab_planes(vol)                      # [nz+2][ny][nx], zero outside the volume
+        own = v[1: g.nz + 1]
+        mm = torch.zeros(2, dtype=torch.int32, device=self.dev)
+        ctx.minmax_u8(own, mm)
+        if g.world > 1:
+            lo, hi = mm[:1].clone(), mm[1:].clone()
+            self._allreduce(lo, d.ReduceOp.MIN)
+            self._allreduce(hi, d.ReduceOp.MAX)
+            mm = torch.cat([lo, hi])
+        x = ctx.normalize_u8_range(v, mm)
+        if g.z0 == 0:
+            x[0].zero_()
+        if g.z0 + g.nz == g.nz_total:
+            x[g.nz + 1].zero_()
+        hist = ctx.hist_u8(own, mm)
+        if g.world > 1:
+            self._allreduce(hist, d.ReduceOp.SUM)
+        c0 = ctx.gmm_init(hist, cfg.C)
+        ev[1].record()
+        # Alg. 1 step 2: FCM start (lambda = xi = 0) from U = 0 (the first step
+        # reads no neighbourhood: its terms are multiplied by 0)
+        sl = self.ifcm
+        sl.set_x(x)
+        sl.load_local(torch.zeros_like(sl.Ua), c0.view(1, 4))
+        zero = torch.zeros((1, 2), dtype=torch.float64, device=self.dev)
+        sl.run(zero, cfg.max_iter, eps=cfg.eps)
+        fcm_iters = int(sl.stats[0, 2].item())
+        c_fcm = sl.centers[0].clone()
+        ev[2].record()
+        # Alg. 1 steps 3-10: PSO over slabs from (U_fcm, c_fcm)
+        sw = self.swarm
+        sw.init(sl.Ua[0], c_fcm)
+        self.trace = []
+        out = sw.run(x, self.pso.max_gen, early_stop=self.pso.patience > 0, trace=self.trace)
+        Ug = torch.empty_like(sl.Ua[0])
+        cg = torch.empty(4, dtype=torch.float32, device=self.dev)
+        sw.gbest_state(Ug, cg)
+        ev[3].record()
+        # Alg. 1 step 11: final IFCM at (lambda*, xi*), then argmax of each slab
+        lx = torch.tensor([[out.lam, out.xi]], dtype=torch.float64, device=self.dev)
+        sl.load_local(Ug.unsqueeze(0), cg.view(1, 4))
+        sl.run(lx, cfg.max_iter, eps=cfg.eps)
+        final_iters = int(sl.stats[0, 2].item())
+        loc = ctx.argmax(sl.local_U()[0], self.nx, self.ny, g.nz, cfg.C)
+        self.labels = self._gather_labels(loc)
+        ev[4].record()
+        torch.cuda.synchronize()
+        return {"lambda": out.lam, "xi": out.xi, "J": out.J, "generations": out.generations,
+                "gbest_particle": out.gbest_particle, "fcm_iters": fcm_iters, "final_iters": final_iters,
+                "c_init": c0[: cfg.C].tolist(), "centers": sl.centers[0, : cfg.C].tolist(),
+                "t_norm": ev[0].elapsed_time(ev[1]) * 1e-3, "t_init": ev[1].elapsed_time(ev[2]) * 1e-3,
+                "t_pso": ev[2].elapsed_time(ev[3]) * 1e-3, "t_final": ev[3].elapsed_time(ev[4]) * 1e-3,
+                "t_total": ev[0].elapsed_time(ev[4]) * 1e-3}
+
+    def _gather_labels(self, loc: torch.Tensor) -> torch.Tensor:
+        g = self.geo
+        if g.world == 1:
+            return loc
+        d = self.dist
+        self.lab_pad[g.rank, : loc.numel()] = loc.reshape(-1)
+        src = _coll_tensor(d, self.lab_pad[g.rank].contiguous())
+        out = _coll_tensor(d, self.lab_pad)
+        if src.device.type == "cpu":
+            torch.cuda.current_stream().synchronize()
+        d.all_gather_into_tensor(out.view(-1), src)
+        if out is not self.lab_pad:
+            self.lab_pad.copy_(out)
+        return torch.cat([self.lab_pad[r, :n] for r, n in enumerate(self.lab_counts)]).view(
+            self.nz, self.ny, self.nx)

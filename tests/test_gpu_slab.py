@@ -48,23 +48,7 @@ def _virtual_slabs(ctx, world, iters, lx):
     cfg = IfcmConfig(C=C)
     slabs = []
     for r in range(world):
-        s = SlabIfcm(ctx, cfg, NX, NY, NZ, P, dist=None)
-        from paper_2002_01981_b200.api import _grid
-        from paper_2002_01981_b200.dist import slab_range
-        s.world, s.rank = world, r
-        tz = ctx.slab_chunk(NX, NY, NZ)
-        s.z0, s.nz = slab_range(NZ, world, r, tz)
-        s.grid = _grid(NX, NY, s.nz, z0=s.z0, nz_total=NZ)
-        s.nrec = ctx.slab_records(s.grid)
-        nrecs = [ctx.slab_records(_grid(NX, NY, slab_range(NZ, world, q, tz)[1],
-                                        z0=slab_range(NZ, world, q, tz)[0], nz_total=NZ)) for q in range(world)]
-        s.nrec_max = max(nrecs)
-        s.counts = torch.tensor(nrecs, dtype=torch.int32, device=dev)
-        pl = NX * NY
-        s.Ua = torch.zeros((P, (s.nz + 2) * pl, 4), device=dev)
-        s.Ub = torch.zeros_like(s.Ua)
-        s.rec = torch.zeros((P, s.nrec, 10), dtype=torch.float64, device=dev)
-        s.rec_pad = torch.zeros((P, s.nrec_max, 10), dtype=torch.float64, device=dev)
+        s = SlabIfcm(ctx, cfg, NX, NY, NZ, P, dist=_OneRank(world, r))
         s.load_x(xt)
         s.load_state(Ut, ct)
         slabs.append(s)
@@ -74,19 +58,21 @@ def _virtual_slabs(ctx, world, iters, lx):
         for i, s in enumerate(slabs):
             if i > 0:
                 nb = slabs[i - 1]
-                s.halo["recv_lo"].copy_(nb.Ua[:, nb.nz * pl:(nb.nz + 1) * pl])
+                s.geo.halo["recv_lo"].copy_(nb.Ua[:, nb.nz * pl:(nb.nz + 1) * pl])
             if i < world - 1:
                 nb = slabs[i + 1]
-                s.halo["recv_hi"].copy_(nb.Ua[:, pl:2 * pl])
+                s.geo.halo["recv_hi"].copy_(nb.Ua[:, pl:2 * pl])
         for s in slabs:
-            s.ctx.slab_halo(s.grid, P, 2, s.Ua, s.halo["recv_lo"] if s.rank > 0 else None)
-            s.ctx.slab_halo(s.grid, P, 3, s.Ua, s.halo["recv_hi"] if s.rank < world - 1 else None)
-            s.ctx.slab_step(s.grid, cfg, s.x, s.Ua, s.Ub, s.centers, lxt, s.rec)
-            s.rec_pad.zero_()
-            s.rec_pad[:, : s.nrec] = s.rec
-        gathered = torch.stack([s.rec_pad for s in slabs])
+            h = s.geo.halo
+            s.ctx.slab_halo(s.grid, P, 2, s.Ua, h["recv_lo"] if s.rank > 0 else None)
+            s.ctx.slab_halo(s.grid, P, 3, s.Ua, h["recv_hi"] if s.rank < world - 1 else None)
+            s.ctx.slab_step(s.grid, cfg, s.x, s.Ua, s.Ub, s.centers, lxt, s.geo.rec)
+            s.geo.rec_pad.zero_()
+            s.geo.rec_pad[:, : s.geo.nrec] = s.geo.rec
+        gathered = torch.stack([s.geo.rec_pad for s in slabs])
         for s in slabs:
-            s.ctx.slab_finalize(C, P, world, s.nrec_max, gathered, s.centers, stats=s.stats, counts=s.counts)
+            s.ctx.slab_finalize(C, P, world, s.geo.nrec_max, gathered, s.centers, stats=s.stats,
+                                counts=s.geo.counts)
             s.Ua, s.Ub = s.Ub, s.Ua
     U_full = torch.cat([s.local_U() for s in slabs], dim=1)
     return U_full, slabs[0].centers.clone(), slabs[0].stats.clone(), [s.centers for s in slabs]
