@@ -30,6 +30,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = "C3: BrainWeb-shaped 181x217x181 synthetic phantom (CSF/GM/WM), 9% noise, C=4, 26-neighbour 3D IFCM, PSO 32 particles x 30 generations"
+WORKLOAD_C5 = ("C5: 512x512x512 synthetic noisy volume (4 nested cubes, 7% noise), C=4, z-slab sharded "
+               "(halo exchange + record all-gather), PSO {P} particles x 30 generations")
 METRIC = "voxel-iterations/s (x particles)"
 SHAPE = (181, 217, 181)  # (nz, ny, nx) with nx = 181, ny = 217, nz = 181
 C, P, GENS = 4, 32, 30
@@ -107,16 +109,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def _volume():
+def _volume(name="C3"):
     from inputs import config_volume
-    vol, _ = config_volume("C3")
+    vol, _ = config_volume(name)
     return vol
 
 
-def cpu_baseline_measure(vol, budget_s=20.0):
+def cpu_baseline_measure(vol, budget_s=20.0, P=P):
     """The oracle as it stands (fp64 C, OpenMP on all host cores) on a bounded
     sample of the same workload: whole IFCM steps of single particles over the
-    full 181x217x181 volume, repeated until ~budget_s of CPU work."""
+    full volume, repeated until ~budget_s of CPU work."""
     import numpy as np
 
     import oracle
@@ -138,7 +140,7 @@ def cpu_baseline_measure(vol, budget_s=20.0):
     return {"value": n_vox * steps / el, "unit": "voxel-iterations/s (x particles)",
             "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"{steps} oracle IFCM steps (one particle each, lambda/xi from the bench "
-                      f"swarm) over the full 181x217x181 C3 volume, {el:.1f} s"}
+                      f"swarm) over the full {'x'.join(map(str, vol.shape[::-1]))} volume, {el:.1f} s"}
 
 
 def run_reference(args, rank, world):
@@ -147,7 +149,9 @@ def run_reference(args, rank, world):
         return
     import oracle
     oracle.build_oracle()
-    vol = _volume()
+    c5 = args.workload == "C5"
+    vol = _volume("C5" if c5 else "C3")
+    workload = WORKLOAD_C5.format(P=64 if world >= 2 else 32) if c5 else WORKLOAD
     x = oracle.normalize_u8(vol)
     c0 = oracle.gmm_init(oracle.histogram_u8(vol), C)
     U, c, _ = oracle.fcm_run(x, c0, max_iter=1)
@@ -164,7 +168,7 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "reference_step": "one oracle IFCM step of one particle over the full volume"},
+        "config": {"workload": workload, "reference_step": "one oracle IFCM step of one particle over the full volume"},
         "cpu_baseline": {"value": value, "unit": "voxel-iterations/s (x particles)",
                          "cores": oracle.num_threads(), "kind": "oracle",
                          "sample": f"{args.steps} oracle IFCM steps of one particle each over the full volume"},
@@ -191,16 +195,33 @@ def run_ours(args, rank, world, local_rank):
         tdist.init_process_group("nccl", device_id=dev)
         dist = tdist
     ctx = Context(local_rank)
-    vol = _volume()
+    c5 = args.workload == "C5"
+    vol = _volume("C5" if c5 else "C3")
     nz, ny, nx = vol.shape
+    # C5: P = 64 as configured when the slot pool fits (>= 2 GPUs: 129 slots of
+    # the slab); one GPU holds 65 slots of the whole 512^3 volume (140 GB): P = 32
+    Pw = (64 if world >= 2 else 32) if c5 else P
+    workload = WORKLOAD_C5.format(P=Pw) if c5 else WORKLOAD
     cfg = IfcmConfig(C=C, m=2.0, q_mode=0, eps=1e-5, max_iter=100)
-    pso = PsoConfig(P=P, ring_k=1, max_gen=GENS, patience=0, seed=12345)
+    pso = PsoConfig(P=Pw, ring_k=1, max_gen=GENS, patience=0, seed=12345)
     vol_d = torch.as_tensor(vol, device=dev)
     vol_h = torch.as_tensor(vol).pin_memory()
     lab_h = torch.empty(vol.shape, dtype=torch.uint8).pin_memory()
     stream = torch.cuda.current_stream(dev)
 
-    if world > 1:
+    if c5:
+        from paper_2002_01981_b200.dist import SlabSegmenter
+        seg = SlabSegmenter(ctx, cfg, pso, (nz, ny, nx), dist)
+
+        def step():
+            return seg.segment(vol_d)
+
+        def step_host():
+            rep = seg.segment(vol_h)
+            lab_h.copy_(seg.labels, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return rep
+    elif world > 1:
         from paper_2002_01981_b200.dist import ShardedSegmenter
         seg = ShardedSegmenter(ctx, cfg, pso, (nz, ny, nx), dist)
 
@@ -254,7 +275,7 @@ def run_ours(args, rank, world, local_rank):
     s_ms, s_n, s_bytes = ctx.timing_read(batched=False)    # final IFCM: one state per launch
     ctx.timing_enable(False)
     for r in reps:
-        vp = nx * ny * nz * (r["fcm_iters"] + P * r["generations"] + r["final_iters"])
+        vp = nx * ny * nz * (r["fcm_iters"] + Pw * r["generations"] + r["final_iters"])
         vp_total += vp
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -270,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
     vp_e2e = 0.0
     for _ in range(args.steps):
         r = step_host()
-        vp_e2e += nx * ny * nz * (r["fcm_iters"] + P * r["generations"] + r["final_iters"])
+        vp_e2e += nx * ny * nz * (r["fcm_iters"] + Pw * r["generations"] + r["final_iters"])
     h1.record(stream)
     barrier()
     te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
@@ -287,15 +308,16 @@ def run_ours(args, rank, world, local_rank):
     hbm, hbm_kind = _peaks()
     achieved = (k_bytes / k_n) / ((k_ms / k_n) * 1e-3) / 1e9 if k_n else None
     traffic = None
-    try:
-        with open(PROFILE_SUMMARY) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    if not c5:  # the committed ncu capture is of the C3 P = 32 launch
+        try:
+            with open(PROFILE_SUMMARY) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            pass
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            cpu = cpu_baseline_measure(vol, budget_s=args.cpu_budget)
+            cpu = cpu_baseline_measure(vol, budget_s=args.cpu_budget, P=Pw)
         except Exception as e:  # reported, never silently substituted
             cpu = {"value": None, "error": str(e), "kind": "oracle"}
     last = reps[-1]
@@ -313,18 +335,21 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "f32",
         "data": "synthetic",
         "config": {
-            "workload": WORKLOAD,
-            "volume": [nx, ny, nz], "C": C, "P": P, "generations": GENS, "m": 2.0,
+            "workload": workload,
+            "volume": [nx, ny, nz], "C": C, "P": Pw, "generations": GENS, "m": 2.0,
             "q_mode": "literal", "eps": 1e-5, "fitness": "chained",
-            "parallelism": f"particles/{world}",
-            "l2": "inputs larger than L2 (65 x 114 MB membership slots, every generation streams 7.3 GB)",
+            "parallelism": f"z-slabs/{world}" if c5 else f"particles/{world}",
+            "l2": ("inputs larger than L2 (the membership slot pool is "
+                   f"{(2 * Pw + 1) * nx * ny * nz * 16 / 1e9:.1f} GB; every generation streams "
+                   f"{Pw * nx * ny * nz * 32 / 1e9:.1f} GB)"),
             "pso_wall_ms": last["t_pso"] * 1e3, "segment_wall_ms": last["t_total"] * 1e3,
             "fcm_iters": last["fcm_iters"], "final_iters": last["final_iters"],
             "lambda_star": last["lambda"], "xi_star": last["xi"],
         },
         "roofline": {
             "bound": "hbm",
-            "kernel": "k_step_stencil, one launch = one PSO generation (all P particles' fused IFCM steps)",
+            "kernel": ("k_step_stencil, one launch = one PSO generation (all P particles' fused IFCM steps"
+                       + (", this rank's slab)" if c5 else ")")),
             "achieved": achieved,
             "peak": hbm,
             "peak_kind": hbm_kind,
@@ -363,6 +388,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--workload", default="C3", choices=["C3", "C5"],
+                    help="C3 (default, the BASELINE metric's config) or C5 (512^3, z-slab sharded)")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)

@@ -176,6 +176,31 @@ int check_ws(pifcm_ctx *ctx, void *ws, size_t ws_bytes, size_t need) {
     return PIFCM_OK;
 }
 
+// A step launch, bracketed by CUDA events on its stream when timing is on
+// (stencil launches only; vox = the voxels the launch updates per state).
+int timed_step(pifcm_ctx *ctx, const StepArgs &a, int C, bool stencil, int P, long long vox, cudaStream_t st) {
+    const bool timed = ctx->timing && stencil;
+    if (timed) {
+        while (ctx->tev.size() < ctx->tused + 2) {
+            cudaEvent_t e;
+            CK(ctx, cudaEventCreate(&e));
+            ctx->tev.push_back(e);
+        }
+        CK(ctx, cudaEventRecord(ctx->tev[ctx->tused], st));
+    }
+    LAUNCH(ctx, 1, launch_step(a, C, stencil, P, st));
+    if (timed) {
+        CK(ctx, cudaEventRecord(ctx->tev[ctx->tused + 1], st));
+        const int cls = P > 1 ? 0 : 1;
+        if (ctx->tcls.size() < ctx->tused / 2 + 1) ctx->tcls.resize(ctx->tused / 2 + 1);
+        ctx->tcls[ctx->tused / 2] = cls;
+        ctx->tused += 2;
+        ctx->t_bytes[cls] += 32.0 * (double)vox * P + 4.0 * (double)vox;
+        ctx->t_launches[cls] += 1;
+    }
+    return PIFCM_OK;
+}
+
 // One step launch + finalize for P states.
 int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x,
              const float4 *Uin, float4 *Uout, const int *in_idx, const int *out_idx,
@@ -200,25 +225,8 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     a.stats_out = stats;
     a.eps = eps;
     a.status = status;
-    const bool timed = ctx->timing && stencil;
-    if (timed) {
-        while (ctx->tev.size() < ctx->tused + 2) {
-            cudaEvent_t e;
-            CK(ctx, cudaEventCreate(&e));
-            ctx->tev.push_back(e);
-        }
-        CK(ctx, cudaEventRecord(ctx->tev[ctx->tused], st));
-    }
-    LAUNCH(ctx, 1, launch_step(a, cfg->C, stencil, P, st));
-    if (timed) {
-        CK(ctx, cudaEventRecord(ctx->tev[ctx->tused + 1], st));
-        const int cls = P > 1 ? 0 : 1;
-        if (ctx->tcls.size() < ctx->tused / 2 + 1) ctx->tcls.resize(ctx->tused / 2 + 1);
-        ctx->tcls[ctx->tused / 2] = cls;
-        ctx->tused += 2;
-        ctx->t_bytes[cls] += 32.0 * (double)a.nvox * P + 4.0 * (double)a.nvox;
-        ctx->t_launches[cls] += 1;
-    }
+    int r = timed_step(ctx, a, cfg->C, stencil, P, a.nvox, st);
+    if (r) return r;
     // Eq. 3 / Eq. 1 finalisation is fused: the last CTA of each state sums the
     // partial records (finalize_if_last in step.cu) -- in the canonical
     // decomposition exactly as k_slab_finalize sums the records of a slab split
@@ -767,8 +775,8 @@ int pifcm_slab_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg
     a.want_du = 1;
     a.counters = nullptr;  // records are combined across ranks by pifcm_slab_finalize
     a.C = cfg->C;
-    LAUNCH(ctx, 1, launch_step(a, cfg->C, true, P, reinterpret_cast<cudaStream_t>(stream)));
-    return PIFCM_OK;
+    return timed_step(ctx, a, cfg->C, true, P, (long long)grid->nx * grid->ny * grid->nz,
+                      reinterpret_cast<cudaStream_t>(stream));
 }
 
 int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int32_t nrec, const int32_t *counts,
@@ -922,8 +930,8 @@ int pifcm_slab_pso_eval(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm
     a.n_in_states = L.nslots;
     a.counters = nullptr;  // records are combined across ranks by pifcm_slab_pso_finalize
     a.C = cfg->C;
-    LAUNCH(ctx, 1, launch_step(a, cfg->C, true, L.Pl, reinterpret_cast<cudaStream_t>(stream)));
-    return PIFCM_OK;
+    return timed_step(ctx, a, cfg->C, true, L.Pl, (long long)slab->nx * slab->ny * slab->nz,
+                      reinterpret_cast<cudaStream_t>(stream));
 }
 
 int pifcm_slab_pso_finalize(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,

@@ -519,6 +519,7 @@ class SlabSegmenter:
         g = self.geo
         self.lab_counts = [slab_range(self.nz, g.world, r, g.tz)[1] * self.nx * self.ny for r in range(g.world)]
         self.lab_pad = torch.zeros((g.world, max(self.lab_counts)), dtype=torch.uint8, device=self.dev)
+        self.keep_trace = False  # record every generation's fitness vector (host sync per generation)
         self.trace = None
 
     def _allreduce(self, t, op):
@@ -570,7 +571,7 @@ class SlabSegmenter:
         # Alg. 1 steps 3-10: PSO over slabs from (U_fcm, c_fcm)
         sw = self.swarm
         sw.init(sl.Ua[0], c_fcm)
-        self.trace = []
+        self.trace = [] if self.keep_trace else None
         out = sw.run(x, self.pso.max_gen, early_stop=self.pso.patience > 0, trace=self.trace)
         Ug = torch.empty_like(sl.Ua[0])
         cg = torch.empty(4, dtype=torch.float32, device=self.dev)

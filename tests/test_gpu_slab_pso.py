@@ -99,6 +99,7 @@ def _worker(rank, world, port, shape, q):
     ctx = Context(0)
     vol, _ = _case(4, shape, seed=6)
     seg = SlabSegmenter(ctx, IfcmConfig(C=4), PsoConfig(P=5, max_gen=4, patience=0, seed=31), vol.shape, dist)
+    seg.keep_trace = True
     rep = seg.segment(torch.as_tensor(vol, device="cuda:0"))
     q.put((rank, seg.labels.cpu().numpy(), rep, np.stack([t.numpy() for t in seg.trace]),
            seg.geo.z0, seg.geo.nz))
@@ -122,6 +123,7 @@ def test_slab_segmenter_g_invariant(ctx):
     shape = (40, 26, 30)
     vol, _ = _case(4, shape, seed=6)
     seg = SlabSegmenter(ctx, IfcmConfig(C=4), PsoConfig(P=5, max_gen=4, patience=0, seed=31), vol.shape)
+    seg.keep_trace = True
     ref = seg.segment(torch.as_tensor(vol, device="cuda:0"))
     ref_lab = seg.labels.cpu().numpy()
     ref_tr = np.stack([t.numpy() for t in seg.trace])
