@@ -77,14 +77,14 @@ def _declare(L):
     L.orc_pso_move.argtypes = [i, d, _dp, _dp, _ip, _dp, _dp, _dp]
     L.orc_pso_update.argtypes = [i, i, ct.c_uint32, u64, d, _dp, _dp, _dp, _dp, _dp, _ip, _ip]
     L.orc_pso_run.argtypes = [_dp, i, i, i, i, d, i, i, d, _dp, _dp, i, i, i, i, d, d, d, u64,
-                              _dp, _dp, _dp, _dp, _dp, _dp, _ip]
+                              _dp, _dp, _dp, _dp, _dp, _dp, _ip, i]
     L.orc_pso_run.restype = i
     L.orc_ifcm_run.argtypes = [_dp, i, i, i, i, d, d, d, i, i, d, d, i, _dp, _dp, _dp]
     L.orc_ifcm_run.restype = i
     L.orc_fcm_run.argtypes = [_dp, l, i, d, d, i, _dp, _dp, _dp]
     L.orc_fcm_run.restype = i
     L.orc_segment_u8.argtypes = [_u8p, i, i, i, i, d, i, i, d, d, i, i, i, i, i, d, d, d, u64,
-                                 _u8p, _dp, _dp, _dp, _dp, _ip, _ip, _dp]
+                                 _u8p, _dp, _dp, _dp, _dp, _ip, _ip, _dp, i]
     L.orc_segment_u8.restype = i
     L.orc_num_threads.restype = i
     L.orc_set_num_threads.argtypes = [i]
@@ -251,7 +251,8 @@ class PsoResult:
 
 
 def pso_run(x, U0, c0, P, max_gen, seed, m=2.0, q_mode=0, v=1, h=1.0, ring_k=1, patience=0,
-            tol=1e-4, v0=0.1, vmax=0.5):
+            tol=1e-4, v0=0.1, vmax=0.5, fitness_mode=0):
+    """fitness_mode: 0 CHAINED, 1 ANCHORED, 2 LEADER (pifcm_oracle.c orc_pso_run)."""
     x = _f64(x)
     nz, ny, nx = x.shape
     U0 = _f64(U0)
@@ -266,7 +267,7 @@ def pso_run(x, U0, c0, P, max_gen, seed, m=2.0, q_mode=0, v=1, h=1.0, ring_k=1, 
     tg = np.zeros(max_gen, np.int32)
     gens = _L().orc_pso_run(_p(x), nx, ny, nz, C, m, q_mode, v, h, _p(U0), _p(c0), P, ring_k,
                             max_gen, patience, tol, v0, vmax, seed, _p(lx), ct.byref(J), _p(Ub),
-                            _p(cb), _p(tp), _p(tf), tg.ctypes.data_as(_ip))
+                            _p(cb), _p(tp), _p(tf), tg.ctypes.data_as(_ip), fitness_mode)
     return PsoResult(lx[0], lx[1], J.value, Ub, cb, gens, tp[:gens], tf[:gens], tg[:gens])
 
 
@@ -305,7 +306,7 @@ class SegmentResult:
 
 
 def segment_u8(vol, C, P, max_gen, seed, m=2.0, q_mode=0, v=1, h=1.0, eps=1e-5, max_iter=100,
-               ring_k=1, patience=0, tol=1e-4, v0=0.1, vmax=0.5, want_U=True):
+               ring_k=1, patience=0, tol=1e-4, v0=0.1, vmax=0.5, want_U=True, fitness_mode=0):
     vol = np.ascontiguousarray(vol, dtype=np.uint8)
     nz, ny, nx = vol.shape
     N = vol.size
@@ -319,6 +320,6 @@ def segment_u8(vol, C, P, max_gen, seed, m=2.0, q_mode=0, v=1, h=1.0, eps=1e-5, 
     ci = np.empty(C)
     _L().orc_segment_u8(_p(vol, _u8p), nx, ny, nz, C, m, q_mode, v, h, eps, max_iter, P, ring_k,
                         max_gen, patience, tol, v0, vmax, seed, _p(lab, _u8p), _p(U), _p(c),
-                        _p(lx), ct.byref(J), ct.byref(gens), ct.byref(fi), _p(ci))
+                        _p(lx), ct.byref(J), ct.byref(gens), ct.byref(fi), _p(ci), fitness_mode)
     return SegmentResult(lab.reshape(nz, ny, nx), U, c, lx[0], lx[1], J.value, gens.value,
                          fi.value, ci)

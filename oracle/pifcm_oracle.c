@@ -532,9 +532,18 @@ void orc_pso_update(int P, int ring_k, uint32_t gen, uint64_t seed, double vmax,
 }
 
 /* ------------------------------------------------------------------------- */
-/* PSO over (lambda, xi) with CHAINED fitness (R11): particle p owns a state   */
-/* (U_p, c_p) that starts at (U0, c0); each generation advances it by one IFCM */
-/* step at the particle's current position, and the fitness is that step's J. */
+/* PSO over (lambda, xi) (Alg. 1 steps 3-10).  Fitness modes     */
+/* (R11):                                                 */
+/*  0 CHAINED  particle p owns a state (U_p, c_p) that starts at (U0, c0); each*/
+/*             generation advances it by one IFCM step at the particle's       */
+/*             current position, and the fitness is that step's J.            */
+/*  1 ANCHORED every evaluation is one IFCM step from the shared start         */
+/*             (U0, c0) at the particle's position; fitness = its J.          */
+/*  2 LEADER   every evaluation is one step from the shared state S_t (S_0 =   */
+/*             (U0, c0)); after the generation's PSO update, S_{t+1} = the     */
+/*             state the gbest particle's evaluation produced (R22).          */
+/* In every mode the gbest snapshot is the (U, c) produced by the evaluation   */
+/* that improved the gbest (Alg. 1 step 10).                        */
 /* Stop (R12, Alg. 1 step 9 "until convergence (i.e small changes to J)"):    */
 /* relative change of the gbest fitness < tol for `patience` consecutive       */
 /* generations, or max_gen.  patience <= 0 disables the early stop.            */
@@ -550,34 +559,42 @@ int orc_pso_run(const double *x, int nx, int ny, int nz, int C, double m, int q_
                 double *best_c /*[C]*/,
                 double *trace_pos /*[max_gen][P][2] nullable*/,
                 double *trace_f /*[max_gen][P] nullable*/,
-                int *trace_gbest /*[max_gen] nullable*/) {
+                int *trace_gbest /*[max_gen] nullable*/, int fitness_mode) {
     const long N = (long)nx * ny * nz;
+    const int shared = (fitness_mode == 1 || fitness_mode == 2);
     double *pos = (double *)malloc(sizeof(double) * 2 * P);
     double *vel = (double *)malloc(sizeof(double) * 2 * P);
     double *pbf = (double *)malloc(sizeof(double) * P);
     double *pbx = (double *)malloc(sizeof(double) * 2 * P);
     double *f = (double *)malloc(sizeof(double) * P);
-    double *Us = (double *)malloc(sizeof(double) * (size_t)N * C * P);
+    /* CHAINED: one state per particle; ANCHORED / LEADER: one shared state */
+    const int nst = shared ? 1 : P;
+    double *Us = (double *)malloc(sizeof(double) * (size_t)N * C * nst);
     double *Ut = (double *)malloc(sizeof(double) * (size_t)N * C);
-    double *cs = (double *)malloc(sizeof(double) * C * P);
+    double *cs = (double *)malloc(sizeof(double) * C * nst);
     double *eval_pos = (double *)malloc(sizeof(double) * 2 * P);
     orc_pso_init(P, seed, v0, pos, vel);
     for (int p = 0; p < P; ++p) {
         pbf[p] = INFINITY;
         pbx[2 * p] = pos[2 * p];
         pbx[2 * p + 1] = pos[2 * p + 1];
-        memcpy(Us + (size_t)p * N * C, U0, sizeof(double) * (size_t)N * C);
-        memcpy(cs + (size_t)p * C, c0, sizeof(double) * C);
+        if (p < nst) {
+            memcpy(Us + (size_t)p * N * C, U0, sizeof(double) * (size_t)N * C);
+            memcpy(cs + (size_t)p * C, c0, sizeof(double) * C);
+        }
     }
     int gbest = -1, improved = 0, gen = 0, calm = 0;
     double prev_gf = INFINITY;
     for (gen = 0; gen < max_gen; ++gen) {
         for (int p = 0; p < P; ++p) {
             double cn[8], J, du;
+            const int sp = shared ? 0 : p;
             orc_ifcm_step(x, nx, ny, nz, C, m, pos[2 * p], pos[2 * p + 1], q_mode, v, h,
-                          Us + (size_t)p * N * C, cs + (size_t)p * C, Ut, cn, &J, &du);
-            memcpy(Us + (size_t)p * N * C, Ut, sizeof(double) * (size_t)N * C);
-            memcpy(cs + (size_t)p * C, cn, sizeof(double) * C);
+                          Us + (size_t)sp * N * C, cs + (size_t)sp * C, Ut, cn, &J, &du);
+            if (!shared) {
+                memcpy(Us + (size_t)p * N * C, Ut, sizeof(double) * (size_t)N * C);
+                memcpy(cs + (size_t)p * C, cn, sizeof(double) * C);
+            }
             f[p] = J;
             if (trace_pos) { trace_pos[((size_t)gen * P + p) * 2] = pos[2 * p];
                              trace_pos[((size_t)gen * P + p) * 2 + 1] = pos[2 * p + 1]; }
@@ -587,12 +604,29 @@ int orc_pso_run(const double *x, int nx, int ny, int nz, int C, double m, int q_
         memcpy(eval_pos, pos, sizeof(double) * 2 * P);
         orc_pso_update(P, ring_k, (uint32_t)gen, seed, vmax, f, pos, vel, pbf, pbx, &gbest, &improved);
         if (trace_gbest) trace_gbest[gen] = gbest;
+        double cg[8];
+        if (shared && (improved || fitness_mode == 2)) {
+            /* the state the gbest's evaluation produced this generation (the
+             * evaluation is deterministic, so it is recomputed rather than kept) */
+            double J, du;
+            orc_ifcm_step(x, nx, ny, nz, C, m, eval_pos[2 * gbest], eval_pos[2 * gbest + 1], q_mode, v, h,
+                          Us, cs, Ut, cg, &J, &du);
+        }
         if (improved) {
             best_lx[0] = eval_pos[2 * gbest];
             best_lx[1] = eval_pos[2 * gbest + 1];
             *best_J = pbf[gbest];
-            memcpy(best_U, Us + (size_t)gbest * N * C, sizeof(double) * (size_t)N * C);
-            memcpy(best_c, cs + (size_t)gbest * C, sizeof(double) * C);
+            if (shared) {
+                memcpy(best_U, Ut, sizeof(double) * (size_t)N * C);
+                memcpy(best_c, cg, sizeof(double) * C);
+            } else {
+                memcpy(best_U, Us + (size_t)gbest * N * C, sizeof(double) * (size_t)N * C);
+                memcpy(best_c, cs + (size_t)gbest * C, sizeof(double) * C);
+            }
+        }
+        if (fitness_mode == 2) { /* LEADER: the shared state follows the gbest's step */
+            memcpy(Us, Ut, sizeof(double) * (size_t)N * C);
+            memcpy(cs, cg, sizeof(double) * C);
         }
         const double gf = pbf[gbest];
         if (gen > 0 && patience > 0) {
@@ -653,7 +687,7 @@ int orc_fcm_run(const double *x, long N, int C, double m, double eps, int max_it
 }
 
 /* The whole pipeline (Alg. 1 / Alg. 2) on a u8 volume:
- * normalise -> histogram + GMM -> FCM -> PSO (CHAINED) -> final IFCM at the
+ * normalise -> histogram + GMM -> FCM -> PSO (fitness_mode) -> final IFCM at the
  * gbest (lambda*, xi*) from the gbest's (U, c) -> argmax labels.
  * Parity unpinned end to end (only oracle-vs-GPU agreement); its parts are
  * pinned individually. */
@@ -663,7 +697,7 @@ int orc_segment_u8(const uint8_t *vol, int nx, int ny, int nz, int C, double m, 
                    double vmax, uint64_t seed,
                    uint8_t *labels, double *U_out /*[N][C] nullable*/, double *c_out /*[C]*/,
                    double *lam_xi_out /*[2]*/, double *J_out, int *gens_out, int *final_iters_out,
-                   double *c_init_out /*[C] nullable: GMM centres*/) {
+                   double *c_init_out /*[C] nullable: GMM centres*/, int fitness_mode) {
     const long N = (long)nx * ny * nz;
     double *x = (double *)malloc(sizeof(double) * (size_t)N);
     double *U = (double *)malloc(sizeof(double) * (size_t)N * C);
@@ -676,7 +710,8 @@ int orc_segment_u8(const uint8_t *vol, int nx, int ny, int nz, int C, double m, 
     if (c_init_out) memcpy(c_init_out, c0, sizeof(double) * C);
     orc_fcm_run(x, N, C, m, eps, max_iter, c0, U, c1);
     const int gens = orc_pso_run(x, nx, ny, nz, C, m, q_mode, v, h, U, c1, P, ring_k, max_gen,
-                                 patience, tol, v0, vmax, seed, lx, &Jb, Ub, cb, NULL, NULL, NULL);
+                                 patience, tol, v0, vmax, seed, lx, &Jb, Ub, cb, NULL, NULL, NULL,
+                                 fitness_mode);
     double Jf = 0.0;
     const int fi = orc_ifcm_run(x, nx, ny, nz, C, m, lx[0], lx[1], q_mode, v, h, eps, max_iter,
                                 Ub, cb, &Jf);

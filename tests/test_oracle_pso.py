@@ -119,6 +119,57 @@ def test_pso_run_on_step_fitness(orc):
     assert r.trace_f[0].min() <= J00 + 1e-15
 
 
+def _mode_problem(orc):
+    from inputs import add_noise_u8, cube_phantom
+    img, _ = cube_phantom(10, 9, 3, (0.1, 0.5, 0.9))
+    x = add_noise_u8(img, 7.0, 4).astype(np.float64) / 255.0
+    U0, c0, _ = orc.fcm_run(x, np.array([0.1, 0.5, 0.9]))
+    return x, U0, c0
+
+
+def _assert_monotone(pos, f):
+    """From one fixed state J is non-increasing in lambda and in xi (pinned in
+    test_oracle_pins.test_cost_monotone_in_lambda_xi): any two evaluations of
+    the same state must be ordered accordingly."""
+    for a in range(len(f)):
+        for b in range(len(f)):
+            if pos[a, 0] <= pos[b, 0] and pos[a, 1] <= pos[b, 1]:
+                assert f[a] >= f[b] - 1e-12 * abs(f[b]), (pos[a], pos[b], f[a], f[b])
+
+
+def test_pso_anchored_mode(orc):
+    """ANCHORED: every evaluation is one step from the
+    shared start, so (i) every fitness of the run is ordered by the
+    monotonicity of J in (lambda, xi) -- across all generations --, (ii) the
+    first generation equals CHAINED's, (iii) the gbest snapshot is the step
+    from the start at (lambda*, xi*)."""
+    x, U0, c0 = _mode_problem(orc)
+    r = orc.pso_run(x, U0, c0, P=6, max_gen=6, seed=77, fitness_mode=1)
+    rc = orc.pso_run(x, U0, c0, P=6, max_gen=1, seed=77, fitness_mode=0)
+    assert (r.trace_f[0] == rc.trace_f[0]).all()
+    _assert_monotone(r.trace_pos.reshape(-1, 2), r.trace_f.ravel())
+    Ub, cb, Jb, _ = orc.ifcm_step(x, U0, c0, r.lam, r.xi)
+    assert Jb == r.J and (Ub == r.U).all() and (cb == r.c).all()
+    assert r.J == r.trace_f.min()
+
+
+def test_pso_leader_mode(orc):
+    """LEADER (R22): within a generation all evaluations share one state
+    (monotonicity per generation); generation 0 equals ANCHORED's; generation
+    1 is evaluated from the state the gbest's generation-0 evaluation produced."""
+    x, U0, c0 = _mode_problem(orc)
+    r = orc.pso_run(x, U0, c0, P=5, max_gen=4, seed=91, fitness_mode=2)
+    ra = orc.pso_run(x, U0, c0, P=5, max_gen=1, seed=91, fitness_mode=1)
+    assert (r.trace_f[0] == ra.trace_f[0]).all()
+    for g in range(4):
+        _assert_monotone(r.trace_pos[g], r.trace_f[g])
+    g0 = r.trace_gbest[0]
+    U1, c1, _, _ = orc.ifcm_step(x, U0, c0, *r.trace_pos[0, g0])
+    for p in range(5):
+        _, _, J, _ = orc.ifcm_step(x, U1, c1, *r.trace_pos[1, p])
+        assert J == r.trace_f[1, p]
+
+
 def test_pso_early_stop(orc):
     from inputs import cube_phantom
     img, _ = cube_phantom(8, 8, 2, (0.1, 0.9))
