@@ -76,7 +76,13 @@ typedef enum {
 } pifcm_status;
 
 typedef enum { PIFCM_Q_LITERAL = 0, PIFCM_Q_SQEUCLID = 1 } pifcm_qmode; /* R1 */
-typedef enum { PIFCM_FIT_CHAINED = 0 } pifcm_fitness;                   /* R11 */
+/* Fitness of a PSO particle (R11): CHAINED = each particle owns a
+ * state and advances it one step per generation; ANCHORED = every evaluation
+ * is one step from the shared start (U0, c0); LEADER = every evaluation is one
+ * step from a shared state that follows the gbest's evaluation (R22).  In
+ * ANCHORED / LEADER the particle-invariant H, F of the shared state are
+ * computed once per state and the P fitness values are pointwise. */
+typedef enum { PIFCM_FIT_CHAINED = 0, PIFCM_FIT_ANCHORED = 1, PIFCM_FIT_LEADER = 2 } pifcm_fitness;
 typedef enum { PIFCM_U8 = 0, PIFCM_U16 = 1, PIFCM_F32 = 2 } pifcm_dtype;
 
 typedef struct pifcm_ctx pifcm_ctx;
@@ -119,7 +125,7 @@ typedef struct {
     double v0;          /* initial |velocity| bound                               */
     double vmax;        /* velocity clamp                                         */
     uint64_t seed;      /* Philox4x32-10 key                                      */
-    int32_t fitness_mode; /* pifcm_fitness; CHAINED only                          */
+    int32_t fitness_mode; /* pifcm_fitness (ANCHORED / LEADER: P <= 128)           */
     int32_t p_begin;    /* this process evaluates particles [p_begin, p_end)      */
     int32_t p_end;      /*   (particle sharding; 0,0 means all P)                 */
 } pifcm_pso_cfg;
@@ -196,9 +202,11 @@ int pifcm_pso_init(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
                    void *ws, size_t ws_bytes, pifcm_stream stream);
 
 /* Fitness evaluation of this process's particles [p_begin, p_end) for the
- * current generation (Alg. 1 step 4; CHAINED fitness R11): one
- * IFCM step of each particle's state at its (lambda, xi); the J values land in
- * the fitness vector returned by pifcm_pso_fitness_ptr().  Async. */
+ * current generation (Alg. 1 step 4; fitness modes R11 / R22): the
+ * J of one IFCM step of the particle's state (CHAINED) or of the shared state
+ * (ANCHORED, LEADER) at its (lambda, xi); the J values land in the fitness
+ * vector returned by pifcm_pso_fitness_ptr().  x must stay the same during a
+ * PSO run (ANCHORED computes the shared H, F once).  Async. */
 int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
                    const pifcm_pso_cfg *pso, const float *x, void *ws, size_t ws_bytes,
                    pifcm_stream stream);
@@ -211,9 +219,13 @@ int pifcm_pso_fitness_ptr(const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
 
 /* PSO bookkeeping and move after all P fitnesses are known (Alg. 1 steps 5-8,
  * PAPER:99-102): pbest (strict <), ring lbest, velocity, fly, gbest snapshot
- * and the stop test of step 9 (R12).  Identical on every process.  Async. */
+ * and the stop test of step 9 (R12).  Identical on every process.  ANCHORED:
+ * on an improvement the snapshot step from the start runs here; LEADER: the
+ * shared state advances here by the gbest's step (x dev fp32 [nz][ny][pitch],
+ * required for those modes, may be NULL for CHAINED).  Async. */
 int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
-                     const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, pifcm_stream stream);
+                     const pifcm_pso_cfg *pso, const float *x, void *ws, size_t ws_bytes,
+                     pifcm_stream stream);
 
 /* One generation on one process: pifcm_pso_eval + pifcm_pso_update.  Async. */
 int pifcm_pso_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,

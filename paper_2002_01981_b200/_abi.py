@@ -16,6 +16,8 @@ STATUS = {0: "PIFCM_OK", -1: "PIFCM_EINVAL", -2: "PIFCM_EALIGN", -3: "PIFCM_ENOM
           -4: "PIFCM_ECUDA", -5: "PIFCM_ENCCL", -6: "PIFCM_ENUMERIC", -7: "PIFCM_ESTATE"}
 Q_LITERAL, Q_SQEUCLID = 0, 1
 FIT_CHAINED = 0
+FIT_ANCHORED = 1
+FIT_LEADER = 2
 U8 = 0
 
 
@@ -71,7 +73,7 @@ SIGNATURES = {
     "pifcm_pso_init": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_eval": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_fitness_ptr": (ct.c_int, [_G, _C, _P, _vp, ct.POINTER(_vp)]),
-    "pifcm_pso_update": (ct.c_int, [_vp, _G, _C, _P, _vp, ct.c_size_t, _vp]),
+    "pifcm_pso_update": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_step": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_result_get": (ct.c_int, [_vp, _G, _C, _P, _vp, ct.POINTER(PsoResult),
                                         ct.POINTER(ct.c_int32), _vp]),
@@ -86,17 +88,17 @@ SIGNATURES = {
     "pifcm_segment_host": (ct.c_int, [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int32, _C, _P, _vp,
                                       ct.c_size_t, _vp, ct.POINTER(Report), _vp]),
     "pifcm_minmax_u8": (ct.c_int, [_vp, _vp, ct.c_int64, _vp, _vp]),
-    "pifcm_normalize_u8_range": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pifcm_normalize_u8_range": (ct.c_int, [_vp, _G, _vp, _vp, _vp, _vp]),
     "pifcm_hist_u8": (ct.c_int, [_vp, _vp, ct.c_int64, _vp, _vp, _vp]),
-    "pifcm_slab_workspace_size": (ct.c_int, [_vp, _vp, _vp, _vp]),
-    "pifcm_slab_pso_init": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, ct.c_size_t, _vp]),
-    "pifcm_slab_pso_halo": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, ct.c_size_t, ct.c_int32, _vp, _vp]),
-    "pifcm_slab_pso_eval": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, ct.c_size_t, _vp, _vp]),
-    "pifcm_slab_pso_finalize": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, ct.c_size_t, ct.c_int32, ct.c_int32, _vp, _vp,
+    "pifcm_slab_workspace_size": (ct.c_int, [_G, _C, _P, _vp]),
+    "pifcm_slab_pso_init": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, ct.c_size_t, _vp]),
+    "pifcm_slab_pso_halo": (ct.c_int, [_vp, _G, _C, _P, _vp, ct.c_size_t, ct.c_int32, _vp, _vp]),
+    "pifcm_slab_pso_eval": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp, _vp]),
+    "pifcm_slab_pso_finalize": (ct.c_int, [_vp, _G, _C, _P, _vp, ct.c_size_t, ct.c_int32, ct.c_int32, _vp, _vp,
                                            _vp]),
-    "pifcm_slab_pso_update": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, ct.c_size_t, _vp]),
-    "pifcm_slab_pso_result_get": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "pifcm_slab_pso_gbest_state": (ct.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "pifcm_slab_pso_update": (ct.c_int, [_vp, _G, _C, _P, _vp, ct.c_size_t, _vp]),
+    "pifcm_slab_pso_result_get": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, _vp]),
+    "pifcm_slab_pso_gbest_state": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, _vp]),
     "pifcm_slab_chunk": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32, _vp]),
     "pifcm_slab_records": (ct.c_int, [_G, ct.POINTER(ct.c_int32)]),
     "pifcm_slab_step": (ct.c_int, [_vp, _G, _C, _vp, _vp, _vp, _vp, _vp, ct.c_int32, _vp, _vp, _vp]),

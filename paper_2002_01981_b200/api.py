@@ -52,10 +52,11 @@ class PsoConfig:
     seed: int = 12345
     p_begin: int = 0
     p_end: int = 0
+    fitness: int = 0  # 0 CHAINED (R11), 1 ANCHORED, 2 LEADER (R22)
 
     def c(self) -> _abi.PsoCfg:
         return _abi.PsoCfg(self.P, self.ring_k, self.max_gen, self.patience, self.tol, self.v0,
-                           self.vmax, self.seed, _abi.FIT_CHAINED, self.p_begin, self.p_end)
+                           self.vmax, self.seed, self.fitness, self.p_begin, self.p_end)
 
 
 def pitch_of(nx: int) -> int:
@@ -204,9 +205,10 @@ class Context:
         self._ck(self.lib.pifcm_pso_eval(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
                                          _ptr(x), _ptr(ws), ws.numel(), _stream(stream)))
 
-    def pso_update(self, grid, cfg, pso, ws, stream=None):
+    def pso_update(self, grid, cfg, pso, ws, x=None, stream=None):
+        """x: required for the ANCHORED / LEADER fitness modes."""
         self._ck(self.lib.pifcm_pso_update(self._h, ct.byref(grid), ct.byref(cfg.c()),
-                                           ct.byref(pso.c()), _ptr(ws), ws.numel(), _stream(stream)))
+                                           ct.byref(pso.c()), _ptr(x), _ptr(ws), ws.numel(), _stream(stream)))
 
     def pso_step(self, grid, cfg, pso, x, ws, stream=None):
         self._ck(self.lib.pifcm_pso_step(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),

@@ -255,33 +255,54 @@ __global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs 
             if (s.pbf[p] < s.pbf[g]) g = p;
         const double gf_old = s.dhdr[kDGbestJ];
         const int improved = (s.pbf[g] < gf_old) ? 1 : 0;
-        for (int q = 0; q < a.Pl; ++q) s.cur[q] = s.nxt[q];
-        if (improved) {
-            s.hdr[kHGbest] = g;
-            s.dhdr[kDGbestJ] = s.pbf[g];
-            s.dhdr[kDGbestL] = s.pos[2 * g];
-            s.dhdr[kDGbestX] = s.pos[2 * g + 1];
-            const int gl = g - a.p0;
-            if (gl >= 0 && gl < a.Pl) {
-                s.hdr[kHGbestSlot] = s.cur[gl];
-                for (int j = 0; j < kMaxC; ++j) s.gbest_c[j] = s.centers[4 * gl + j];
-            } else {
-                s.hdr[kHGbestSlot] = -1;
+        s.hdr[kHGbest] = g;
+        if (a.mode == PIFCM_FIT_CHAINED) {
+            for (int q = 0; q < a.Pl; ++q) s.cur[q] = s.nxt[q];
+            if (improved) {
+                s.dhdr[kDGbestJ] = s.pbf[g];
+                s.dhdr[kDGbestL] = s.pos[2 * g];
+                s.dhdr[kDGbestX] = s.pos[2 * g + 1];
+                const int gl = g - a.p0;
+                if (gl >= 0 && gl < a.Pl) {
+                    s.hdr[kHGbestSlot] = s.cur[gl];
+                    for (int j = 0; j < kMaxC; ++j) s.gbest_c[j] = s.centers[4 * gl + j];
+                } else {
+                    s.hdr[kHGbestSlot] = -1;
+                }
+            }
+            // free-slot assignment for the next evaluation
+            unsigned int used[(2 * 1024 + 1 + 31) / 32];
+            const int nw = (a.nslots + 31) / 32;
+            for (int w = 0; w < nw; ++w) used[w] = 0u;
+            for (int q = 0; q < a.Pl; ++q) used[s.cur[q] >> 5] |= 1u << (s.cur[q] & 31);
+            const int gs = s.hdr[kHGbestSlot];
+            if (gs >= 0) used[gs >> 5] |= 1u << (gs & 31);
+            int next_free = 0;
+            for (int q = 0; q < a.Pl; ++q) {
+                while (used[next_free >> 5] & (1u << (next_free & 31))) ++next_free;
+                s.nxt[q] = next_free++;
+            }
+        } else {
+            // ANCHORED: slot 0 = the shared start, slot 1 = the gbest snapshot
+            // (written by the guarded snapshot step after this kernel).
+            // LEADER: three slots: the shared state cur[0], the slot nxt[0] the
+            // advance writes, and the pinned gbest snapshot.
+            if (improved) {
+                s.dhdr[kDGbestJ] = s.pbf[g];
+                s.dhdr[kDGbestL] = s.pos[2 * g];
+                s.dhdr[kDGbestX] = s.pos[2 * g + 1];
+            }
+            if (a.mode == PIFCM_FIT_LEADER) {
+                int nf = 0;
+                while (nf == s.cur[0] || nf == s.hdr[kHGbestSlot]) ++nf;
+                s.nxt[0] = nf;
+                if (improved) s.hdr[kHGbestSlot] = nf;
+            } else if (improved) {
+                s.hdr[kHGbestSlot] = 1;
             }
         }
         s.hdr[kHImproved] = improved;
-        // free-slot assignment for the next evaluation
-        unsigned int used[(2 * 1024 + 1 + 31) / 32];
-        const int nw = (a.nslots + 31) / 32;
-        for (int w = 0; w < nw; ++w) used[w] = 0u;
-        for (int q = 0; q < a.Pl; ++q) used[s.cur[q] >> 5] |= 1u << (s.cur[q] & 31);
-        const int gs = s.hdr[kHGbestSlot];
-        if (gs >= 0) used[gs >> 5] |= 1u << (gs & 31);
-        int next_free = 0;
-        for (int q = 0; q < a.Pl; ++q) {
-            while (used[next_free >> 5] & (1u << (next_free & 31))) ++next_free;
-            s.nxt[q] = next_free++;
-        }
+        s.hdr[kHNotImproved] = improved ? 0 : 1;
         // step 9 stop rule on the relative decrease of the gbest fitness
         const double gf = s.pbf[g];
         if (t > 0 && a.patience > 0) {

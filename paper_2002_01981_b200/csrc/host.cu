@@ -90,7 +90,10 @@ int check_pso(pifcm_ctx *ctx, const pifcm_pso_cfg *p) {
     if (p->ring_k < 0) return fail(ctx, PIFCM_EINVAL, "ring_k must be >= 0");
     if (p->max_gen < 1) return fail(ctx, PIFCM_EINVAL, "max_gen must be >= 1");
     if (!(p->vmax > 0.0) || !(p->v0 >= 0.0)) return fail(ctx, PIFCM_EINVAL, "vmax > 0, v0 >= 0 required");
-    if (p->fitness_mode != PIFCM_FIT_CHAINED) return fail(ctx, PIFCM_EINVAL, "only CHAINED fitness");
+    if (p->fitness_mode < PIFCM_FIT_CHAINED || p->fitness_mode > PIFCM_FIT_LEADER)
+        return fail(ctx, PIFCM_EINVAL, "fitness_mode %d unknown", p->fitness_mode);
+    if (p->fitness_mode != PIFCM_FIT_CHAINED && p->P > 128)
+        return fail(ctx, PIFCM_EINVAL, "ANCHORED / LEADER fitness supports P <= 128");
     const bool all = (p->p_begin == 0 && p->p_end == 0);
     if (!all && (p->p_begin < 0 || p->p_end > p->P || p->p_begin >= p->p_end))
         return fail(ctx, PIFCM_EINVAL, "particle range [%d, %d) invalid for P = %d", p->p_begin, p->p_end, p->P);
@@ -105,8 +108,8 @@ void prange(const pifcm_pso_cfg *p, int *p0, int *pl) {
 // Workspace layout (all offsets 256-byte aligned).
 struct Layout {
     size_t x, vol, lab, hist, mm, c0, slots, hdr, dhdr, pos, vel, pbf, pbx, fit, evalpos, cur, nxt,
-        gbc, cent, part, stats, lamxi, cnt, total;
-    int nslots, P, Pl, p0, nblk;
+        gbc, cent, part, stats, lamxi, cnt, hf, shc, total;
+    int nslots, P, Pl, p0, nblk, mode;
     long long nvox;
 };
 
@@ -117,7 +120,11 @@ Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg 
     int P = 1, p0 = 0, Pl = 1;
     if (pso) { P = pso->P; prange(pso, &p0, &Pl); }
     L.P = P; L.Pl = Pl; L.p0 = p0;
-    L.nslots = 2 * Pl + 1;
+    L.mode = pso ? pso->fitness_mode : PIFCM_FIT_CHAINED;
+    // CHAINED: every particle's state, the slot its next evaluation writes and
+    // the pinned gbest; ANCHORED: the shared start + the gbest snapshot;
+    // LEADER: the shared state, its successor and the pinned gbest
+    L.nslots = L.mode == PIFCM_FIT_CHAINED ? 2 * Pl + 1 : (L.mode == PIFCM_FIT_LEADER ? 3 : 2);
     L.nblk = step_nblk_max(g->nx, g->ny, g->nz);
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
@@ -140,10 +147,16 @@ Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg 
     L.nxt = take(sizeof(int) * Pl);
     L.gbc = take(sizeof(float) * 4);
     L.cent = take(sizeof(float) * 4 * (Pl > 2 ? Pl : 2));
-    L.part = take(sizeof(double) * kNR * (size_t)L.nblk * (Pl > 1 ? Pl : 1));
+    {
+        size_t np = (size_t)kNR * L.nblk * (Pl > 1 ? Pl : 1);
+        const size_t ne = (size_t)eval_shared_parts(L.nvox, Pl) * Pl;
+        L.part = take(sizeof(double) * (np > ne ? np : ne));
+    }
     L.stats = take(sizeof(double) * 4 * (Pl > 1 ? Pl : 1));
     L.lamxi = take(sizeof(double) * 2 * (Pl > 1 ? Pl : 1));
     L.cnt = take(sizeof(unsigned) * (Pl > 1 ? Pl : 1));
+    L.hf = L.mode == PIFCM_FIT_CHAINED ? take(0) : take(sizeof(float4) * 2 * (size_t)L.nvox);
+    L.shc = take(sizeof(float) * 4);
     L.total = o;
     return L;
 }
@@ -411,6 +424,8 @@ int pifcm_pso_init(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
     const uint32_t k0 = (uint32_t)(pso->seed & 0xFFFFFFFFu), k1 = (uint32_t)(pso->seed >> 32);
     CK(ctx, cudaMemsetAsync(at<unsigned>(ws, L.cnt), 0, sizeof(unsigned) * (L.Pl > 1 ? L.Pl : 1), st));
     LAUNCH(ctx, 1, launch_pso_init(swarm_of(ws, L), L.P, L.Pl, L.p0, pso->v0, k0, k1, c0, L.nslots, st));
+    if (L.mode != PIFCM_FIT_CHAINED)  // the shared state's centres
+        CK(ctx, cudaMemcpyAsync(at<float>(ws, L.shc), c0, sizeof(float) * 4, cudaMemcpyDeviceToDevice, st));
     return PIFCM_OK;
 }
 
@@ -432,22 +447,73 @@ int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     SwarmDev s = swarm_of(ws, L);
     float4 *slots = at<float4>(ws, L.slots);
-    return run_step(ctx, grid, cfg, x, slots, slots, s.cur, s.nxt, s.centers, s.pos + 2 * L.p0, true, 0,
-                    L.Pl, at<double>(ws, L.part), s.fit + L.p0, nullptr, 0.f, s.hdr + kHStatus,
-                    s.hdr + kHStop, st, L.nslots, at<unsigned>(ws, L.cnt));
+    if (L.mode == PIFCM_FIT_CHAINED)
+        return run_step(ctx, grid, cfg, x, slots, slots, s.cur, s.nxt, s.centers, s.pos + 2 * L.p0, true, 0,
+                        L.Pl, at<double>(ws, L.part), s.fit + L.p0, nullptr, 0.f, s.hdr + kHStatus,
+                        s.hdr + kHStop, st, L.nslots, at<unsigned>(ws, L.cnt));
+    // ANCHORED / LEADER: H, F of the shared state (ANCHORED: once per run, the
+    // pass is skipped once hdr[kHHfValid] is set), then all particles' J
+    float4 *hf = at<float4>(ws, L.hf);
+    {
+        StepArgs a{};
+        a.x = x;
+        a.nx = grid->nx; a.ny = grid->ny; a.nz = grid->nz; a.pitch = grid->pitch;
+        a.nvox = L.nvox;
+        a.U_in = slots; a.U_out = slots;
+        a.in_idx = L.mode == PIFCM_FIT_LEADER ? s.cur : nullptr;  // ANCHORED: slot 0
+        a.centers = at<float>(ws, L.shc);
+        a.lam_xi = at<double>(ws, L.lamxi);
+        a.stop = L.mode == PIFCM_FIT_ANCHORED ? s.hdr + kHHfValid : s.hdr + kHStop;
+        a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f); a.q_mode = cfg->q_mode;
+        a.n_in_states = L.nslots;
+        a.C = cfg->C;
+        a.hf = hf;
+        LAUNCH(ctx, 1, launch_step(a, cfg->C, true, 1, st));
+        if (L.mode == PIFCM_FIT_ANCHORED) LAUNCH(ctx, 1, launch_set_hdr(s.hdr, kHHfValid, 1, st));
+    }
+    int nparts = 0;
+    double *parts = at<double>(ws, L.part);
+    LAUNCH(ctx, 1, launch_eval_shared(x, grid->nx, grid->ny, grid->nz, grid->pitch, hf, at<float>(ws, L.shc),
+                                      s.pos + 2 * L.p0, L.Pl, cfg->C, cfg->m, parts, &nparts, st));
+    LAUNCH(ctx, 1, launch_fit_sum(parts, nparts, L.Pl, s.fit + L.p0, s.hdr + kHStatus, st));
+    return PIFCM_OK;
 }
 
 int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
-                     void *ws, size_t ws_bytes, pifcm_stream stream) {
+                     const float *x, void *ws, size_t ws_bytes, pifcm_stream stream) {
     Layout L;
     int r = pso_common(ctx, grid, cfg, pso, ws, ws_bytes, &L);
     if (r) return r;
+    if (L.mode != PIFCM_FIT_CHAINED && !x) return fail(ctx, PIFCM_EINVAL, "ANCHORED / LEADER updates need x");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     PsoUpdateArgs a{};
     a.s = swarm_of(ws, L);
     a.P = L.P; a.Pl = L.Pl; a.p0 = L.p0; a.ring_k = pso->ring_k; a.patience = pso->patience;
-    a.nslots = L.nslots; a.tol = pso->tol; a.vmax = pso->vmax;
+    a.nslots = L.nslots; a.tol = pso->tol; a.vmax = pso->vmax; a.mode = L.mode;
     a.key0 = (uint32_t)(pso->seed & 0xFFFFFFFFu); a.key1 = (uint32_t)(pso->seed >> 32);
-    LAUNCH(ctx, 1, launch_pso_update(a, reinterpret_cast<cudaStream_t>(stream)));
+    LAUNCH(ctx, 1, launch_pso_update(a, st));
+    if (L.mode == PIFCM_FIT_CHAINED) return PIFCM_OK;
+    // ANCHORED: on an improvement, the snapshot = one step from the start at the
+    // gbest's evaluation position (slot 0 -> slot 1; skipped otherwise).
+    // LEADER: S_{t+1} = one step from S_t at the gbest's evaluation position
+    // (slot cur[0] -> nxt[0]); it becomes the shared state (and, on an
+    // improvement, the pinned snapshot).
+    SwarmDev s = a.s;
+    float4 *slots = at<float4>(ws, L.slots);
+    double *lamxi = at<double>(ws, L.lamxi);
+    const bool anch = L.mode == PIFCM_FIT_ANCHORED;
+    LAUNCH(ctx, 1, launch_mode_pre(s, at<float>(ws, L.shc), lamxi, L.mode, st));
+    if (anch) {
+        r = run_step(ctx, grid, cfg, x, slots, slots + L.nvox, nullptr, nullptr, s.gbest_c, lamxi, true, 0, 1,
+                     at<double>(ws, L.part), nullptr, nullptr, 0.f, s.hdr + kHStatus, s.hdr + kHNotImproved, st, 1,
+                     at<unsigned>(ws, L.cnt));
+    } else {
+        r = run_step(ctx, grid, cfg, x, slots, slots, s.cur, s.nxt, at<float>(ws, L.shc), lamxi, true, 0, 1,
+                     at<double>(ws, L.part), nullptr, nullptr, 0.f, s.hdr + kHStatus, s.hdr + kHStop, st,
+                     L.nslots, at<unsigned>(ws, L.cnt));
+    }
+    if (r) return r;
+    if (!anch) LAUNCH(ctx, 1, launch_leader_post(s, at<float>(ws, L.shc), st));
     return PIFCM_OK;
 }
 
@@ -455,7 +521,7 @@ int pifcm_pso_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
                    const float *x, void *ws, size_t ws_bytes, pifcm_stream stream) {
     int r = pifcm_pso_eval(ctx, grid, cfg, pso, x, ws, ws_bytes, stream);
     if (r) return r;
-    return pifcm_pso_update(ctx, grid, cfg, pso, ws, ws_bytes, stream);
+    return pifcm_pso_update(ctx, grid, cfg, pso, x, ws, ws_bytes, stream);
 }
 
 int pifcm_pso_result_get(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
@@ -855,6 +921,7 @@ static int slab_pso_common(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_i
     if ((r = check_slab(ctx, slab)) || (r = check_cfg(ctx, cfg)) || (r = check_pso(ctx, pso))) return r;
     if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
         return fail(ctx, PIFCM_EINVAL, "slab ranks hold every particle (p_begin = p_end = 0)");
+    if (pso->fitness_mode != PIFCM_FIT_CHAINED) return fail(ctx, PIFCM_EINVAL, "slab PSO: CHAINED fitness only");
     *pg = plain_of(slab);
     *L = layout(pg, cfg, pso);
     return ws ? check_ws(ctx, ws, ws_bytes, L->total) : PIFCM_OK;
@@ -956,7 +1023,7 @@ int pifcm_slab_pso_update(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_if
     pifcm_grid pg;
     int r = slab_pso_common(ctx, slab, cfg, pso, ws, ws_bytes, &L, &pg);
     if (r) return r;
-    return pifcm_pso_update(ctx, &pg, cfg, pso, ws, ws_bytes, stream);
+    return pifcm_pso_update(ctx, &pg, cfg, pso, nullptr, ws, ws_bytes, stream);
 }
 
 int pifcm_slab_pso_result_get(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,

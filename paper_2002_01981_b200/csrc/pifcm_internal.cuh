@@ -82,6 +82,7 @@ struct StepArgs {
     double *stats_out;   // nullable [P][4] {J, du, iters, converged} (same array as stats)
     float eps;
     int *status;         // nullable: PIFCM_ENUMERIC on a non-finite J
+    float4 *hf;          // non-null: emit H (float4) and F (float4) per voxel [nvox][2] instead of a step
 };
 
 // Swarm state in the workspace (all device pointers).
@@ -101,13 +102,14 @@ struct SwarmDev {
 };
 // header int indices
 constexpr int kHGen = 0, kHGbest = 1, kHGbestSlot = 2, kHImproved = 3, kHCalm = 4,
-              kHStop = 5, kHStatus = 6, kHInit = 7;
+              kHStop = 5, kHStatus = 6, kHInit = 7, kHNotImproved = 8, kHHfValid = 9;
 // header double indices
 constexpr int kDPrevGf = 0, kDGbestJ = 1, kDGbestL = 2, kDGbestX = 3;
 
 struct PsoUpdateArgs {
     SwarmDev s;
     int P, Pl, p0, ring_k, patience, nslots;
+    int mode;  // pifcm_fitness: CHAINED / ANCHORED / LEADER
     double tol, vmax;
     uint32_t key0, key1;
 };
@@ -135,6 +137,16 @@ cudaError_t launch_argmax(const float4 *U, long long n, int C, uint8_t *labels,
 cudaError_t launch_gather_gbest(const float4 *slots, long long nvox, const int *hdr,
                                 const float *gbest_c, float4 *U_out, float *c_out,
                                 cudaStream_t st);
+// fitness modes ANCHORED / LEADER (fitness.cu)
+cudaError_t launch_eval_shared(const float *x, int nx, int ny, int nz, int pitch, const float4 *hf,
+                               const float *centers, const double *pos, int P, int C, float m, double *partials,
+                               int *nparts, cudaStream_t st);
+int eval_shared_parts(long long nvox, int P);
+cudaError_t launch_fit_sum(const double *partials, int nparts, int P, double *fitness, int *status,
+                           cudaStream_t st);
+cudaError_t launch_mode_pre(SwarmDev s, const float *shared_c, double *lamxi, int mode, cudaStream_t st);
+cudaError_t launch_leader_post(SwarmDev s, const float *shared_c, cudaStream_t st);
+cudaError_t launch_set_hdr(int *hdr, int idx, int value, cudaStream_t st);
 cudaError_t launch_set_lamxi(double *dst, const double *dhdr, cudaStream_t st);
 cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const int *counts, const double *records,
                                  float *centers, double *stats, double *fitness, float eps, int *status,

@@ -463,7 +463,7 @@ __device__ __forceinline__ void plane_SR(const float4 *Us, int ty, int tx, float
 //   newest plane (plane_SR), carried across the z march.
 //   Planes arrive by TMA into a 4-stage ring (full barriers); each warp
 //   releases a stage on its empty barrier, so warps are not lock-stepped.
-template <int C, bool M2, bool DU>
+template <int C, bool M2, bool DU, bool HF>
 __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     k_step_stencil(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
                    const StepArgs a) {
@@ -692,6 +692,21 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
             if (C > 3) G += hn[r][NP - 1].y;  // = sum_k g_ik (rows of U sum to 1)
             const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
             float2 A[2], Ar[2];
+            if (HF) {  // particle-invariant H, F of this state (ANCHORED / LEADER fitness)
+                float2 Hh[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                float2 Ff[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                for (int q = 0; q < NP; ++q) {
+                    Hh[q] = __fmul2_rn(hn[r][q], make_float2(invG, invG));        // Eq. 5
+                    Ff[q] = __fmul2_rn(Fn[r][q], make_float2(invQ[r], invQ[r]));  // Eq. 7
+                }
+                if ((vmask >> r) & 1u) {
+                    float4 *o = a.hf + 2 * ((long long)z * plane + (long long)(y0 + ty * kRY + r) * a.nx + gx);
+                    o[0] = make_float4(Hh[0].x, Hh[0].y, Hh[1].x, Hh[1].y);
+                    o[1] = make_float4(Ff[0].x, Ff[0].y, Ff[1].x, Ff[1].y);
+                }
+                continue;
+            }
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
                 const float2 H = __fmul2_rn(hn[r][q], make_float2(invG, invG));          // Eq. 5
@@ -757,6 +772,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     }
 #undef PIFCM_ISSUE_PLANE
 
+    if (HF) return;  // no reductions: H, F only
     float num[kMaxC] = {num2[0].x, num2[0].y, num2[1].x, num2[1].y};
     float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
     const int blk = blockIdx.x + gridDim.x * blockIdx.y;
@@ -910,24 +926,25 @@ static bool make_maps(const StepArgs &a, CUtensorMap *mU, CUtensorMap *mX) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int C, bool M2, bool DU>
+template <int C, bool M2, bool DU, bool HF = false>
 static cudaError_t launch_stencil(const StepArgs &a, int P, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_step_stencil<C, M2, DU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_step_stencil<C, M2, DU, HF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kStencilSmem);
         attr = true;
     }
     CUtensorMap mU, mX;
     if (!make_maps(a, &mU, &mX)) return cudaErrorInvalidValue;
     dim3 grid(a.tiles_x * a.tiles_y, a.zchunks, P);
-    k_step_stencil<C, M2, DU><<<grid, kStepThreads, kStencilSmem, st>>>(mU, mX, a);
+    k_step_stencil<C, M2, DU, HF><<<grid, kStepThreads, kStencilSmem, st>>>(mU, mX, a);
     return cudaGetLastError();
 }
 
 template <int C, bool M2>
 static cudaError_t launch_t(const StepArgs &a, bool stencil, int P, cudaStream_t st) {
     if (stencil) {
+        if (a.hf) return M2 ? launch_stencil<C, true, false, true>(a, P, st) : cudaErrorInvalidValue;
         return a.want_du ? launch_stencil<C, M2, true>(a, P, st) : launch_stencil<C, M2, false>(a, P, st);
     }
     dim3 grid(a.nblk, P);
@@ -961,7 +978,7 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
         a.zchunks = (a.nz_t + a.tz - 1) / a.tz;
         a.nblk = a.tiles_x * a.tiles_y * a.zchunks;
     }
-    const bool m2 = (a.m == 2.0f);
+    const bool m2 = (a.m == 2.0f) || a.hf != nullptr;  // the H, F pass does not depend on m
     switch (C) {
         case 2: return m2 ? launch_t<2, true>(a, stencil, P, st) : launch_t<2, false>(a, stencil, P, st);
         case 3: return m2 ? launch_t<3, true>(a, stencil, P, st) : launch_t<3, false>(a, stencil, P, st);

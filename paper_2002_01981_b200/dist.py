@@ -139,7 +139,7 @@ class GpuPsoEngine:
         self.fit.copy_(full)
 
     def update(self):
-        self.ctx.pso_update(self.grid, self.cfg, self.pso, self.ws)
+        self.ctx.pso_update(self.grid, self.cfg, self.pso, self.ws, x=self.x)
 
     def summary(self):
         s, stopped = self.ctx.pso_result(self.grid, self.cfg, self.pso, self.ws)
