@@ -77,15 +77,44 @@ __global__ void __launch_bounds__(kEvThreads) k_eval_shared(const float *__restr
                 const float xv = sx[v];
                 const float4 H = sH[v], F = sF[v];
                 const float hh[4] = {H.x, H.y, H.z, H.w}, ff[4] = {F.x, F.y, F.z, F.w};
-                float S = 0.f;
+                float d2[4];
 #pragma unroll
                 for (int j = 0; j < C; ++j) {
                     const float aj = fmaxf(fmaf(-lam[g], hh[j], fmaf(-xi[g], ff[j], 1.0f)), kAFloor);  // Eq. 4
                     const float dx = xv - c[j];
-                    const float d2 = dx * dx * aj;
-                    S += M2 ? rcp_fast(d2) : exp2f(-log2f(d2) * inv_m1);  // d2 = 0 -> +inf
+                    d2[j] = dx * dx * aj;
                 }
-                part += M2 ? rcp_fast(S) : exp2f((1.0f - m) * log2f(S));  // J_i (S = inf -> 0, R5)
+                float Ji;
+                if (M2) {
+                    // J_i = 1 / sum_j 1/d2_j as one quotient of products (one MUFU
+                    // instead of C + 1): prod_j d2_j / sum_j prod_{k != j} d2_k
+                    float num, den;
+                    if (C == 2) {
+                        num = d2[0] * d2[1];
+                        den = d2[0] + d2[1];
+                    } else if (C == 3) {
+                        const float p01 = d2[0] * d2[1];
+                        num = p01 * d2[2];
+                        den = fmaf(d2[0] + d2[1], d2[2], p01);
+                    } else {
+                        const float p01 = d2[0] * d2[1], p23 = d2[2] * d2[3];
+                        num = p01 * p23;
+                        den = fmaf(p01, d2[2] + d2[3], p23 * (d2[0] + d2[1]));
+                    }
+                    Ji = num * rcp_fast(den);
+                    if (!(num >= 1e-30f) || !(den < 1e30f)) {  // tiny / zero distances (R5): the sum form
+                        float S = 0.f;
+#pragma unroll
+                        for (int j = 0; j < C; ++j) S += rcp_fast(d2[j]);  // d2 = 0 -> +inf
+                        Ji = rcp_fast(S);                                  // S = inf -> 0
+                    }
+                } else {
+                    float S = 0.f;
+#pragma unroll
+                    for (int j = 0; j < C; ++j) S += exp2f(-log2f(d2[j]) * inv_m1);
+                    Ji = exp2f((1.0f - m) * log2f(S));  // J_i = S^{1-m}
+                }
+                part += Ji;
             }
             acc[g] += (double)part;
         }
