@@ -6,6 +6,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <cmath>
+
 #include <chrono>
 #include <string>
 #include <vector>
@@ -76,7 +78,7 @@ int check_cfg(pifcm_ctx *ctx, const pifcm_ifcm_cfg *c) {
     if (!c) return fail(ctx, PIFCM_EINVAL, "cfg is NULL");
     if (c->C < 2 || c->C > kMaxC) return fail(ctx, PIFCM_EINVAL, "C = %d outside [2, 4]", c->C);
     if (!(c->m > 1.0f) || !(c->m < 1e6f)) return fail(ctx, PIFCM_EINVAL, "m = %g must be > 1", (double)c->m);
-    if (c->v != 1) return fail(ctx, PIFCM_EINVAL, "v = %d: only v = 1 (26-neighbourhood) on the device path", c->v);
+    if (c->v != 1 && c->v != 2) return fail(ctx, PIFCM_EINVAL, "v = %d: the device path has v = 1 and v = 2", c->v);
     if (!(c->h > 0.0f)) return fail(ctx, PIFCM_EINVAL, "h must be > 0");
     if (c->q_mode != PIFCM_Q_LITERAL && c->q_mode != PIFCM_Q_SQEUCLID)
         return fail(ctx, PIFCM_EINVAL, "q_mode %d unknown", c->q_mode);
@@ -97,6 +99,13 @@ int check_pso(pifcm_ctx *ctx, const pifcm_pso_cfg *p) {
     const bool all = (p->p_begin == 0 && p->p_end == 0);
     if (!all && (p->p_begin < 0 || p->p_end > p->P || p->p_begin >= p->p_end))
         return fail(ctx, PIFCM_EINVAL, "particle range [%d, %d) invalid for P = %d", p->p_begin, p->p_end, p->P);
+    return PIFCM_OK;
+}
+
+// mode / shell combinations the device path implements
+int check_pso_cfg(pifcm_ctx *ctx, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg *p) {
+    if (p->fitness_mode != PIFCM_FIT_CHAINED && c->v != 1)
+        return fail(ctx, PIFCM_EINVAL, "ANCHORED / LEADER fitness with v = %d is not implemented", c->v);
     return PIFCM_OK;
 }
 
@@ -189,6 +198,17 @@ int check_ws(pifcm_ctx *ctx, void *ws, size_t ws_bytes, size_t need) {
     return PIFCM_OK;
 }
 
+// Eq. 10 shell weights W_r = e^{-r/h} / sum_{s=1..v} e^{-s/h}.
+void set_shells(StepArgs &a, const pifcm_ifcm_cfg *cfg) {
+    a.v = cfg->v;
+    double s = 0.0;
+    for (int r = 1; r <= cfg->v; ++r) s += exp(-(double)r / (double)cfg->h);
+    a.w1d = exp(-1.0 / (double)cfg->h) / s;
+    a.w2d = cfg->v >= 2 ? exp(-2.0 / (double)cfg->h) / s : 0.0;
+    a.w1 = (float)a.w1d;
+    a.w2 = (float)a.w2d;
+}
+
 // A step launch, bracketed by CUDA events on its stream when timing is on
 // (stencil launches only; vox = the voxels the launch updates per state).
 int timed_step(pifcm_ctx *ctx, const StepArgs &a, int C, bool stencil, int P, long long vox, cudaStream_t st) {
@@ -229,6 +249,7 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     a.stats = stats; a.stop = stop;
     a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f);
     a.q_mode = cfg->q_mode; a.first = first;
+    set_shells(a, cfg);
     a.n_in_states = n_in_states;
     a.want_du = (stats != nullptr) ? 1 : 0;
     a.counters = counters;
@@ -330,7 +351,7 @@ int pifcm_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, cons
     if (!bytes) return PIFCM_EINVAL;
     int r;
     if ((r = check_grid(nullptr, grid)) || (r = check_cfg(nullptr, cfg))) return r;
-    if (pso && (r = check_pso(nullptr, pso))) return r;
+    if (pso && ((r = check_pso(nullptr, pso)) || (r = check_pso_cfg(nullptr, cfg, pso)))) return r;
     *bytes = layout(grid, cfg, pso).total;
     return PIFCM_OK;
 }
@@ -405,7 +426,9 @@ static int pso_common(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg 
                       void *ws, size_t ws_bytes, Layout *L) {
     if (!ctx) return PIFCM_EINVAL;
     int r;
-    if ((r = check_grid(ctx, g)) || (r = check_cfg(ctx, c)) || (r = check_pso(ctx, p))) return r;
+    if ((r = check_grid(ctx, g)) || (r = check_cfg(ctx, c)) || (r = check_pso(ctx, p)) ||
+        (r = check_pso_cfg(ctx, c, p)))
+        return r;
     *L = layout(g, c, p);
     return check_ws(ctx, ws, ws_bytes, L->total);
 }
@@ -824,6 +847,7 @@ int pifcm_slab_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg
     if (!ctx) return PIFCM_EINVAL;
     int r;
     if ((r = check_slab(ctx, grid)) || (r = check_cfg(ctx, cfg))) return r;
+    if (cfg->v != 1) return fail(ctx, PIFCM_EINVAL, "z-slab ranks carry one halo plane: v = 1 only");
     if (P < 1 || P > 65535) return fail(ctx, PIFCM_EINVAL, "P = %d outside [1, 65535]", P);
     if (!x || !U_in || !U_out || !centers || !lam_xi || !records)
         return fail(ctx, PIFCM_EINVAL, "x, U_in, U_out, centers, lam_xi and records must be non-NULL");
@@ -919,6 +943,7 @@ static int slab_pso_common(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_i
                            const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, Layout *L, pifcm_grid *pg) {
     int r;
     if ((r = check_slab(ctx, slab)) || (r = check_cfg(ctx, cfg)) || (r = check_pso(ctx, pso))) return r;
+    if (cfg->v != 1) return fail(ctx, PIFCM_EINVAL, "z-slab ranks carry one halo plane: v = 1 only");
     if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
         return fail(ctx, PIFCM_EINVAL, "slab ranks hold every particle (p_begin = p_end = 0)");
     if (pso->fitness_mode != PIFCM_FIT_CHAINED) return fail(ctx, PIFCM_EINVAL, "slab PSO: CHAINED fitness only");

@@ -83,6 +83,9 @@ struct StepArgs {
     float eps;
     int *status;         // nullable: PIFCM_ENUMERIC on a non-finite J
     float4 *hf;          // non-null: emit H (float4) and F (float4) per voxel [nvox][2] instead of a step
+    int v;               // neighbourhood shells (Eq. 9-10): 1 = the 26-neighbourhood, 2 = two shells
+    float w1, w2;        // Eq. 10 shell weights W_1, W_2 (v = 2)
+    double w1d, w2d;     // the same in fp64 (ill-conditioned re-evaluation)
 };
 
 // Swarm state in the workspace (all device pointers).
@@ -117,6 +120,7 @@ struct PsoUpdateArgs {
 // ---------------------------------------------------------------- launchers
 // All return cudaGetLastError() of the launch.
 cudaError_t launch_step(const StepArgs &a, int C, bool stencil, int P, cudaStream_t st);
+cudaError_t launch_step_v2(const StepArgs &a, int C, int P, cudaStream_t st);  // step_v2.cu
 int step_nblk(int nx, int ny, int nz, bool stencil, int P);
 int slab_tz(int nx, int ny, int nz_total);
 int step_nblk_max(int nx, int ny, int nz);

@@ -93,3 +93,58 @@ def qsum_bruteforce(nx, ny, nz, X, Y, Z, q_mode=0):
 
 def isclose(a, b, tol):
     return math.isclose(a, b, rel_tol=0.0, abs_tol=tol)
+
+
+def ifcm_step_bruteforce_shells(x, U, c, lam, xi, v, h, m=2.0, q_mode=0):
+    """One IFCM step with v Chebyshev shells (reading R2 of Eq. 9 for v >= 2)
+    weighted by Eq. 10 (PAPER:85): W_r = e^{-r/h} / sum_{s=1..v} e^{-s/h};
+    every shell is normalised on its own (its own G and Qs), a shell whose
+    g's are all zero contributes 0 (R3).  Pairwise over all voxel pairs."""
+    nz, ny, nx = len(x), len(x[0]), len(x[0][0])
+    coords = [(X, Y, Z) for Z in range(nz) for Y in range(ny) for X in range(nx)]
+    xs = [float(x[Z][Y][X]) for (X, Y, Z) in coords]
+    N, C = len(coords), len(c)
+    den_w = sum(math.exp(-s / h) for s in range(1, v + 1))
+    W = [math.exp(-r / h) / den_w for r in range(1, v + 1)]
+    U_new = [[0.0] * C for _ in range(N)]
+    num, den = [0.0] * C, [0.0] * C
+    J, maxdu = 0.0, 0.0
+    for i in range(N):
+        Xi, Yi, Zi = coords[i]
+        G = [0.0] * v
+        Q = [0.0] * v
+        Hn = [[0.0] * C for _ in range(v)]
+        Fn = [[0.0] * C for _ in range(v)]
+        for k in range(N):
+            Xk, Yk, Zk = coords[k]
+            r = max(abs(Xi - Xk), abs(Yi - Yk), abs(Zi - Zk))
+            if r == 0 or r > v:
+                continue
+            q = (Xi - Xk) ** 2 + (Yi - Yk) ** 2 + (Zi - Zk) ** 2
+            q2 = q * q if q_mode == 0 else q
+            g = abs(xs[i] - xs[k])
+            G[r - 1] += g
+            Q[r - 1] += q2
+            for j in range(C):
+                Hn[r - 1][j] += float(U[k][j]) * g
+                Fn[r - 1][j] += float(U[k][j]) ** 2 * q2
+        d2 = []
+        for j in range(C):
+            H = sum(W[s] * Hn[s][j] / G[s] for s in range(v) if G[s] > 0)
+            F = sum(W[s] * Fn[s][j] / Q[s] for s in range(v) if Q[s] > 0)
+            a = max(1.0 - lam * H - xi * F, 1e-9)
+            d2.append((xs[i] - float(c[j])) ** 2 * a)
+        zero = [j for j in range(C) if d2[j] == 0.0]
+        for j in range(C):
+            if zero:
+                u = 1.0 if j == zero[0] else 0.0
+            else:
+                u = 1.0 / sum((d2[j] / d2[k]) ** (1.0 / (m - 1.0)) for k in range(C))
+            U_new[i][j] = u
+            um = u ** m
+            num[j] += um * xs[i]
+            den[j] += um
+            J += um * d2[j]
+            maxdu = max(maxdu, abs(u - float(U[i][j])))
+    c_new = [num[j] / den[j] if den[j] >= 1e-12 else float(c[j]) for j in range(C)]
+    return U_new, c_new, J, maxdu

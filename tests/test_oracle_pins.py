@@ -229,6 +229,31 @@ def test_oracle_equals_bruteforce(orc, shape, C, m, mode, seed):
     assert abs(du - dub) < 1e-12
 
 
+@pytest.mark.parametrize("shape,C,v,h,mode,seed", [((5, 6, 7), 3, 2, 1.0, 0, 3), ((6, 5, 5), 4, 2, 0.5, 1, 4),
+                                                   ((1, 9, 8), 2, 2, 2.0, 0, 5), ((7, 4, 6), 4, 3, 1.0, 0, 6)])
+def test_oracle_shells_equal_bruteforce(orc, shape, C, v, h, mode, seed):
+    """v >= 2 (R2: Chebyshev shells, Eq. 10 weights, per-shell normalisation)
+    == the pairwise reference within 1e-12."""
+    from inputs import random_state
+    nz, ny, nx = shape
+    x, U, c = random_state(nx, ny, nz, C, seed, crisp_frac=0.2)
+    Un, cn, J, du = orc.ifcm_step(x, U, c, 0.8, 0.6, q_mode=mode, v=v, h=h)
+    Ub, cb, Jb, dub = bf.ifcm_step_bruteforce_shells(x, U.astype(np.float64), c, 0.8, 0.6, v, h, q_mode=mode)
+    assert np.abs(Un - np.array(Ub)).max() < 1e-12
+    assert np.abs(cn - np.array(cb)).max() < 1e-12
+    assert abs(J - Jb) < 1e-12 * max(1.0, abs(Jb))
+
+
+def test_shells_reduce_to_single_shell(orc):
+    """v = 1 is W_1 = 1 (Eq. 10): the shell reference at v = 1 equals the
+    literal-Eq. 9 reference."""
+    from inputs import random_state
+    x, U, c = random_state(5, 4, 3, 3, 9)
+    a = bf.ifcm_step_bruteforce(x, U.astype(np.float64), c, 0.5, 0.9)
+    b = bf.ifcm_step_bruteforce_shells(x, U.astype(np.float64), c, 0.5, 0.9, 1, 1.0)
+    assert np.abs(np.array(a[0]) - np.array(b[0])).max() < 1e-14 and abs(a[2] - b[2]) < 1e-14
+
+
 # --------------------------------------------------------------------------- invariants
 def _rand_case(seed, shape=(3, 7, 6), C=3):
     from inputs import random_state
