@@ -97,17 +97,28 @@ __device__ __forceinline__ float4 attraction_coop_v2(const float4 *const (&Us)[5
         if (gx + dx < 0 || gx + dx >= nx || gy + dy < 0 || gy + dy >= ny || gz + dz < 0 || gz + dz >= nz) continue;
         const int ad = max(max(abs(dx), abs(dy)), abs(dz));
         const int s = ad - 1;
-        const float4 u = Us[dz + 2][(row + dy) * kSX2 + col + 2 + dx];
-        const double g = fabs(xr - (double)Xs[dz + 2][(row + dy) * kSXP2 + col + kXOff2 + dx]);  // Eq. 6
+        // plane pointer by selection (no dynamic indexing of the pointer arrays,
+        // which would put them in local memory for the whole kernel)
+        const float4 *Uk = dz == -2 ? Us[0] : dz == -1 ? Us[1] : dz == 0 ? Us[2] : dz == 1 ? Us[3] : Us[4];
+        const float *Xk = dz == -2 ? Xs[0] : dz == -1 ? Xs[1] : dz == 0 ? Xs[2] : dz == 1 ? Xs[3] : Xs[4];
+        const float4 u = Uk[(row + dy) * kSX2 + col + 2 + dx];
+        const double g = fabs(xr - (double)Xk[(row + dy) * kSXP2 + col + kXOff2 + dx]);  // Eq. 6
         const double q = (double)(dx * dx + dy * dy + dz * dz);
         const double q2 = lit ? q * q : q;                                                      // Eq. 8, R1
         const double uk[4] = {u.x, u.y, u.z, u.w};
-        v[s] += g;
-        v[2 + s] += q2;
+        // compile-time indices only (a runtime shell index would move v[] to local memory)
+        const double g0 = s == 0 ? g : 0.0, g1 = s == 0 ? 0.0 : g;
+        const double q0 = s == 0 ? q2 : 0.0, q1 = s == 0 ? 0.0 : q2;
+        v[0] += g0;
+        v[1] += g1;
+        v[2] += q0;
+        v[3] += q1;
 #pragma unroll
         for (int j = 0; j < C; ++j) {
-            v[4 + s * kMaxC + j] += uk[j] * g;                        // Eq. 5 numerators
-            v[4 + 2 * kMaxC + s * kMaxC + j] += uk[j] * uk[j] * q2;   // Eq. 7 numerators
+            v[4 + j] += uk[j] * g0;                                   // Eq. 5 numerators
+            v[4 + kMaxC + j] += uk[j] * g1;
+            v[4 + 2 * kMaxC + j] += uk[j] * uk[j] * q0;               // Eq. 7 numerators
+            v[4 + 3 * kMaxC + j] += uk[j] * uk[j] * q1;
         }
     }
 #pragma unroll

@@ -20,7 +20,7 @@ def ctx():
     return Context(0)
 
 
-def gpu_step(ctx, x, Us, cs, lamxi, C, m=2.0, q_mode=0, iters=1, eps=0.0):
+def gpu_step(ctx, x, Us, cs, lamxi, C, m=2.0, q_mode=0, iters=1, eps=0.0, v=1, h=1.0):
     """Run `iters` iterations for P states; returns (U_new [P,N,C] f64, c [P,C], stats [P,4])."""
     from paper_2002_01981_b200 import IfcmConfig, to_aos, to_pitched_x
     dev = torch.device("cuda:0")
@@ -33,7 +33,7 @@ def gpu_step(ctx, x, Us, cs, lamxi, C, m=2.0, q_mode=0, iters=1, eps=0.0):
     cen[:, :C] = torch.as_tensor(np.stack(cs), dtype=torch.float32)
     lx = torch.as_tensor(np.asarray(lamxi, np.float64).reshape(P, 2), device=dev)
     stats = torch.zeros((P, 4), dtype=torch.float64, device=dev)
-    cfg = IfcmConfig(C=C, m=m, q_mode=q_mode, eps=eps)
+    cfg = IfcmConfig(C=C, m=m, q_mode=q_mode, eps=eps, v=v, h=h)
     ctx.iterate(xt, Uin, Uout, cen, lx, cfg, iters=iters, stats=stats, nx=nx)
     torch.cuda.synchronize()
     U = Uout.cpu().numpy().astype(np.float64)
@@ -74,6 +74,63 @@ def test_step_parity(ctx, orc, shape, C, m, q_mode):
         assert abs(st[p, 0] - Jo) <= 1e-4 * abs(Jo) + 1e-9, (st[p, 0], Jo)
         assert abs(st[p, 1] - duo) < 2e-4
         assert np.abs(U[p].sum(1) - 1).max() < 1e-5
+
+
+CASES_V2 = [
+    # (nz, ny, nx), C, m, q_mode, h -- two Chebyshev shells (NEXT-2, Eq. 10)
+    ((1, 9, 9), 2, 2.0, 0, 1.0),
+    ((6, 13, 14), 3, 2.0, 0, 1.0),
+    ((11, 21, 37), 4, 2.0, 1, 0.5),     # ragged tiles in x and y, z chunk tails
+    ((20, 33, 66), 4, 2.0, 0, 2.0),     # several tiles in every direction
+    ((5, 3, 40), 4, 1.5, 0, 1.0),       # thin in y: boundary Qs everywhere
+    ((2, 2, 2), 2, 2.0, 1, 1.0),        # every voxel sees the whole volume
+]
+
+
+@pytest.mark.parametrize("shape,C,m,q_mode,h", CASES_V2)
+def test_step_parity_v2(ctx, orc, shape, C, m, q_mode, h):
+    """v = 2: every membership within 1e-4, centres 1e-4 relative, J 1e-4."""
+    nz, ny, nx = shape
+    states = [random_state(nx, ny, nz, C, seed=300 + s, crisp_frac=0.1) for s in range(3)]
+    x = states[0][0]
+    Us = [s[1] for s in states]
+    cs = [s[2] for s in states]
+    lamxi = [(0.3, 0.6), (1.0, 1.0), (0.05, 0.95)]
+    U, c, st = gpu_step(ctx, x, Us, cs, lamxi, C, m=m, q_mode=q_mode, v=2, h=h)
+    for p in range(3):
+        Uo, co, Jo, duo = orc.ifcm_step(x, Us[p], cs[p], *lamxi[p], m=m, q_mode=q_mode, v=2, h=h)
+        err = np.abs(U[p] - Uo).max()
+        assert err < U_TOL, (p, err)
+        assert np.all(np.abs(c[p] - co) <= C_TOL * np.abs(co) + 1e-7), (c[p], co)
+        assert abs(st[p, 0] - Jo) <= 1e-4 * abs(Jo) + 1e-9, (st[p, 0], Jo)
+        assert np.abs(U[p].sum(1) - 1).max() < 1e-5
+
+
+def test_v2_multi_iteration_and_pso(ctx, orc):
+    """v = 2 over 5 iterations from the same start (1e-4 per iteration is
+    compounded; checked at 5e-4) and the CHAINED PSO eval (generation 0
+    fitness within 1e-5)."""
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig, to_aos, to_pitched_x
+    from paper_2002_01981_b200.api import _grid
+    nz, ny, nx, C = 8, 20, 24, 3
+    x, U0, c0 = random_state(nx, ny, nz, C, seed=41, crisp_frac=0.1)
+    U, c, st = gpu_step(ctx, x, [U0], [c0], [(0.4, 0.5)], C, iters=5, v=2, h=1.0)
+    Uo, co = U0.astype(np.float64), c0.astype(np.float64)
+    for _ in range(5):
+        Uo, co, _, _ = orc.ifcm_step(x, Uo, co, 0.4, 0.5, v=2, h=1.0)
+    assert np.abs(U[0] - Uo).max() < 5e-4
+    dev = torch.device("cuda:0")
+    cfg = IfcmConfig(C=C, v=2, h=1.0)
+    pso = PsoConfig(P=5, max_gen=2, patience=0, seed=9)
+    ws = ctx.workspace(nx, ny, nz, cfg, pso)
+    g = _grid(nx, ny, nz)
+    c4 = torch.zeros(4, device=dev)
+    c4[:C] = torch.as_tensor(c0)
+    ctx.pso_init(g, cfg, pso, to_aos(U0, dev), c4, ws)
+    ctx.pso_eval(g, cfg, pso, to_pitched_x(x, dev), ws)
+    f = ctx.pso_fitness(g, cfg, pso, ws).cpu().numpy()
+    r = orc.pso_run(x, U0, c0, P=5, max_gen=1, seed=9, v=2, h=1.0)
+    assert np.allclose(f, r.trace_f[0], rtol=1e-5, atol=0)
 
 
 def test_fcm_pointwise_parity(ctx, orc):
