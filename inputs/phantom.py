@@ -104,15 +104,23 @@ CONFIGS = {
     "C2": dict(kind="cube", shape=(1, 854, 854), C=4, noise=7.0, seed=2, P=20, gens=30),
     "C3": dict(kind="brainweb", shape=(181, 217, 181), C=4, noise=9.0, seed=3, P=32, gens=30),
     "C5": dict(kind="cube", shape=(512, 512, 512), C=4, noise=7.0, seed=5, P=64, gens=30),
+    # C4: a batch of 16 BrainWeb-shaped volumes, seeds 100..115, noise cycling
+    # 3/5/7/9 %; volume k is config_volume("C4", k=k)
+    "C4": dict(kind="brainweb", shape=(181, 217, 181), C=4, noise=(3.0, 5.0, 7.0, 9.0), seed=100, P=32,
+               gens=30, batch=16),
 }
 
 
-def config_volume(name: str, shape=None):
-    """u8 noisy volume and truth labels for a named config (optionally reshaped)."""
+def config_volume(name: str, shape=None, k: int = 0):
+    """u8 noisy volume and truth labels for a named config (optionally
+    reshaped); k selects the volume of a batch config (C4)."""
     cfg = CONFIGS[name]
     nz, ny, nx = shape if shape is not None else cfg["shape"]
     if cfg["kind"] == "cube":
         img, lab = cube_phantom(nx, ny, nz, LEVELS_C3 if cfg["C"] == 3 else LEVELS_C4)
     else:
         img, lab = brainweb_phantom(nx, ny, nz)
-    return add_noise_u8(img, cfg["noise"], cfg["seed"]), lab
+    noise = cfg["noise"]
+    if isinstance(noise, tuple):
+        noise = noise[k % len(noise)]
+    return add_noise_u8(img, noise, cfg["seed"] + k), lab
