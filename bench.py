@@ -187,20 +187,28 @@ def run_ours(args, rank, world, local_rank):
 
     if rank == 0 or not os.path.exists(pbuild.LIB):
         pbuild.build()
-    torch.cuda.set_device(local_rank)
-    dev = torch.device(f"cuda:{local_rank}")
+    # one GPU per rank; PIFCM_BENCH_BACKEND=gloo (with ranks sharing a GPU)
+    # only exercises the multi-rank code path, its numbers are not bench values
+    backend = os.environ.get("PIFCM_BENCH_BACKEND", "nccl")
+    dev_index = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dev = torch.device(f"cuda:{dev_index}")
     dist = None
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group(backend)
         dist = tdist
-    ctx = Context(local_rank)
+    ctx = Context(dev_index)
     c5 = args.workload == "C5"
     vol = _volume("C5" if c5 else "C3")
     nz, ny, nx = vol.shape
     # C5: P = 64 as configured when the slot pool fits (>= 2 GPUs: 129 slots of
     # the slab); one GPU holds 65 slots of the whole 512^3 volume (140 GB): P = 32
     Pw = (64 if world >= 2 else 32) if c5 else P
+    Pw = _env_int("PIFCM_BENCH_P", Pw)  # test hook (a smaller swarm), reported in config
     workload = WORKLOAD_C5.format(P=Pw) if c5 else WORKLOAD
     cfg = IfcmConfig(C=C, m=2.0, q_mode=0, eps=1e-5, max_iter=100)
     pso = PsoConfig(P=Pw, ring_k=1, max_gen=GENS, patience=0, seed=12345)
@@ -254,7 +262,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- timed region: device-resident input
     ctx.timing_enable(True)
     l0 = ctx.launch_count()
-    clocks = ClockSampler(local_rank) if rank == 0 else None
+    clocks = ClockSampler(dev_index) if rank == 0 else None
     if clocks:
         clocks.start()
     barrier()
