@@ -502,17 +502,32 @@ __global__ void __launch_bounds__(kPwThreads) k_step_pointwise(const StepArgs a)
     // is checked by the host)
     const unsigned nx = (unsigned)a.nx, nvox = (unsigned)a.nvox;
     const unsigned stride = gridDim.x * blockDim.x;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nvox; i += stride) {
-        const unsigned row = i / nx;  // = z*ny + y
-        const unsigned X = i - row * nx;
-        const float xv = __ldg(a.x + (size_t)row * a.pitch + X);
-        const float4 un = membership<C, M2>(xv, c, av, a.m, a.inv_m1, num, den, Jacc);
-        if (!a.first) {
-            const float4 uo = Uin[i];
-            duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
-                                       fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
+    // kPwILP voxels per thread per round, their loads issued before any use
+    // (more bytes in flight per thread: the kernel is HBM-latency bound)
+    constexpr int kPwILP = 4;
+    for (unsigned i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < nvox; i0 += kPwILP * stride) {
+        float xv[kPwILP];
+        float4 uo[kPwILP];
+#pragma unroll
+        for (int k = 0; k < kPwILP; ++k) {
+            const unsigned i = i0 + k * stride;
+            if (i < nvox) {
+                const unsigned row = i / nx;  // = z*ny + y
+                xv[k] = __ldg(a.x + (size_t)row * a.pitch + (i - row * nx));
+                if (!a.first) uo[k] = __ldcs(Uin + i);
+            }
         }
-        __stcs(Uout + i, un);
+#pragma unroll
+        for (int k = 0; k < kPwILP; ++k) {
+            const unsigned i = i0 + k * stride;
+            if (i < nvox) {
+                const float4 un = membership<C, M2>(xv[k], c, av, a.m, a.inv_m1, num, den, Jacc);
+                if (!a.first)
+                    duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo[k].x), fabsf(un.y - uo[k].y)),
+                                               fmaxf(fabsf(un.z - uo[k].z), fabsf(un.w - uo[k].w))));
+                __stcs(Uout + i, un);
+            }
+        }
     }
     block_partials<kPwThreads / 32>(num, den, Jacc, duacc,
                                    a.partials + ((long long)p * a.nblk + blockIdx.x) * kNR);
