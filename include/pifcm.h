@@ -191,6 +191,17 @@ int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
                   const double *lam_xi, int32_t P, int32_t iters, double *stats,
                   void *ws, size_t ws_bytes, pifcm_stream stream);
 
+/* pifcm_iterate with flags: PIFCM_ITER_CANONICAL runs the neighbourhood
+ * launches in the canonical z-chunk decomposition (pifcm_slab_chunk), the one
+ * pifcm_segment's final IFCM and every z-slab split use, so the results are
+ * bit-identical to those (used by multi-rank pipelines that run the final
+ * IFCM replicated on every rank). */
+#define PIFCM_ITER_CANONICAL 1
+int pifcm_iterate_ex(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
+                     const float *x, const float *U_in, float *U_out, float *centers,
+                     const double *lam_xi, int32_t P, int32_t iters, double *stats,
+                     void *ws, size_t ws_bytes, int32_t flags, pifcm_stream stream);
+
 /* --------------------------------------------------------------------- PSO */
 /* Initialise the swarm (Alg. 1 step 3; Alg. 2 step 3)
  * in the workspace: positions ~ U[0,1]^2 and velocities ~ U[-v0,v0]^2 from

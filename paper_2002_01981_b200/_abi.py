@@ -18,6 +18,7 @@ Q_LITERAL, Q_SQEUCLID = 0, 1
 FIT_CHAINED = 0
 FIT_ANCHORED = 1
 FIT_LEADER = 2
+ITER_CANONICAL = 1  # pifcm_iterate_ex flag
 U8 = 0
 
 
@@ -70,6 +71,8 @@ SIGNATURES = {
     "pifcm_iterate_workspace_size": (ct.c_int, [_G, _C, ct.c_int32, ct.c_int32, ct.POINTER(ct.c_size_t)]),
     "pifcm_iterate": (ct.c_int, [_vp, _G, _C, _vp, _vp, _vp, _vp, _vp, ct.c_int32, ct.c_int32, _vp,
                                  _vp, ct.c_size_t, _vp]),
+    "pifcm_iterate_ex": (ct.c_int, [_vp, _G, _C, _vp, _vp, _vp, _vp, _vp, ct.c_int32, ct.c_int32, _vp,
+                                 _vp, ct.c_size_t, ct.c_int32, _vp]),
     "pifcm_pso_init": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_eval": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_fitness_ptr": (ct.c_int, [_G, _C, _P, _vp, ct.POINTER(_vp)]),

@@ -376,6 +376,16 @@ int pifcm_iterate_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *c
 int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const float *x,
                   const float *U_in, float *U_out, float *centers, const double *lam_xi, int32_t P,
                   int32_t iters, double *stats, void *ws, size_t ws_bytes, pifcm_stream stream) {
+    return pifcm_iterate_ex(ctx, grid, cfg, x, U_in, U_out, centers, lam_xi, P, iters, stats, ws, ws_bytes, 0,
+                            stream);
+}
+
+int pifcm_iterate_ex(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const float *x,
+                     const float *U_in, float *U_out, float *centers, const double *lam_xi, int32_t P,
+                     int32_t iters, double *stats, void *ws, size_t ws_bytes, int32_t flags,
+                     pifcm_stream stream) {
+    if (flags & ~PIFCM_ITER_CANONICAL) return ctx ? fail(ctx, PIFCM_EINVAL, "unknown flags %d", flags) : PIFCM_EINVAL;
+    const bool canonical = (flags & PIFCM_ITER_CANONICAL) != 0;
     if (!ctx) return PIFCM_EINVAL;
     int r;
     if ((r = check_grid(ctx, grid)) || (r = check_cfg(ctx, cfg))) return r;
@@ -412,7 +422,7 @@ int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
     for (int t = 1; t <= iters; ++t) {
         float4 *dst = (((iters - t) & 1) == 0) ? reinterpret_cast<float4 *>(U_out) : scratch;
         r = run_step(ctx, grid, cfg, x, src, dst, nullptr, nullptr, centers, lam_xi, !zero, 0, P,
-                     partials, nullptr, S, eps, status, nullptr, st, P, counters);
+                     partials, nullptr, S, eps, status, nullptr, st, P, counters, canonical && !zero);
         if (r) return r;
         src = dst;
     }

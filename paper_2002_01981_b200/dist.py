@@ -150,16 +150,20 @@ class GpuPsoEngine:
 
 
 class ShardedSegmenter:
+    SHARD_FINAL_MIN_VOXELS = 16 * 1024 * 1024
+
     """pifcm_segment with the PSO particles sharded over the ranks of `dist`.
 
     Every rank normalises, fits the GMM and runs the FCM start (identical,
     deterministic), the PSO generations are sharded, the gbest state is
-    broadcast from its owner, the final IFCM runs z-slab sharded (SlabIfcm)
-    and each rank's slab labels are all-gathered.  pifcm_segment runs its
-    final IFCM in the same canonical 16-plane decomposition, so labels are
-    bit-identical to the single-process pifcm_segment for any world size."""
+    broadcast from its owner, and the final IFCM runs either z-slab sharded
+    (SlabIfcm, each rank's slab labels all-gathered; large volumes) or whole on
+    every rank.  Both use the canonical z-chunk decomposition of
+    pifcm_segment's final IFCM, so labels are bit-identical to the
+    single-process pifcm_segment for any world size."""
 
-    def __init__(self, ctx, cfg, pso, shape, dist=None):
+    def __init__(self, ctx, cfg, pso, shape, dist=None, shard_final=None):
+        """shard_final: None = by size (SHARD_FINAL_MIN_VOXELS), True / False force."""
         self.ctx, self.cfg, self.pso = ctx, cfg, pso
         self.nz, self.ny, self.nx = shape
         self.dist = dist
@@ -171,9 +175,14 @@ class ShardedSegmenter:
         self.engine = None
         world = dist.get_world_size() if dist is not None else 1
         tz = ctx.slab_chunk(self.nx, self.ny, self.nz)
-        # fewer z-chunks than ranks: every rank runs the whole volume
-        self.slab = SlabIfcm(ctx, cfg, self.nx, self.ny, self.nz, 1,
-                             dist if -(-self.nz // tz) >= world else None)
+        # The final IFCM (one state) runs z-slab sharded only when a rank's
+        # share of an iteration outweighs the per-iteration exchange and
+        # launch overheads (~0.1 ms); otherwise every rank runs it whole, in
+        # the same canonical decomposition -- the results are bit-identical
+        # either way.
+        big = nvox >= self.SHARD_FINAL_MIN_VOXELS if shard_final is None else bool(shard_final)
+        self.shard_final = world > 1 and -(-self.nz // tz) >= world and big
+        self.slab = SlabIfcm(ctx, cfg, self.nx, self.ny, self.nz, 1, dist if self.shard_final else None)
         w = self.slab.world
         self.lab_counts = [slab_range(self.nz, w, r, tz)[1] * self.nx * self.ny for r in range(w)]
         self.lab_pad = torch.zeros((w, max(self.lab_counts)), dtype=torch.uint8, device=self.dev)
@@ -212,15 +221,23 @@ class ShardedSegmenter:
         ev[3].record()
         # Alg. 1 step 11: final IFCM at (lambda*, xi*) until eps, then argmax
         lx = torch.tensor([[out.lam, out.xi]], dtype=torch.float64, device=self.dev)
-        sl = self.slab
-        sl.load_x(x)
-        sl.load_state(self.Ua, self.cen)
-        sl.run(lx, cfg.max_iter, eps=cfg.eps)
-        self.cen.copy_(sl.centers)
-        loc = ctx.argmax(sl.local_U()[0], nx, ny, sl.nz, cfg.C)
-        labels = self._gather_labels(loc)
+        if self.shard_final:
+            sl = self.slab
+            sl.load_x(x)
+            sl.load_state(self.Ua, self.cen)
+            sl.run(lx, cfg.max_iter, eps=cfg.eps)
+            self.cen.copy_(sl.centers)
+            loc = ctx.argmax(sl.local_U()[0], nx, ny, sl.nz, cfg.C)
+            labels = self._gather_labels(loc)
+            final_iters = int(sl.stats[0, 2].item())
+        else:
+            stats.zero_()
+            zero = out.lam == 0.0 and out.xi == 0.0
+            ctx.iterate(x, self.Ua, self.Ub, self.cen, lx, cfg, iters=cfg.max_iter, stats=stats, nx=nx,
+                        canonical=not zero)
+            labels = ctx.argmax(self.Ub[0], nx, ny, nz, cfg.C)
+            final_iters = int(stats[0, 2].item())
         ev[4].record()
-        final_iters = int(sl.stats[0, 2].item())
         torch.cuda.synchronize()
         self.labels = labels
         return {"lambda": out.lam, "xi": out.xi, "J": out.J, "generations": out.generations,

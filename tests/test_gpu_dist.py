@@ -22,7 +22,7 @@ CFG = dict(C=4)
 PSO = dict(P=5, max_gen=4, patience=0, seed=31)
 
 
-def _worker(rank, world, port, nz, q):
+def _worker(rank, world, port, nz, shard, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -31,7 +31,7 @@ def _worker(rank, world, port, nz, q):
     from paper_2002_01981_b200.dist import ShardedSegmenter
     ctx = Context(0)
     vol = _case(nz)
-    seg = ShardedSegmenter(ctx, IfcmConfig(**CFG), PsoConfig(**PSO), vol.shape, dist)
+    seg = ShardedSegmenter(ctx, IfcmConfig(**CFG), PsoConfig(**PSO), vol.shape, dist, shard_final=shard)
     rep = seg.segment(torch.as_tensor(vol, device="cuda:0"))
     q.put((rank, seg.labels.cpu().numpy(), rep["lambda"], rep["xi"], rep["final_iters"], rep["centers"]))
     dist.barrier()
@@ -46,10 +46,10 @@ def _port():
     return p
 
 
-# nz = 12: one 16-plane chunk, the final IFCM runs replicated; nz = 40: three
-# chunks, z-slab sharded 2 + 1 (uneven record counts)
-@pytest.mark.parametrize("nz", [12, 40])
-def test_sharded_equals_single(nz):
+# nz = 12: one z-chunk, the final IFCM runs replicated; nz = 40: five chunks,
+# the final IFCM z-slab sharded 3 + 2 (uneven record counts) or replicated
+@pytest.mark.parametrize("nz,shard", [(12, None), (40, True), (40, False)])
+def test_sharded_equals_single(nz, shard):
     from paper_2002_01981_b200 import Context, IfcmConfig, PsoConfig
     from paper_2002_01981_b200.dist import ShardedSegmenter
     ctx = Context(0)
@@ -68,7 +68,7 @@ def test_sharded_equals_single(nz):
     cm = mp.get_context("spawn")
     q = cm.Queue()
     port = _port()
-    procs = [cm.Process(target=_worker, args=(r, 2, port, nz, q)) for r in range(2)]
+    procs = [cm.Process(target=_worker, args=(r, 2, port, nz, shard, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=180) for _ in range(2)]
