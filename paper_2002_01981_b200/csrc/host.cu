@@ -52,10 +52,13 @@ int fail(pifcm_ctx *ctx, int code, const char *fmt, ...) {
                         __FILE__, __LINE__);                                              \
     } while (0)
 
-#define LAUNCH(ctx, n, expr)       \
-    do {                           \
-        CK(ctx, expr);             \
-        (ctx)->launches += (n);    \
+// Every launch goes to the context's device (a process may hold contexts on
+// several devices; cudaSetDevice is a no-op when it is already current).
+#define LAUNCH(ctx, n, expr)                        \
+    do {                                            \
+        CK(ctx, cudaSetDevice((ctx)->device));      \
+        CK(ctx, expr);                              \
+        (ctx)->launches += (n);                     \
     } while (0)
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -440,6 +443,7 @@ static int pso_common(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg 
         (r = check_pso_cfg(ctx, c, p)))
         return r;
     *L = layout(g, c, p);
+    CK(ctx, cudaSetDevice(ctx->device));
     return check_ws(ctx, ws, ws_bytes, L->total);
 }
 
@@ -962,6 +966,7 @@ static int slab_pso_common(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_i
     if (pso->fitness_mode != PIFCM_FIT_CHAINED) return fail(ctx, PIFCM_EINVAL, "slab PSO: CHAINED fitness only");
     *pg = plain_of(slab);
     *L = layout(pg, cfg, pso);
+    if (ctx) CK(ctx, cudaSetDevice(ctx->device));
     return ws ? check_ws(ctx, ws, ws_bytes, L->total) : PIFCM_OK;
 }
 

@@ -645,11 +645,15 @@ static bool make_maps(const StepArgs &a, CUtensorMap *mU, CUtensorMap *mX) {
 
 template <int C, bool M2, bool DU, bool HF = false>
 static cudaError_t launch_stencil(const StepArgs &a, int P, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_step_stencil<C, M2, DU, HF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kStencilSmem);
-        attr = true;
+    // the dynamic shared-memory opt-in is per device: remember it per device
+    static unsigned long long attr_set = 0ull;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+    if (dev < 64 && !(attr_set & (1ull << dev))) {
+        const cudaError_t e = cudaFuncSetAttribute(k_step_stencil<C, M2, DU, HF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kStencilSmem);
+        if (e != cudaSuccess) return e;
+        attr_set |= 1ull << dev;
     }
     CUtensorMap mU, mX;
     if (!make_maps(a, &mU, &mX)) return cudaErrorInvalidValue;

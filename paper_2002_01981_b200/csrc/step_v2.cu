@@ -385,10 +385,15 @@ static bool make_maps2(const StepArgs &a, CUtensorMap *mU, CUtensorMap *mX) {
 
 template <int C, bool M2, bool DU, bool QL>
 static cudaError_t launch_v2_t(const StepArgs &a, int P, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_step_v2<C, M2, DU, QL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2Smem);
-        attr = true;
+    // the dynamic shared-memory opt-in is per device: remember it per device
+    static unsigned long long attr_set = 0ull;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+    if (dev < 64 && !(attr_set & (1ull << dev))) {
+        const cudaError_t e = cudaFuncSetAttribute(k_step_v2<C, M2, DU, QL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   kV2Smem);
+        if (e != cudaSuccess) return e;
+        attr_set |= 1ull << dev;
     }
     CUtensorMap mU, mX;
     if (!make_maps2(a, &mU, &mX)) return cudaErrorInvalidValue;
