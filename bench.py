@@ -322,6 +322,26 @@ def run_ours(args, rank, world, local_rank):
                 traffic = json.load(f).get("dram_bytes_per_launch")
         except Exception:
             pass
+    # The kernel's binding resource is the FP32 pipe, not HBM:
+    # the same launches against the FP32 lane-instruction peak, with SURVEY
+    # §8(d)'s algorithmic count of 245 + 52/P FP32 instructions per vp
+    # (an FMA counts once; H 78, F 112, g / G 52 shared by the P particles of
+    # a launch, Eq. 4 / 2 / 3 / 1 ~53) and the peak 148 SMs x 128 lanes x the
+    # max SM clock (B200_PROFILING: 1965 MHz).
+    alu_view = None
+    if k_n:
+        if c5:  # every slab launch holds all particles on this rank's voxels
+            p_launch = float(Pw)
+            vox = (k_bytes / k_n) / (32.0 * Pw + 4.0)
+        else:   # whole volume, this rank's particles
+            vox = float(nx * ny * nz)
+            p_launch = (k_bytes / k_n - 4.0 * vox) / (32.0 * vox)
+        instr_per_vp = 245.0 + 52.0 / max(p_launch, 1.0)
+        vp_per_s = p_launch * vox / ((k_ms / k_n) * 1e-3)
+        peak_alu = 148 * 128 * 1.965e9 / 1e12
+        alu_view = {"bound": "alu", "achieved": vp_per_s * instr_per_vp / 1e12, "peak": peak_alu,
+                    "unit": "T FP32 lane-instructions/s", "frac": vp_per_s * instr_per_vp / 1e12 / peak_alu,
+                    "alg_instr_per_vp": instr_per_vp, "peak_kind": "derived (148 SM x 128 FP32 lanes x 1965 MHz)"}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -369,6 +389,7 @@ def run_ours(args, rank, world, local_rank):
             "avg_launch_ms": (k_ms / k_n) if k_n else None,
             "launches": k_n,
             "share_of_step": (k_ms / ms) if ms else None,
+            "alu": alu_view,
             "single_state_launches": {
                 "what": "final IFCM (P = 1) launches of the same kernel",
                 "launches": s_n, "avg_launch_ms": (s_ms / s_n) if s_n else None,
