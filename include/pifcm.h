@@ -354,6 +354,53 @@ int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int
 int pifcm_slab_halo(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t P, int32_t op, float *U,
                     float *buf, pifcm_stream stream);
 
+/* ---------------------------------------- z-slab exchange over peer memory
+ * The exchange steps of the slab iteration (halo planes, record gather)
+ * done by the GPUs themselves over NVLink / NVSwitch peer mappings instead of
+ * host-driven collectives: every rank allocates its two state buffers, two
+ * gathered-record buffers and a flag word array with pifcm_peer_alloc,
+ * exports them (pifcm_peer_handle, 64-byte CUDA IPC handles), opens the
+ * other ranks' (pifcm_peer_open) and describes all of them in a
+ * pifcm_peers.  pifcm_slab_p2p_run then runs the iterations with one device
+ * barrier each and no host involvement between convergence checks. */
+#define PIFCM_MAX_PEERS 16
+typedef struct {
+    int32_t world, rank;
+    float *U[2][PIFCM_MAX_PEERS];      /* rank w's two state buffers [P][nz_w+2][ny][nx][4], this process's mapping */
+    double *rec[2][PIFCM_MAX_PEERS];   /* rank w's gathered-record buffers [world][P][nrec_max][10] (even / odd epochs) */
+    uint32_t *flags[PIFCM_MAX_PEERS];  /* rank w's words: [world] arrival epochs, [world] block counter, [world+1] status */
+    int32_t nz[PIFCM_MAX_PEERS];       /* planes held by rank w */
+} pifcm_peers;
+
+/* Device memory that can be shared with other processes (cudaMalloc'ed,
+ * zero-filled); free with pifcm_peer_free.  Sync. */
+int pifcm_peer_alloc(pifcm_ctx *ctx, size_t bytes, void **ptr);
+int pifcm_peer_free(pifcm_ctx *ctx, void *ptr);
+/* 64-byte handle of an allocation of pifcm_peer_alloc (host out). */
+int pifcm_peer_handle(pifcm_ctx *ctx, void *ptr, uint8_t *handle);
+/* Map another process's allocation into this one; close with pifcm_peer_close. */
+int pifcm_peer_open(pifcm_ctx *ctx, const uint8_t *handle, void **ptr);
+int pifcm_peer_close(pifcm_ctx *ctx, void *ptr);
+
+/* `iters` Jacobi IFCM iterations of P states over z-slab
+ * ranks exchanging over peer memory.  Every rank calls it with the same
+ * arguments except its slab.  The states start in the local planes of
+ * U[*cur][rank] (their halo planes are filled here); after each step the
+ * slab's boundary planes go straight into the neighbours' halo planes and
+ * its records [P][nrec][10] (rec_local, scratch) into slot `rank` of every
+ * rank's rec[epoch & 1]; after the device barrier (arrival epochs in the
+ * flag words) each rank finalises Eq. 3 / Eq. 1 from its gathered buffer in
+ * canonical order (as pifcm_slab_finalize with `counts`, dev int32 [world]).
+ * The host checks convergence (stats, dev fp64 [P][4]) every 16 iterations.
+ * On return *cur names the buffer holding the last iteration, *epoch the
+ * next barrier epoch (pass it back on the next call), *iters_done the
+ * iterations run.  A barrier that does not complete within ~20 s sets the
+ * status word and the call returns PIFCM_ECUDA.  Sync. */
+int pifcm_slab_p2p_run(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const float *x,
+                       const pifcm_peers *peers, int32_t P, const int32_t *counts, int32_t nrec_max,
+                       float *centers, const double *lam_xi, double *stats, double *rec_local, int32_t iters,
+                       uint32_t *epoch, int32_t *cur, int32_t *iters_done, pifcm_stream stream);
+
 /* ------------------------------------------- pipeline parts for z-slab ranks
  * Alg. 2 step 1 when the volume is split into slabs: each
  * rank reduces min / max over its own planes (pifcm_minmax_u8), the caller

@@ -52,6 +52,16 @@ class Report(ct.Structure):
                 ("t_final", ct.c_double), ("t_total", ct.c_double)]
 
 
+MAX_PEERS = 16
+
+
+class Peers(ct.Structure):
+    """pifcm_peers: every rank's buffers as mapped into this process."""
+    _fields_ = [("world", ct.c_int32), ("rank", ct.c_int32),
+                ("U", (ct.c_void_p * MAX_PEERS) * 2), ("rec", (ct.c_void_p * MAX_PEERS) * 2),
+                ("flags", ct.c_void_p * MAX_PEERS), ("nz", ct.c_int32 * MAX_PEERS)]
+
+
 _vp = ct.c_void_p
 _G = ct.POINTER(Grid)
 _C = ct.POINTER(IfcmCfg)
@@ -102,6 +112,14 @@ SIGNATURES = {
     "pifcm_slab_pso_update": (ct.c_int, [_vp, _G, _C, _P, _vp, ct.c_size_t, _vp]),
     "pifcm_slab_pso_result_get": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, _vp]),
     "pifcm_slab_pso_gbest_state": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, _vp]),
+    "pifcm_peer_alloc": (ct.c_int, [_vp, ct.c_size_t, ct.POINTER(ct.c_void_p)]),
+    "pifcm_peer_free": (ct.c_int, [_vp, _vp]),
+    "pifcm_peer_handle": (ct.c_int, [_vp, _vp, _vp]),
+    "pifcm_peer_open": (ct.c_int, [_vp, _vp, ct.POINTER(ct.c_void_p)]),
+    "pifcm_peer_close": (ct.c_int, [_vp, _vp]),
+    "pifcm_slab_p2p_run": (ct.c_int, [_vp, _G, _C, _vp, ct.POINTER(Peers), ct.c_int32, _vp, ct.c_int32, _vp, _vp,
+                                      _vp, _vp, ct.c_int32, ct.POINTER(ct.c_uint32), ct.POINTER(ct.c_int32),
+                                      ct.POINTER(ct.c_int32), _vp]),
     "pifcm_slab_chunk": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32, _vp]),
     "pifcm_slab_records": (ct.c_int, [_G, ct.POINTER(ct.c_int32)]),
     "pifcm_slab_step": (ct.c_int, [_vp, _G, _C, _vp, _vp, _vp, _vp, _vp, ct.c_int32, _vp, _vp, _vp]),

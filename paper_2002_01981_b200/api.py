@@ -327,6 +327,42 @@ class Context:
     def slab_halo(self, grid, P, op, U, buf=None, stream=None):
         self._ck(self.lib.pifcm_slab_halo(self._h, ct.byref(grid), P, op, _ptr(U), _ptr(buf), _stream(stream)))
 
+    # ------------------------------------------------------- peer memory
+    def peer_alloc(self, nbytes: int) -> int:
+        """Zeroed device memory shareable with other processes (raw pointer)."""
+        p = ct.c_void_p()
+        self._ck(self.lib.pifcm_peer_alloc(self._h, nbytes, ct.byref(p)))
+        return p.value
+
+    def peer_free(self, ptr: int):
+        self._ck(self.lib.pifcm_peer_free(self._h, ptr))
+
+    def peer_handle(self, ptr: int) -> bytes:
+        h = (ct.c_uint8 * 64)()
+        self._ck(self.lib.pifcm_peer_handle(self._h, ptr, h))
+        return bytes(h)
+
+    def peer_open(self, handle: bytes) -> int:
+        h = (ct.c_uint8 * 64).from_buffer_copy(handle)
+        p = ct.c_void_p()
+        self._ck(self.lib.pifcm_peer_open(self._h, h, ct.byref(p)))
+        return p.value
+
+    def peer_close(self, ptr: int):
+        self._ck(self.lib.pifcm_peer_close(self._h, ptr))
+
+    def slab_p2p_run(self, grid, cfg, x, peers, P, counts, nrec_max, centers, lam_xi, stats, rec_local, iters,
+                     epoch: int, cur: int, stream=None):
+        """pifcm_slab_p2p_run -> (epoch, cur, iters_done)."""
+        e = ct.c_uint32(epoch)
+        c = ct.c_int32(cur)
+        n = ct.c_int32(0)
+        self._ck(self.lib.pifcm_slab_p2p_run(self._h, ct.byref(grid), ct.byref(cfg.c()), _ptr(x), ct.byref(peers), P,
+                                             _ptr(counts), nrec_max, _ptr(centers), _ptr(lam_xi), _ptr(stats),
+                                             _ptr(rec_local), iters, ct.byref(e), ct.byref(c), ct.byref(n),
+                                             _stream(stream)))
+        return e.value, c.value, n.value
+
     # -------------------------------------------- pipeline parts for slab ranks
     def minmax_u8(self, vol: torch.Tensor, mm: torch.Tensor, stream=None):
         """mm: device int32 [2] <- {min, max} of vol (uint32 bits; values <= 255)."""

@@ -1090,4 +1090,124 @@ int pifcm_slab_pso_gbest_state(pifcm_ctx *ctx, const pifcm_grid *slab, const pif
     return pifcm_pso_gbest_state(ctx, &pg, cfg, pso, ws, U_out, c_out, stream);
 }
 
+
+// ============================================================== ABI: peer memory
+int pifcm_peer_alloc(pifcm_ctx *ctx, size_t bytes, void **ptr) {
+    if (!ctx || !ptr || bytes == 0) return PIFCM_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, cudaMalloc(ptr, bytes));
+    CK(ctx, cudaMemset(*ptr, 0, bytes));
+    return PIFCM_OK;
+}
+int pifcm_peer_free(pifcm_ctx *ctx, void *ptr) {
+    if (!ctx) return PIFCM_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, cudaFree(ptr));
+    return PIFCM_OK;
+}
+int pifcm_peer_handle(pifcm_ctx *ctx, void *ptr, uint8_t *handle) {
+    if (!ctx || !ptr || !handle) return PIFCM_EINVAL;
+    cudaIpcMemHandle_t h;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, cudaIpcGetMemHandle(&h, ptr));
+    static_assert(sizeof h == 64, "CUDA IPC handles are 64 bytes");
+    memcpy(handle, &h, sizeof h);
+    return PIFCM_OK;
+}
+int pifcm_peer_open(pifcm_ctx *ctx, const uint8_t *handle, void **ptr) {
+    if (!ctx || !ptr || !handle) return PIFCM_EINVAL;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return PIFCM_OK;
+}
+int pifcm_peer_close(pifcm_ctx *ctx, void *ptr) {
+    if (!ctx) return PIFCM_EINVAL;
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, cudaIpcCloseMemHandle(ptr));
+    return PIFCM_OK;
+}
+
+int pifcm_slab_p2p_run(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const float *x,
+                       const pifcm_peers *peers, int32_t P, const int32_t *counts, int32_t nrec_max,
+                       float *centers, const double *lam_xi, double *stats, double *rec_local, int32_t iters,
+                       uint32_t *epoch, int32_t *cur, int32_t *iters_done, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_slab(ctx, slab)) || (r = check_cfg(ctx, cfg))) return r;
+    if (!peers || !x || !centers || !lam_xi || !stats || !rec_local || !epoch || !cur || !iters_done)
+        return fail(ctx, PIFCM_EINVAL, "NULL argument");
+    const int world = peers->world, rank = peers->rank;
+    if (world < 1 || world > PIFCM_MAX_PEERS || rank < 0 || rank >= world || P < 1 || iters < 1 ||
+        (*cur != 0 && *cur != 1) || peers->nz[rank] != slab->nz)
+        return fail(ctx, PIFCM_EINVAL, "invalid peer description");
+    int32_t nrec = 0;
+    if ((r = pifcm_slab_records(slab, &nrec))) return fail(ctx, r, "slab records");
+    if (nrec > nrec_max) return fail(ctx, PIFCM_EINVAL, "nrec_max %d < this slab's %d records", nrec_max, nrec);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CK(ctx, cudaSetDevice(ctx->device));
+    const long long plane = (long long)slab->nx * slab->ny;
+    unsigned *myflags = peers->flags[rank];
+    int *status = reinterpret_cast<int *>(myflags + world + 1);
+    CK(ctx, cudaMemsetAsync(stats, 0, sizeof(double) * 4 * P, st));
+    auto put = [&](int buf, bool records, unsigned e) -> int {
+        P2PPut a{};
+        a.src = reinterpret_cast<const float4 *>(peers->U[buf][rank]);
+        a.plane = plane;
+        a.state = plane * (slab->nz + 2);
+        a.nz = slab->nz;
+        a.P = P;
+        if (rank > 0) {
+            a.lo_dst = reinterpret_cast<float4 *>(peers->U[buf][rank - 1]) + (long long)(peers->nz[rank - 1] + 1) * plane;
+            a.lo_state = plane * (peers->nz[rank - 1] + 2);
+        }
+        if (rank < world - 1) {
+            a.hi_dst = reinterpret_cast<float4 *>(peers->U[buf][rank + 1]);
+            a.hi_state = plane * (peers->nz[rank + 1] + 2);
+        }
+        a.rec_src = records ? rec_local : nullptr;
+        a.nrec = nrec; a.nrec_max = nrec_max; a.world = world; a.rank = rank;
+        for (int w = 0; w < world; ++w) {
+            a.rec_dst[w] = peers->rec[e & 1u][w];
+            a.flags[w] = peers->flags[w];
+        }
+        a.counter = myflags + world;
+        a.epoch = e;
+        LAUNCH(ctx, 1, launch_p2p_put(a, st));
+        LAUNCH(ctx, 1, launch_p2p_wait(myflags, world, e, status, st));
+        return PIFCM_OK;
+    };
+    unsigned e = *epoch;
+    int c = *cur;
+    // halos of the starting states
+    if ((r = put(c, false, ++e))) return r;
+    int t = 0;
+    const int check_every = 16;
+    for (t = 1; t <= iters; ++t) {
+        if ((r = pifcm_slab_step(ctx, slab, cfg, x, peers->U[c][rank], peers->U[1 - c][rank], centers, lam_xi, P,
+                                 stats, rec_local, stream)))
+            return r;
+        if ((r = put(1 - c, true, ++e))) return r;
+        LAUNCH(ctx, 1, launch_slab_finalize(cfg->C, P, world, nrec_max, counts, peers->rec[e & 1u][rank], centers,
+                                            stats, nullptr, cfg->eps, nullptr, st));
+        c = 1 - c;
+        if (t % check_every == 0 || t == iters) {
+            std::vector<double> h(4 * (size_t)P);
+            int hs = 0;
+            CK(ctx, cudaMemcpyAsync(h.data(), stats, sizeof(double) * 4 * P, cudaMemcpyDeviceToHost, st));
+            CK(ctx, cudaMemcpyAsync(&hs, status, sizeof hs, cudaMemcpyDeviceToHost, st));
+            CK(ctx, cudaStreamSynchronize(st));
+            if (hs) return fail(ctx, PIFCM_ECUDA, "peer barrier timed out at epoch %u", e);
+            bool all = cfg->eps > 0.f;
+            for (int p = 0; p < P && all; ++p) all = h[4 * p + 3] != 0.0;
+            if (all) break;
+        }
+    }
+    *epoch = e;
+    *cur = c;
+    *iters_done = t > iters ? iters : t;
+    return PIFCM_OK;
+}
+
 }  // extern "C"

@@ -117,6 +117,24 @@ struct PsoUpdateArgs {
     uint32_t key0, key1;
 };
 
+// z-slab exchange over peer memory (p2p.cu)
+constexpr int kMaxPeers = 16;
+struct P2PPut {
+    const float4 *src;           // this rank's new states [P][nz+2][ny][nx]
+    long long plane, state;      // voxels per plane, per state (incl. halos)
+    int nz, P;
+    float4 *lo_dst;              // rank-1's buffer + its upper halo plane (nullable)
+    long long lo_state;          // rank-1's voxels per state
+    float4 *hi_dst;              // rank+1's buffer + its lower halo plane (nullable)
+    long long hi_state;
+    const double *rec_src;       // this rank's records [P][nrec][kNR] (nullable)
+    int nrec, nrec_max, world, rank;
+    double *rec_dst[kMaxPeers];  // every rank's gathered buffer [world][P][nrec_max][kNR]
+    unsigned *flags[kMaxPeers];  // every rank's flags [world]
+    unsigned *counter;           // this rank's block-arrival counter (0 between launches)
+    unsigned epoch;
+};
+
 // ---------------------------------------------------------------- launchers
 // All return cudaGetLastError() of the launch.
 cudaError_t launch_step(const StepArgs &a, int C, bool stencil, int P, cudaStream_t st);
@@ -151,6 +169,8 @@ cudaError_t launch_fit_sum(const double *partials, int nparts, int P, double *fi
 cudaError_t launch_mode_pre(SwarmDev s, const float *shared_c, double *lamxi, int mode, cudaStream_t st);
 cudaError_t launch_leader_post(SwarmDev s, const float *shared_c, cudaStream_t st);
 cudaError_t launch_set_hdr(int *hdr, int idx, int value, cudaStream_t st);
+cudaError_t launch_p2p_put(const P2PPut &a, cudaStream_t st);
+cudaError_t launch_p2p_wait(const unsigned *flags, int world, unsigned epoch, int *status, cudaStream_t st);
 cudaError_t launch_set_lamxi(double *dst, const double *dhdr, cudaStream_t st);
 cudaError_t launch_slab_finalize(int C, int P, int world, int nrec, const int *counts, const double *records,
                                  float *centers, double *stats, double *fitness, float eps, int *status,

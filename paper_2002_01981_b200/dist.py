@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import torch
 
 __all__ = ["shard_range", "allgather_fitness", "ShardedPso", "GpuPsoEngine", "ShardedSegmenter",
-           "slab_range", "SlabIfcm", "SlabPso", "SlabSegmenter"]
+           "slab_range", "SlabIfcm", "SlabIfcmP2P", "SlabPso", "SlabSegmenter"]
 
 
 def shard_range(P: int, world: int, rank: int) -> tuple[int, int]:
@@ -457,6 +457,9 @@ class SlabIfcm:
                 self.Ua[p].copy_(self.Ub[p])
 
     def run(self, lam_xi: torch.Tensor, iters: int, eps: float = 0.0, check_every: int = 4) -> int:
+        """`iters` iterations from the current states (stats restart)."""
+        self.stats.zero_()
+        self.swaps = 0
         done = 0
         for it in range(iters):
             self.step(lam_xi, eps)
@@ -464,6 +467,119 @@ class SlabIfcm:
             if eps > 0 and (it + 1) % check_every == 0 and bool((self.stats[:, 3] != 0).all()):
                 break
         self.sync_states()
+        return done
+
+
+class _DevArray:
+    """A raw device allocation seen by torch (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _as_tensor(ptr, shape, dtype, dev):
+    typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4"}[dtype]
+    return torch.as_tensor(_DevArray(ptr, shape, typestr), device=dev)
+
+
+class SlabIfcmP2P:
+    """SlabIfcm with the exchange done by the GPUs over peer memory
+    (pifcm_slab_p2p_run): every rank maps the others' state buffers,
+    gathered-record buffers and flag words (CUDA IPC handles swapped once
+    through torch.distributed); per iteration the step, a put kernel that
+    stores the boundary planes into the neighbours' halo planes and the
+    records into every rank's gathered buffer, a device barrier and the
+    canonical finalisation -- no NCCL call and no host round trip between the
+    convergence checks.  Results are bit-identical to SlabIfcm."""
+
+    def __init__(self, ctx, cfg, nx, ny, nz_total, P, dist=None):
+        from . import _abi
+        self.ctx, self.cfg, self.P, self.dist = ctx, cfg, P, dist
+        self.geo = g = _SlabGeometry(ctx, nx, ny, nz_total, P, dist)
+        self.world, self.rank, self.nz, self.grid, self.plane = g.world, g.rank, g.nz, g.grid, g.plane
+        if self.world > _abi.MAX_PEERS:
+            raise ValueError(f"at most {_abi.MAX_PEERS} ranks")
+        self.dev = g.dev
+        sb = P * (self.nz + 2) * self.plane * 16
+        rb = self.world * P * g.nrec_max * 10 * 8
+        self._own = [ctx.peer_alloc(sb), ctx.peer_alloc(sb), ctx.peer_alloc(rb), ctx.peer_alloc(rb),
+                     ctx.peer_alloc(4 * (self.world + 2))]
+        mine = ([ctx.peer_handle(p) for p in self._own], self.nz)
+        if self.world > 1:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, mine)
+        else:
+            allh = [mine]
+        self._opened = []
+        ptrs = []
+        for w, (hs, _) in enumerate(allh):
+            if w == self.rank:
+                ptrs.append(self._own)
+            else:
+                op = [ctx.peer_open(h) for h in hs]
+                self._opened += op
+                ptrs.append(op)
+        pe = _abi.Peers()
+        pe.world, pe.rank = self.world, self.rank
+        for w in range(self.world):
+            pe.U[0][w], pe.U[1][w], pe.rec[0][w], pe.rec[1][w], pe.flags[w] = ptrs[w]
+            pe.nz[w] = allh[w][1]
+        self.peers = pe
+        shape = (P, (self.nz + 2) * self.plane, 4)
+        self.U = [_as_tensor(self._own[i], shape, torch.float32, self.dev) for i in range(2)]
+        self.centers = torch.zeros((P, 4), dtype=torch.float32, device=self.dev)
+        self.stats = torch.zeros((P, 4), dtype=torch.float64, device=self.dev)
+        self.epoch, self.cur = 0, 0
+        if self.world > 1:
+            dist.barrier()  # every mapping is open before any rank writes into it
+
+    def close(self):
+        for p in self._opened:
+            self.ctx.peer_close(p)
+        if self.world > 1:
+            self.dist.barrier()  # nobody maps this rank's memory any more
+        for p in self._own:
+            self.ctx.peer_free(p)
+        self._opened, self._own = [], []
+
+    def load_x(self, x_full: torch.Tensor):
+        self.x = self.geo.slab_planes(x_full)
+        return self.x
+
+    def set_x(self, x_slab: torch.Tensor):
+        self.x = x_slab
+
+    def load_state(self, U_full: torch.Tensor, centers: torch.Tensor):
+        """U_full [P][nz_total*ny*nx][4]: this slab's local planes (the outer
+        halo planes stay zero, the interior ones are exchanged by the run)."""
+        pl = self.plane
+        self.U[self.cur][:, pl: pl * (self.nz + 1)] = U_full[:, self.geo.z0 * pl:(self.geo.z0 + self.nz) * pl]
+        self.centers.copy_(centers.view(self.P, 4))
+
+    def load_local(self, U_slab: torch.Tensor, centers: torch.Tensor):
+        """U_slab [P][(nz+2)*ny*nx][4] in the slab layout (local planes used)."""
+        pl = self.plane
+        self.U[self.cur][:, pl: pl * (self.nz + 1)] = U_slab.view(self.P, -1, 4)[:, pl: pl * (self.nz + 1)]
+        self.centers.copy_(centers.view(self.P, 4))
+
+    def local_U(self) -> torch.Tensor:
+        return self.U[self.cur][:, self.plane: self.plane * (self.nz + 1)]
+
+    def run(self, lam_xi: torch.Tensor, iters: int, eps: float = 0.0) -> int:
+        from dataclasses import replace
+        cfg = replace(self.cfg, eps=eps)
+        start = self.cur
+        self.epoch, self.cur, done = self.ctx.slab_p2p_run(
+            self.grid, cfg, self.x, self.peers, self.P, self.geo.counts, self.geo.nrec_max, self.centers,
+            lam_xi, self.stats, self.geo.rec, iters, self.epoch, self.cur)
+        # a converged state was skipped from then on: its latest U is in the
+        # buffer its last real step wrote
+        n = self.stats[:, 2].to(torch.int64).cpu()
+        for p in range(self.P):
+            b = (start + int(n[p])) % 2
+            if b != self.cur:
+                self.U[self.cur][p].copy_(self.U[b][p])
         return done
 
 
