@@ -149,8 +149,19 @@ class GpuPsoEngine:
         self.ctx.pso_gbest_state(self.grid, self.cfg, self.pso, self.ws, U_out, c_out)
 
 
+def _slab_driver(ctx, cfg, nx, ny, nz_total, P, dist):
+    """SlabIfcmP2P (exchange over peer memory) where the ranks can map each
+    other's memory, else SlabIfcm (host-driven collectives); same results."""
+    try:
+        return SlabIfcmP2P(ctx, cfg, nx, ny, nz_total, P, dist)
+    except Exception:  # no peer mapping between these devices
+        if dist is not None and dist.get_world_size() > 1:
+            dist.barrier()
+        return SlabIfcm(ctx, cfg, nx, ny, nz_total, P, dist)
+
+
 class ShardedSegmenter:
-    SHARD_FINAL_MIN_VOXELS = 16 * 1024 * 1024
+    SHARD_FINAL_MIN_VOXELS = 4 * 1024 * 1024
 
     """pifcm_segment with the PSO particles sharded over the ranks of `dist`.
 
@@ -175,14 +186,15 @@ class ShardedSegmenter:
         self.engine = None
         world = dist.get_world_size() if dist is not None else 1
         tz = ctx.slab_chunk(self.nx, self.ny, self.nz)
-        # The final IFCM (one state) runs z-slab sharded only when a rank's
-        # share of an iteration outweighs the per-iteration exchange and
-        # launch overheads (~0.1 ms); otherwise every rank runs it whole, in
+        # The final IFCM (one state) runs z-slab sharded (exchange over peer
+        # memory, a few tens of us per iteration) when a rank's share of an
+        # iteration outweighs that; otherwise every rank runs it whole, in
         # the same canonical decomposition -- the results are bit-identical
         # either way.
         big = nvox >= self.SHARD_FINAL_MIN_VOXELS if shard_final is None else bool(shard_final)
         self.shard_final = world > 1 and -(-self.nz // tz) >= world and big
-        self.slab = SlabIfcm(ctx, cfg, self.nx, self.ny, self.nz, 1, dist if self.shard_final else None)
+        self.slab = (_slab_driver(ctx, cfg, self.nx, self.ny, self.nz, 1, dist) if self.shard_final
+                     else SlabIfcm(ctx, cfg, self.nx, self.ny, self.nz, 1, None))
         w = self.slab.world
         self.lab_counts = [slab_range(self.nz, w, r, tz)[1] * self.nx * self.ny for r in range(w)]
         self.lab_pad = torch.zeros((w, max(self.lab_counts)), dtype=torch.uint8, device=self.dev)
@@ -566,6 +578,11 @@ class SlabIfcmP2P:
     def local_U(self) -> torch.Tensor:
         return self.U[self.cur][:, self.plane: self.plane * (self.nz + 1)]
 
+    @property
+    def Ua(self) -> torch.Tensor:
+        """The current states in the slab layout (as SlabIfcm.Ua)."""
+        return self.U[self.cur]
+
     def run(self, lam_xi: torch.Tensor, iters: int, eps: float = 0.0) -> int:
         from dataclasses import replace
         cfg = replace(self.cfg, eps=eps)
@@ -645,7 +662,7 @@ class SlabSegmenter:
     def __init__(self, ctx, cfg, pso, shape, dist=None):
         self.ctx, self.cfg, self.pso, self.dist = ctx, cfg, pso, dist
         self.nz, self.ny, self.nx = shape
-        self.ifcm = SlabIfcm(ctx, cfg, self.nx, self.ny, self.nz, 1, dist)
+        self.ifcm = _slab_driver(ctx, cfg, self.nx, self.ny, self.nz, 1, dist)
         self.swarm = SlabPso(ctx, cfg, pso, self.nx, self.ny, self.nz, dist)
         self.geo = self.ifcm.geo
         self.dev = self.geo.dev
