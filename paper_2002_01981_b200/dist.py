@@ -150,13 +150,12 @@ class GpuPsoEngine:
 
 
 def _slab_driver(ctx, cfg, nx, ny, nz_total, P, dist):
-    """SlabIfcmP2P (exchange over peer memory) where the ranks can map each
-    other's memory, else SlabIfcm (host-driven collectives); same results."""
+    """SlabIfcmP2P (exchange over peer memory) where every rank can map the
+    others' memory (decided collectively), else SlabIfcm (host-driven
+    collectives); the results are the same."""
     try:
         return SlabIfcmP2P(ctx, cfg, nx, ny, nz_total, P, dist)
-    except Exception:  # no peer mapping between these devices
-        if dist is not None and dist.get_world_size() > 1:
-            dist.barrier()
+    except RuntimeError:
         return SlabIfcm(ctx, cfg, nx, ny, nz_total, P, dist)
 
 
@@ -511,27 +510,49 @@ class SlabIfcmP2P:
         self.geo = g = _SlabGeometry(ctx, nx, ny, nz_total, P, dist)
         self.world, self.rank, self.nz, self.grid, self.plane = g.world, g.rank, g.nz, g.grid, g.plane
         if self.world > _abi.MAX_PEERS:
-            raise ValueError(f"at most {_abi.MAX_PEERS} ranks")
+            raise RuntimeError(f"peer exchange supports at most {_abi.MAX_PEERS} ranks")
         self.dev = g.dev
         sb = P * (self.nz + 2) * self.plane * 16
         rb = self.world * P * g.nrec_max * 10 * 8
-        self._own = [ctx.peer_alloc(sb), ctx.peer_alloc(sb), ctx.peer_alloc(rb), ctx.peer_alloc(rb),
-                     ctx.peer_alloc(4 * (self.world + 2))]
-        mine = ([ctx.peer_handle(p) for p in self._own], self.nz)
+        # every step below is agreed on by all ranks, so that either all of
+        # them use peer memory or none does (a rank that cannot map a peer
+        # must not leave the others waiting at a barrier)
+        self._own, self._opened = [], []
+        ok = 1
+        try:
+            for nb in (sb, sb, rb, rb, 4 * (self.world + 2)):
+                self._own.append(ctx.peer_alloc(nb))
+            mine = ([ctx.peer_handle(p) for p in self._own], self.nz)
+        except Exception:
+            ok, mine = 0, None
+        allh = [mine]
         if self.world > 1:
             allh = [None] * self.world
             dist.all_gather_object(allh, mine)
-        else:
-            allh = [mine]
-        self._opened = []
+        ok = ok and all(h is not None for h in allh)
         ptrs = []
-        for w, (hs, _) in enumerate(allh):
-            if w == self.rank:
-                ptrs.append(self._own)
-            else:
-                op = [ctx.peer_open(h) for h in hs]
-                self._opened += op
-                ptrs.append(op)
+        if ok:
+            try:
+                for w, (hs, _) in enumerate(allh):
+                    if w == self.rank:
+                        ptrs.append(self._own)
+                    else:
+                        op = [ctx.peer_open(h) for h in hs]
+                        self._opened += op
+                        ptrs.append(op)
+            except Exception:
+                ok = 0
+        if self.world > 1:
+            flag = torch.tensor([ok], dtype=torch.int32,
+                                device=self.dev if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            ok = int(flag.item())
+        if not ok:
+            for p in self._opened:
+                ctx.peer_close(p)
+            for p in self._own:
+                ctx.peer_free(p)
+            raise RuntimeError("peer memory mapping is not available on every rank")
         pe = _abi.Peers()
         pe.world, pe.rank = self.world, self.rank
         for w in range(self.world):
