@@ -268,6 +268,12 @@ int pifcm_pso_run(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
  * the 256-bin histogram of R15 into hist (dev int64 [256], nullable).  Async. */
 int pifcm_normalize_u8(pifcm_ctx *ctx, const pifcm_grid *grid, const uint8_t *vol, float *x,
                        int64_t *hist, void *ws, size_t ws_bytes, pifcm_stream stream);
+/* The same for a volume of type dtype (PIFCM_U8, PIFCM_U16 --
+ * integer arithmetic as u8 -- or PIFCM_F32: x = (v - min) / (max - min) and
+ * the R15 bin floor((v - min) * 255 / (max - min) + 0.5) in fp64, values
+ * assumed finite).  PIFCM_EINVAL for another dtype.  Async. */
+int pifcm_normalize(pifcm_ctx *ctx, const pifcm_grid *grid, const void *vol, int32_t dtype, float *x,
+                    int64_t *hist, void *ws, size_t ws_bytes, pifcm_stream stream);
 
 /* R15 "Modified_FCM with Gaussian mixture model": 1-D EM on
  * the 256-bin histogram -> C initial centres (fp32 [4], device).  Async. */
@@ -284,7 +290,7 @@ int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float 
  * histogram + GMM, FCM start (lambda = xi = 0) until eps, PSO over
  * (lambda, xi) with CHAINED fitness, final IFCM at the gbest from the gbest's
  * (U, c) until eps, argmax.  Sync.
- *   vol      dev u8 [nz][ny][nx] (dtype must be PIFCM_U8 in this version)
+ *   vol      dev [nz][ny][nx] of type dtype (PIFCM_U8, PIFCM_U16, PIFCM_F32)
  *   labels   dev u8 [nz][ny][nx]  out
  *   U_out    dev fp32 [nz][ny][nx][4] out, nullable: final memberships
  *   z_slice  -1: whole volume.  >= 0: the paper's `z` argument;

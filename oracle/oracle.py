@@ -20,7 +20,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 __all__ = [
     "shell_weights", "ifcm_step", "ifcm_voxels", "fcm_step", "centers", "argmax",
-    "normalize_u8", "histogram_u8", "gmm_init", "philox4x32_10", "philox_pair",
+    "normalize_u8", "histogram_u8", "normalize", "histogram", "gmm_init", "philox4x32_10", "philox_pair",
     "pso_init", "pso_move", "pso_update", "pso_run", "ifcm_run", "fcm_run", "segment_u8",
     "num_threads", "set_num_threads", "PsoResult", "SegmentResult",
 ]
@@ -70,6 +70,13 @@ def _declare(L):
     L.orc_argmax.argtypes = [_dp, l, i, _u8p]
     L.orc_normalize_u8.argtypes = [_u8p, l, _dp]
     L.orc_histogram_u8.argtypes = [_u8p, l, _i64p]
+    L.orc_normalize_u16.argtypes = [_vp, l, _dp]
+    L.orc_histogram_u16.argtypes = [_vp, l, _i64p]
+    L.orc_normalize_f32.argtypes = [_vp, l, _dp]
+    L.orc_histogram_f32.argtypes = [_vp, l, _i64p]
+    L.orc_segment_typed.argtypes = [_vp, i, i, i, i, i, d, i, i, d, d, i, i, i, i, i, d, d, d, u64,
+                                    _u8p, _dp, _dp, _dp, _dp, _ip, _ip, _dp, i]
+    L.orc_segment_typed.restype = i
     L.orc_gmm_init.argtypes = [_i64p, i, i, _dp]
     L.orc_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
     L.orc_philox_pair.argtypes = [u64, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, _dp, _dp]
@@ -88,6 +95,9 @@ def _declare(L):
     L.orc_segment_u8.restype = i
     L.orc_num_threads.restype = i
     L.orc_set_num_threads.argtypes = [i]
+
+
+_vp = ct.c_void_p
 
 
 def _p(a, t=_dp):
@@ -186,6 +196,29 @@ def histogram_u8(vol):
     vol = np.ascontiguousarray(vol, dtype=np.uint8)
     h = np.zeros(256, np.int64)
     _L().orc_histogram_u8(_p(vol, _u8p), vol.size, _p(h, _i64p))
+    return h
+
+
+_TYPED = {np.dtype(np.uint8): (0, "u8"), np.dtype(np.uint16): (1, "u16"), np.dtype(np.float32): (2, "f32")}
+
+
+def normalize(vol):
+    """Alg. 2 step 1 for a u8 / u16 / f32 volume (R16)."""
+    vol = np.ascontiguousarray(vol)
+    code, name = _TYPED[vol.dtype]
+    x = np.empty(vol.shape, np.float64)
+    ptr = vol.ctypes.data_as(_u8p if code == 0 else _vp)
+    getattr(_L(), "orc_normalize_" + name)(ptr, vol.size, _p(x))
+    return x
+
+
+def histogram(vol):
+    """R15 histogram of a u8 / u16 / f32 volume."""
+    vol = np.ascontiguousarray(vol)
+    code, name = _TYPED[vol.dtype]
+    h = np.zeros(256, np.int64)
+    ptr = vol.ctypes.data_as(_u8p if code == 0 else _vp)
+    getattr(_L(), "orc_histogram_" + name)(ptr, vol.size, _p(h, _i64p))
     return h
 
 
@@ -307,7 +340,9 @@ class SegmentResult:
 
 def segment_u8(vol, C, P, max_gen, seed, m=2.0, q_mode=0, v=1, h=1.0, eps=1e-5, max_iter=100,
                ring_k=1, patience=0, tol=1e-4, v0=0.1, vmax=0.5, want_U=True, fitness_mode=0):
-    vol = np.ascontiguousarray(vol, dtype=np.uint8)
+    vol = np.ascontiguousarray(vol)
+    if vol.dtype not in _TYPED:
+        vol = vol.astype(np.uint8)
     nz, ny, nx = vol.shape
     N = vol.size
     lab = np.empty(N, np.uint8)
@@ -318,8 +353,9 @@ def segment_u8(vol, C, P, max_gen, seed, m=2.0, q_mode=0, v=1, h=1.0, eps=1e-5, 
     gens = ct.c_int()
     fi = ct.c_int()
     ci = np.empty(C)
-    _L().orc_segment_u8(_p(vol, _u8p), nx, ny, nz, C, m, q_mode, v, h, eps, max_iter, P, ring_k,
-                        max_gen, patience, tol, v0, vmax, seed, _p(lab, _u8p), _p(U), _p(c),
-                        _p(lx), ct.byref(J), ct.byref(gens), ct.byref(fi), _p(ci), fitness_mode)
+    code = _TYPED[vol.dtype][0]
+    _L().orc_segment_typed(vol.ctypes.data_as(_vp), code, nx, ny, nz, C, m, q_mode, v, h, eps, max_iter, P,
+                           ring_k, max_gen, patience, tol, v0, vmax, seed, _p(lab, _u8p), _p(U), _p(c),
+                           _p(lx), ct.byref(J), ct.byref(gens), ct.byref(fi), _p(ci), fitness_mode)
     return SegmentResult(lab.reshape(nz, ny, nx), U, c, lx[0], lx[1], J.value, gens.value,
                          fi.value, ci)

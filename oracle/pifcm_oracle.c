@@ -304,6 +304,59 @@ void orc_histogram_u8(const uint8_t *vol, long N, int64_t *hist) {
     }
 }
 
+/* Alg. 2 step 1 for 16-bit and fp32 volumes (u8 / u16 /
+ * f32 inputs): the same global min-max normalisation (R16) and the R15
+ * histogram of the same levels b/255 -- u16 in integers like u8; f32 in fp64:
+ * bin = floor((v - min) * 255 / (max - min) + 0.5). */
+void orc_normalize_u16(const uint16_t *vol, long N, double *x) {
+    int mn = 65535, mx = 0;
+    for (long i = 0; i < N; ++i) {
+        if (vol[i] < mn) mn = vol[i];
+        if (vol[i] > mx) mx = vol[i];
+    }
+    for (long i = 0; i < N; ++i)
+        x[i] = (mx > mn) ? (double)(vol[i] - mn) / (double)(mx - mn) : 0.0;
+}
+void orc_histogram_u16(const uint16_t *vol, long N, int64_t *hist) {
+    int64_t mn = 65535, mx = 0;
+    for (long i = 0; i < N; ++i) {
+        if (vol[i] < mn) mn = vol[i];
+        if (vol[i] > mx) mx = vol[i];
+    }
+    for (int b = 0; b < 256; ++b) hist[b] = 0;
+    const int64_t rng = mx - mn;
+    for (long i = 0; i < N; ++i) {
+        int64_t b = 0;
+        if (rng > 0) b = (((int64_t)vol[i] - mn) * 255 + rng / 2) / rng;
+        hist[b] += 1;
+    }
+}
+void orc_normalize_f32(const float *vol, long N, double *x) {
+    double mn = INFINITY, mx = -INFINITY;
+    for (long i = 0; i < N; ++i) {
+        if ((double)vol[i] < mn) mn = vol[i];
+        if ((double)vol[i] > mx) mx = vol[i];
+    }
+    for (long i = 0; i < N; ++i) x[i] = (mx > mn) ? ((double)vol[i] - mn) / (mx - mn) : 0.0;
+}
+void orc_histogram_f32(const float *vol, long N, int64_t *hist) {
+    double mn = INFINITY, mx = -INFINITY;
+    for (long i = 0; i < N; ++i) {
+        if ((double)vol[i] < mn) mn = vol[i];
+        if ((double)vol[i] > mx) mx = vol[i];
+    }
+    for (int b = 0; b < 256; ++b) hist[b] = 0;
+    for (long i = 0; i < N; ++i) {
+        int b = 0;
+        if (mx > mn) {
+            b = (int)floor(((double)vol[i] - mn) * 255.0 / (mx - mn) + 0.5);
+            if (b < 0) b = 0;
+            if (b > 255) b = 255;
+        }
+        hist[b] += 1;
+    }
+}
+
 /* R15: "Modified_FCM with Gaussian mixture model" is read as a
  * 1-D EM fit of a C-component Gaussian mixture on the 256-bin histogram
  * (bin b at level y_b = b/255), evenly spaced initialisation, <= max_iter EM
@@ -691,6 +744,41 @@ int orc_fcm_run(const double *x, long N, int C, double m, double eps, int max_it
  * gbest (lambda*, xi*) from the gbest's (U, c) -> argmax labels.
  * Parity unpinned end to end (only oracle-vs-GPU agreement); its parts are
  * pinned individually. */
+static int segment_core(const double *xin, const int64_t *histin, int nx, int ny, int nz, int C, double m,
+                        int q_mode, int v, double h, double eps, int max_iter, int P, int ring_k, int max_gen,
+                        int patience, double tol, double v0, double vmax, uint64_t seed, uint8_t *labels,
+                        double *U_out, double *c_out, double *lam_xi_out, double *J_out, int *gens_out,
+                        int *final_iters_out, double *c_init_out, int fitness_mode);
+
+/* dtype 0 u8, 1 u16, 2 f32 (pifcm_dtype): normalise + histogram by type, then
+ * the pipeline of orc_segment_u8. */
+int orc_segment_typed(const void *vol, int dtype, int nx, int ny, int nz, int C, double m, int q_mode,
+                      int v, double h, double eps, int max_iter,
+                      int P, int ring_k, int max_gen, int patience, double tol, double v0,
+                      double vmax, uint64_t seed,
+                      uint8_t *labels, double *U_out, double *c_out,
+                      double *lam_xi_out, double *J_out, int *gens_out, int *final_iters_out,
+                      double *c_init_out, int fitness_mode) {
+    const long N = (long)nx * ny * nz;
+    double *x = (double *)malloc(sizeof(double) * (size_t)N);
+    int64_t hist[256];
+    if (dtype == 1) {
+        orc_normalize_u16((const uint16_t *)vol, N, x);
+        orc_histogram_u16((const uint16_t *)vol, N, hist);
+    } else if (dtype == 2) {
+        orc_normalize_f32((const float *)vol, N, x);
+        orc_histogram_f32((const float *)vol, N, hist);
+    } else {
+        orc_normalize_u8((const uint8_t *)vol, N, x);
+        orc_histogram_u8((const uint8_t *)vol, N, hist);
+    }
+    const int r = segment_core(x, hist, nx, ny, nz, C, m, q_mode, v, h, eps, max_iter, P, ring_k, max_gen,
+                               patience, tol, v0, vmax, seed, labels, U_out, c_out, lam_xi_out, J_out, gens_out,
+                               final_iters_out, c_init_out, fitness_mode);
+    free(x);
+    return r;
+}
+
 int orc_segment_u8(const uint8_t *vol, int nx, int ny, int nz, int C, double m, int q_mode,
                    int v, double h, double eps, int max_iter,
                    int P, int ring_k, int max_gen, int patience, double tol, double v0,
@@ -698,14 +786,23 @@ int orc_segment_u8(const uint8_t *vol, int nx, int ny, int nz, int C, double m, 
                    uint8_t *labels, double *U_out /*[N][C] nullable*/, double *c_out /*[C]*/,
                    double *lam_xi_out /*[2]*/, double *J_out, int *gens_out, int *final_iters_out,
                    double *c_init_out /*[C] nullable: GMM centres*/, int fitness_mode) {
+    return orc_segment_typed(vol, 0, nx, ny, nz, C, m, q_mode, v, h, eps, max_iter, P, ring_k, max_gen, patience,
+                             tol, v0, vmax, seed, labels, U_out, c_out, lam_xi_out, J_out, gens_out,
+                             final_iters_out, c_init_out, fitness_mode);
+}
+
+static int segment_core(const double *xin, const int64_t *histin, int nx, int ny, int nz, int C, double m,
+                        int q_mode, int v, double h, double eps, int max_iter, int P, int ring_k, int max_gen,
+                        int patience, double tol, double v0, double vmax, uint64_t seed, uint8_t *labels,
+                        double *U_out, double *c_out, double *lam_xi_out, double *J_out, int *gens_out,
+                        int *final_iters_out, double *c_init_out, int fitness_mode) {
     const long N = (long)nx * ny * nz;
-    double *x = (double *)malloc(sizeof(double) * (size_t)N);
+    const double *x = xin;
     double *U = (double *)malloc(sizeof(double) * (size_t)N * C);
     double *Ub = (double *)malloc(sizeof(double) * (size_t)N * C);
     int64_t hist[256];
+    memcpy(hist, histin, sizeof hist);
     double c0[8], c1[8], cb[8], lx[2], Jb = 0.0;
-    orc_normalize_u8(vol, N, x);
-    orc_histogram_u8(vol, N, hist);
     orc_gmm_init(hist, C, 100, c0);
     if (c_init_out) memcpy(c_init_out, c0, sizeof(double) * C);
     orc_fcm_run(x, N, C, m, eps, max_iter, c0, U, c1);
@@ -723,6 +820,6 @@ int orc_segment_u8(const uint8_t *vol, int nx, int ny, int nz, int C, double m, 
     *J_out = Jb;
     *gens_out = gens;
     *final_iters_out = fi;
-    free(x); free(U); free(Ub);
+    free(U); free(Ub);
     return 0;
 }

@@ -20,6 +20,8 @@ FIT_ANCHORED = 1
 FIT_LEADER = 2
 ITER_CANONICAL = 1  # pifcm_iterate_ex flag
 U8 = 0
+U16 = 1
+F32 = 2
 
 
 class Grid(ct.Structure):
@@ -93,6 +95,7 @@ SIGNATURES = {
     "pifcm_pso_gbest_state": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, _vp]),
     "pifcm_pso_run": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, _vp, _vp, ct.c_size_t,
                                  ct.POINTER(PsoResult), _vp]),
+    "pifcm_normalize": (ct.c_int, [_vp, _G, _vp, ct.c_int32, _vp, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_normalize_u8": (ct.c_int, [_vp, _G, _vp, _vp, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_gmm_init": (ct.c_int, [_vp, ct.c_int32, _vp, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_argmax": (ct.c_int, [_vp, _G, ct.c_int32, _vp, _vp, _vp]),

@@ -59,6 +59,14 @@ class PsoConfig:
                            self.vmax, self.seed, self.fitness, self.p_begin, self.p_end)
 
 
+def dtype_code(vol: torch.Tensor) -> int:
+    """pifcm_dtype of a volume tensor (u8, uint16, float32)."""
+    codes = {torch.uint8: _abi.U8, torch.uint16: _abi.U16, torch.float32: _abi.F32}
+    if vol.dtype not in codes:
+        raise TypeError(f"volumes are uint8, uint16 or float32, not {vol.dtype}")
+    return codes[vol.dtype]
+
+
 def pitch_of(nx: int) -> int:
     return (nx + 3) // 4 * 4
 
@@ -252,15 +260,22 @@ class Context:
                           list(r.centers)[:cfg.C])
 
     # ------------------------------------------------------------ pipeline parts
-    def normalize_u8(self, vol: torch.Tensor, want_hist=True, stream=None):
+    def normalize(self, vol: torch.Tensor, want_hist=True, stream=None):
+        """pifcm_normalize: device u8 / uint16 / float32 volume [nz, ny, nx] ->
+        (x [nz, ny, pitch] f32, R15 histogram int64 [256] or None)."""
         nz, ny, nx = vol.shape
         g = _grid(nx, ny, nz)
         x = torch.empty((nz, ny, g.pitch), dtype=torch.float32, device=vol.device)
         hist = torch.empty(256, dtype=torch.int64, device=vol.device) if want_hist else None
         ws = torch.empty(256, dtype=torch.uint8, device=vol.device)
-        self._ck(self.lib.pifcm_normalize_u8(self._h, ct.byref(g), _ptr(vol), _ptr(x), _ptr(hist),
-                                             _ptr(ws), 256, _stream(stream)))
+        self._ck(self.lib.pifcm_normalize(self._h, ct.byref(g), _ptr(vol), dtype_code(vol), _ptr(x), _ptr(hist),
+                                          _ptr(ws), 256, _stream(stream)))
         return x, hist
+
+    def normalize_u8(self, vol: torch.Tensor, want_hist=True, stream=None):
+        if vol.dtype != torch.uint8:
+            raise TypeError("normalize_u8 takes a uint8 volume (see normalize)")
+        return self.normalize(vol, want_hist, stream)
 
     def gmm_init(self, hist: torch.Tensor, C: int, stream=None) -> torch.Tensor:
         c0 = torch.zeros(4, dtype=torch.float32, device=hist.device)
@@ -276,7 +291,8 @@ class Context:
     # ------------------------------------------------------------ pipeline
     def segment(self, vol: torch.Tensor, cfg: IfcmConfig, pso: PsoConfig, ws=None, want_U=False,
                 z_slice: int = -1, stream=None):
-        """pifcm_segment on a device u8 volume [nz, ny, nx] -> (labels, U or None, report)."""
+        """pifcm_segment on a device u8 / uint16 / float32 volume [nz, ny, nx]
+        -> (labels, U or None, report)."""
         nz, ny, nx = vol.shape
         if ws is None:
             ws = self.workspace(nx, ny, nz, cfg, pso)
@@ -286,7 +302,7 @@ class Context:
             labels = torch.empty((ny, nx), dtype=torch.uint8, device=vol.device)
         U = torch.empty((nz * ny * nx, 4), dtype=torch.float32, device=vol.device) if want_U else None
         rep = _abi.Report()
-        self._ck(self.lib.pifcm_segment(self._h, _ptr(vol), _abi.U8, nx, ny, nz, ct.byref(cfg.c()),
+        self._ck(self.lib.pifcm_segment(self._h, _ptr(vol), dtype_code(vol), nx, ny, nz, ct.byref(cfg.c()),
                                         ct.byref(pso.c()), z_slice, _ptr(ws), ws.numel(), _ptr(labels),
                                         _ptr(U), ct.byref(rep), _stream(stream)))
         return labels, U, report_dict(rep, cfg.C)

@@ -368,12 +368,27 @@ cudaError_t launch_gather_gbest(const float4 *slots, long long nvox, const int *
 }
 
 // ---------------------------------------------------------------- normalise
-// Alg. 2 step 1: global min / max of the u8 volume.
-__global__ void k_minmax_u8(const uint8_t *vol, long long n, unsigned int *mm) {
-    unsigned int lo = 255u, hi = 0u;
+// Alg. 2 step 1 for u8 / u16 / f32 volumes.
+// min / max are reduced as order-preserving 32-bit keys: the value itself for
+// the unsigned types, the sign-flipped bit pattern for floats.
+__device__ __forceinline__ unsigned key_of(uint8_t v) { return v; }
+__device__ __forceinline__ unsigned key_of(uint16_t v) { return v; }
+__device__ __forceinline__ unsigned key_of(float v) {
+    const unsigned b = __float_as_uint(v);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ double value_of_key(unsigned k, int dtype) {
+    if (dtype != PIFCM_F32) return (double)k;
+    const unsigned b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+    return (double)__uint_as_float(b);
+}
+
+template <typename T>
+__global__ void k_minmax(const T *vol, long long n, unsigned int *mm) {
+    unsigned int lo = 0xFFFFFFFFu, hi = 0u;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        const unsigned int v = vol[i];
+        const unsigned int v = key_of(vol[i]);
         lo = min(lo, v);
         hi = max(hi, v);
     }
@@ -388,23 +403,26 @@ __global__ void k_minmax_u8(const uint8_t *vol, long long n, unsigned int *mm) {
     }
 }
 __global__ void k_mm_reset(unsigned int *mm) {
-    mm[0] = 255u;
+    mm[0] = 0xFFFFFFFFu;
     mm[1] = 0u;
 }
-cudaError_t launch_minmax_u8(const uint8_t *vol, long long n, unsigned int *mm, cudaStream_t st) {
+template <typename T>
+static cudaError_t launch_minmax_t(const T *vol, long long n, unsigned int *mm, cudaStream_t st) {
     k_mm_reset<<<1, 1, 0, st>>>(mm);
     long long b = (n + 256 * 16 - 1) / (256 * 16);
     if (b > 148 * 8) b = 148 * 8;
     if (b < 1) b = 1;
-    k_minmax_u8<<<(int)b, 256, 0, st>>>(vol, n, mm);
+    k_minmax<T><<<(int)b, 256, 0, st>>>(vol, n, mm);
     return cudaGetLastError();
 }
 
-// x = (v - min) / (max - min) in IEEE fp32 (constant volume -> 0, R16), pitched rows.
-__global__ void k_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int pitch,
-                               const unsigned int *mm, float *x) {
-    const int lo = (int)mm[0], hi = (int)mm[1];
-    const float rng = (float)(hi - lo);
+// x = (v - min) / (max - min), constant volume -> 0 (R16), pitched rows.
+// u8 / u16: exact integer differences, one correctly rounded fp32 division;
+// f32: the quotient in fp64, rounded once to fp32.
+template <typename T>
+__global__ void k_normalize(const T *vol, int nx, int ny, int nz, int pitch, const unsigned int *mm, float *x,
+                            int dtype) {
+    const double lo = value_of_key(mm[0], dtype), hi = value_of_key(mm[1], dtype);
     const long long rows = (long long)ny * nz;
     const long long n = rows * pitch;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
@@ -412,26 +430,38 @@ __global__ void k_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int p
         const long long row = e / pitch;
         const int X = (int)(e - row * pitch);
         float v = 0.f;
-        if (X < nx && hi > lo) v = __fdiv_rn((float)((int)vol[row * nx + X] - lo), rng);
+        if (X < nx && hi > lo) {
+            const T t = vol[row * nx + X];
+            if (dtype == PIFCM_F32)
+                v = (float)(((double)t - lo) / (hi - lo));
+            else
+                v = __fdiv_rn((float)((int)t - (int)lo), (float)((int)hi - (int)lo));
+        }
         x[e] = v;
     }
 }
-cudaError_t launch_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int pitch,
-                                const unsigned int *mm, float *x, cudaStream_t st) {
-    k_normalize_u8<<<148 * 8, 256, 0, st>>>(vol, nx, ny, nz, pitch, mm, x);
-    return cudaGetLastError();
-}
 
-// R15: 256-bin histogram in integers, bin = ((v-min)*255 + (max-min)/2) / (max-min).
-__global__ void k_hist_u8(const uint8_t *vol, long long n, const unsigned int *mm, int64_t *hist) {
+// R15: 256-bin histogram.  u8 / u16 in integers:
+// bin = ((v-min)*255 + (max-min)/2) / (max-min); f32 in fp64:
+// bin = floor((v-min)*255/(max-min) + 0.5) (the oracle's arithmetic).
+template <typename T>
+__global__ void k_hist(const T *vol, long long n, const unsigned int *mm, int64_t *hist, int dtype) {
     __shared__ unsigned int h[256];
     for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0u;
     __syncthreads();
-    const int lo = (int)mm[0], rng = (int)mm[1] - (int)mm[0];
+    const double lo = value_of_key(mm[0], dtype), hi = value_of_key(mm[1], dtype);
+    const long long ilo = (long long)lo, irng = (long long)hi - (long long)lo;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         int b = 0;
-        if (rng > 0) b = (((int)vol[i] - lo) * 255 + rng / 2) / rng;
+        if (hi > lo) {
+            if (dtype == PIFCM_F32) {
+                b = (int)floor(((double)vol[i] - lo) * 255.0 / (hi - lo) + 0.5);
+                b = min(max(b, 0), 255);
+            } else {
+                b = (int)((((long long)vol[i] - ilo) * 255 + irng / 2) / irng);
+            }
+        }
         atomicAdd(&h[b], 1u);
     }
     __syncthreads();
@@ -441,14 +471,49 @@ __global__ void k_hist_u8(const uint8_t *vol, long long n, const unsigned int *m
 __global__ void k_zero_i64(int64_t *p, int n) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
 }
-cudaError_t launch_hist_u8(const uint8_t *vol, long long n, const unsigned int *mm,
-                           int64_t *hist, cudaStream_t st) {
+
+cudaError_t launch_minmax(const void *vol, int dtype, long long n, unsigned int *mm, cudaStream_t st) {
+    switch (dtype) {
+        case PIFCM_U8: return launch_minmax_t(static_cast<const uint8_t *>(vol), n, mm, st);
+        case PIFCM_U16: return launch_minmax_t(static_cast<const uint16_t *>(vol), n, mm, st);
+        case PIFCM_F32: return launch_minmax_t(static_cast<const float *>(vol), n, mm, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+cudaError_t launch_normalize(const void *vol, int dtype, int nx, int ny, int nz, int pitch,
+                             const unsigned int *mm, float *x, cudaStream_t st) {
+    switch (dtype) {
+        case PIFCM_U8: k_normalize<<<148 * 8, 256, 0, st>>>(static_cast<const uint8_t *>(vol), nx, ny, nz, pitch, mm, x, dtype); break;
+        case PIFCM_U16: k_normalize<<<148 * 8, 256, 0, st>>>(static_cast<const uint16_t *>(vol), nx, ny, nz, pitch, mm, x, dtype); break;
+        case PIFCM_F32: k_normalize<<<148 * 8, 256, 0, st>>>(static_cast<const float *>(vol), nx, ny, nz, pitch, mm, x, dtype); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+cudaError_t launch_hist(const void *vol, int dtype, long long n, const unsigned int *mm, int64_t *hist,
+                        cudaStream_t st) {
     k_zero_i64<<<1, 256, 0, st>>>(hist, 256);
     long long b = (n + 256 * 32 - 1) / (256 * 32);
     if (b > 148 * 4) b = 148 * 4;
     if (b < 1) b = 1;
-    k_hist_u8<<<(int)b, 256, 0, st>>>(vol, n, mm, hist);
+    switch (dtype) {
+        case PIFCM_U8: k_hist<<<(int)b, 256, 0, st>>>(static_cast<const uint8_t *>(vol), n, mm, hist, dtype); break;
+        case PIFCM_U16: k_hist<<<(int)b, 256, 0, st>>>(static_cast<const uint16_t *>(vol), n, mm, hist, dtype); break;
+        case PIFCM_F32: k_hist<<<(int)b, 256, 0, st>>>(static_cast<const float *>(vol), n, mm, hist, dtype); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
+}
+cudaError_t launch_minmax_u8(const uint8_t *vol, long long n, unsigned int *mm, cudaStream_t st) {
+    return launch_minmax(vol, PIFCM_U8, n, mm, st);
+}
+cudaError_t launch_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int pitch, const unsigned int *mm,
+                                float *x, cudaStream_t st) {
+    return launch_normalize(vol, PIFCM_U8, nx, ny, nz, pitch, mm, x, st);
+}
+cudaError_t launch_hist_u8(const uint8_t *vol, long long n, const unsigned int *mm, int64_t *hist,
+                           cudaStream_t st) {
+    return launch_hist(vol, PIFCM_U8, n, mm, hist, st);
 }
 
 // ---------------------------------------------------------------- GMM start

@@ -626,20 +626,27 @@ int pifcm_pso_run(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
 }
 
 // ============================================================== ABI: pipeline parts
-int pifcm_normalize_u8(pifcm_ctx *ctx, const pifcm_grid *grid, const uint8_t *vol, float *x, int64_t *hist,
-                       void *ws, size_t ws_bytes, pifcm_stream stream) {
+int pifcm_normalize(pifcm_ctx *ctx, const pifcm_grid *grid, const void *vol, int32_t dtype, float *x,
+                    int64_t *hist, void *ws, size_t ws_bytes, pifcm_stream stream) {
     if (!ctx) return PIFCM_EINVAL;
     int r;
     if ((r = check_grid(ctx, grid))) return r;
     if (!vol || !x) return fail(ctx, PIFCM_EINVAL, "vol and x must be non-NULL");
+    if (dtype != PIFCM_U8 && dtype != PIFCM_U16 && dtype != PIFCM_F32)
+        return fail(ctx, PIFCM_EINVAL, "dtype %d unknown", dtype);
     if (!ws || ws_bytes < 256) return fail(ctx, PIFCM_ENOMEM, "normalize needs >= 256 bytes of workspace");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const long long n = (long long)grid->nx * grid->ny * grid->nz;
     unsigned int *mm = static_cast<unsigned int *>(ws);
-    LAUNCH(ctx, 2, launch_minmax_u8(vol, n, mm, st));
-    LAUNCH(ctx, 1, launch_normalize_u8(vol, grid->nx, grid->ny, grid->nz, grid->pitch, mm, x, st));
-    if (hist) LAUNCH(ctx, 2, launch_hist_u8(vol, n, mm, hist, st));
+    LAUNCH(ctx, 2, launch_minmax(vol, dtype, n, mm, st));
+    LAUNCH(ctx, 1, launch_normalize(vol, dtype, grid->nx, grid->ny, grid->nz, grid->pitch, mm, x, st));
+    if (hist) LAUNCH(ctx, 2, launch_hist(vol, dtype, n, mm, hist, st));
     return PIFCM_OK;
+}
+
+int pifcm_normalize_u8(pifcm_ctx *ctx, const pifcm_grid *grid, const uint8_t *vol, float *x, int64_t *hist,
+                       void *ws, size_t ws_bytes, pifcm_stream stream) {
+    return pifcm_normalize(ctx, grid, vol, PIFCM_U8, x, hist, ws, ws_bytes, stream);
 }
 
 int pifcm_gmm_init(pifcm_ctx *ctx, int32_t C, const int64_t *hist, float *c0, void *ws, size_t ws_bytes,
@@ -707,7 +714,8 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
                   const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso, int32_t z_slice, void *ws,
                   size_t ws_bytes, uint8_t *labels, float *U_out, pifcm_report *rep, pifcm_stream stream) {
     if (!ctx) return PIFCM_EINVAL;
-    if (dtype != PIFCM_U8) return fail(ctx, PIFCM_EINVAL, "only PIFCM_U8 volumes are supported");
+    if (dtype != PIFCM_U8 && dtype != PIFCM_U16 && dtype != PIFCM_F32)
+        return fail(ctx, PIFCM_EINVAL, "dtype %d unknown", dtype);
     if (!vol || !labels) return fail(ctx, PIFCM_EINVAL, "vol and labels must be non-NULL");
     pifcm_grid g{nx, ny, nz, (nx + 3) / 4 * 4};
     Layout L;
@@ -731,11 +739,11 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     float *cent = s.centers;  // [Pl][4]; entry 0 reused by the FCM start and the final IFCM
     CK(ctx, cudaEventRecord(ev[0], st));
     // Alg. 2 step 1: normalise (+ histogram for the GMM start)
-    const uint8_t *v8 = static_cast<const uint8_t *>(vol);
+
     unsigned int *mm = at<unsigned int>(ws, L.mm);
-    LAUNCH(ctx, 2, launch_minmax_u8(v8, L.nvox, mm, st));
-    LAUNCH(ctx, 1, launch_normalize_u8(v8, nx, ny, nz, g.pitch, mm, x, st));
-    LAUNCH(ctx, 2, launch_hist_u8(v8, L.nvox, mm, hist, st));
+    LAUNCH(ctx, 2, launch_minmax(vol, dtype, L.nvox, mm, st));
+    LAUNCH(ctx, 1, launch_normalize(vol, dtype, nx, ny, nz, g.pitch, mm, x, st));
+    LAUNCH(ctx, 2, launch_hist(vol, dtype, L.nvox, mm, hist, st));
     CK(ctx, cudaEventRecord(ev[1], st));
     // Alg. 1 step 2: GMM centres, then FCM (lambda = xi = 0) until eps
     LAUNCH(ctx, 1, launch_gmm(hist, cfg->C, 100, c0, st));

@@ -148,6 +148,11 @@ cudaError_t launch_fixup_copy(const float4 *scratch, float4 *out, long long nvox
 cudaError_t launch_pso_init(SwarmDev s, int P, int Pl, int p0, double v0, uint32_t k0,
                             uint32_t k1, const float *c0, int nslots, cudaStream_t st);
 cudaError_t launch_pso_update(const PsoUpdateArgs &a, cudaStream_t st);
+cudaError_t launch_minmax(const void *vol, int dtype, long long n, unsigned int *mm, cudaStream_t st);
+cudaError_t launch_normalize(const void *vol, int dtype, int nx, int ny, int nz, int pitch,
+                             const unsigned int *mm, float *x, cudaStream_t st);
+cudaError_t launch_hist(const void *vol, int dtype, long long n, const unsigned int *mm, int64_t *hist,
+                        cudaStream_t st);
 cudaError_t launch_minmax_u8(const uint8_t *vol, long long n, unsigned int *mm, cudaStream_t st);
 cudaError_t launch_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int pitch,
                                 const unsigned int *mm, float *x, cudaStream_t st);

@@ -707,6 +707,8 @@ class SlabSegmenter:
         """vol: the whole u8 volume [nz][ny][nx] (any device); each rank reads
         its slab planes."""
         ctx, cfg, g, d = self.ctx, self.cfg, self.geo, self.dist
+        if vol.dtype != torch.uint8:
+            raise TypeError("the z-slab pipeline takes uint8 volumes")
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
         # Alg. 2 step 1: global min-max (all-reduce) and the R15 histogram

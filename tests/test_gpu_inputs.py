@@ -1,0 +1,71 @@
+"""Alg. 2 step 1 for every input type of SURVEY 8(a) a0 (u8, u16, f32):
+normalisation and R15 histogram against the oracle, and the whole pipeline
+on 16-bit and float volumes."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2002_01981_b200 import Context
+    return Context(0)
+
+
+def _volumes(shape, seed):
+    g = np.random.default_rng(seed)
+    v8 = g.integers(3, 250, size=shape, dtype=np.uint8)
+    v16 = g.integers(100, 60000, size=shape).astype(np.uint16)
+    f = (g.normal(size=shape) * 3.0 - 1.0).astype(np.float32)
+    return {"u8": v8, "u16": v16, "f32": f}
+
+
+@pytest.mark.parametrize("shape,seed", [((1, 7, 9), 1), ((5, 33, 34), 2), ((17, 20, 65), 3), ((1, 1, 1), 4)])
+def test_normalize_and_histogram_typed(ctx, orc, shape, seed):
+    for name, v in _volumes(shape, seed).items():
+        x, hist = ctx.normalize(torch.as_tensor(v, device="cuda:0"))
+        xg = x[..., : shape[2]].cpu().numpy()
+        xo = orc.normalize(v)
+        if name == "f32":
+            assert (xg == xo.astype(np.float32)).all(), name  # one rounding of the fp64 quotient
+        else:
+            ulp = np.spacing(xo.astype(np.float32))
+            assert (np.abs(xg - xo) <= ulp).all(), name
+        assert (x[..., shape[2]:] == 0).all()
+        assert (hist.cpu().numpy() == orc.histogram(v)).all(), name
+
+
+def test_segment_u16_equals_u8(ctx):
+    """A 16-bit volume 257 * v8 normalises to the same x, so the whole
+    pipeline gives the same labels, (lambda*, xi*) and centres."""
+    from inputs import add_noise_u8, cube_phantom
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    img, _ = cube_phantom(28, 24, 10, (0.1, 0.35, 0.65, 0.9))
+    v8 = add_noise_u8(img, 7.0, 4)
+    cfg, pso = IfcmConfig(C=4), PsoConfig(P=5, max_gen=3, patience=0, seed=8)
+    la, _, ra = ctx.segment(torch.as_tensor(v8, device="cuda:0"), cfg, pso)
+    lb, _, rb = ctx.segment(torch.as_tensor(v8.astype(np.uint16) * 257, device="cuda:0"), cfg, pso)
+    assert (la == lb).all()
+    for k in ("lambda", "xi", "J", "centers", "c_init", "fcm_iters", "final_iters"):
+        assert ra[k] == rb[k], k
+
+
+def test_segment_f32_parity(ctx, orc):
+    """A float volume through the pipeline against the oracle's typed
+    pipeline: same GMM start (1e-6), same PSO trajectory, labels >= 99.9 %
+    where the final IFCM is well conditioned."""
+    from inputs import cube_phantom
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    img, _ = cube_phantom(30, 26, 12, (0.1, 0.35, 0.65, 0.9))
+    g = np.random.default_rng(3)
+    vol = (img * 1000.0 + g.normal(size=img.shape) * 60.0).astype(np.float32)
+    cfg, pso = IfcmConfig(C=4), PsoConfig(P=6, max_gen=2, patience=0, seed=1)
+    lab, _, rep = ctx.segment(torch.as_tensor(vol, device="cuda:0"), cfg, pso)
+    r = orc.segment_u8(vol, C=4, P=6, max_gen=2, seed=1)
+    assert np.abs(np.array(rep["c_init"]) - r.c_init).max() < 1e-6
+    assert rep["lambda"] == r.lam and rep["xi"] == r.xi
+    if min(r.lam, r.xi) > 0.95:
+        pytest.skip(f"ill-conditioned final IFCM at lambda*={r.lam:.3f}, xi*={r.xi:.3f}")
+    assert (lab.cpu().numpy() == r.labels).mean() >= 0.999

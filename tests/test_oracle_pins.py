@@ -254,6 +254,31 @@ def test_shells_reduce_to_single_shell(orc):
     assert np.abs(np.array(a[0]) - np.array(b[0])).max() < 1e-14 and abs(a[2] - b[2]) < 1e-14
 
 
+# --------------------------------------------------------------------------- input types (a0)
+def test_typed_normalize_and_histogram(orc):
+    """u16 = 257 * u8 normalises and bins exactly like the u8 volume (the
+    integer formula scales); f32 closed forms: min -> 0, max -> 1, constant ->
+    0 / bin 0, a value at k/255 of the range -> bin k, affine invariance."""
+    from inputs import add_noise_u8, cube_phantom
+    img, _ = cube_phantom(11, 9, 4, (0.1, 0.5, 0.9))
+    v8 = add_noise_u8(img, 9.0, 12)
+    v16 = v8.astype(np.uint16) * 257
+    assert (orc.normalize(v16) == orc.normalize(v8)).all()
+    assert (orc.histogram(v16) == orc.histogram(v8)).all()
+    g = np.random.default_rng(5)
+    f = (g.random((3, 5, 7)) * 10 - 3).astype(np.float32)
+    x = orc.normalize(f)
+    assert x.min() == 0.0 and x.max() == 1.0
+    assert np.abs(orc.normalize(f * np.float32(4) + np.float32(2)) - x).max() < 1e-6
+    lo, hi = float(f.min()), float(f.max())
+    probe = np.array([lo, hi] + [lo + (hi - lo) * k / 255 for k in (1, 17, 128, 254)], np.float32).reshape(1, 1, -1)
+    h = orc.histogram(np.concatenate([probe, probe], axis=2))
+    for k in (0, 255, 1, 17, 128, 254):
+        assert h[k] == 2, (k, h[k])
+    c = np.full((2, 3, 4), 7.5, np.float32)
+    assert (orc.normalize(c) == 0).all() and orc.histogram(c)[0] == c.size
+
+
 # --------------------------------------------------------------------------- invariants
 def _rand_case(seed, shape=(3, 7, 6), C=3):
     from inputs import random_state
