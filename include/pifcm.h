@@ -280,6 +280,36 @@ int pifcm_normalize(pifcm_ctx *ctx, const pifcm_grid *grid, const void *vol, int
 int pifcm_gmm_init(pifcm_ctx *ctx, int32_t C, const int64_t *hist, float *c0, void *ws,
                    size_t ws_bytes, pifcm_stream stream);
 
+/* The FCM start of a quantised volume on its value histogram (
+ * Alg. 1 step 2; Alg. 2 step 5; DESIGN R24).  FCM is the
+ * IFCM step at lambda = xi = 0, where Eq. 4's factor is 1 and a voxel's Eq. 2
+ * row depends on its x and the centres only, so the Eq. 3 / Eq. 1 sums over
+ * voxels are the count-weighted sums over the distinct values.
+ *   pifcm_value_hist: counts[v] += number of voxels of raw value v among the
+ *     n values at vol (dev; dtype PIFCM_U8 -> 256 entries, PIFCM_U16 -> 65536
+ *     entries, dev int64, zeroed by the caller; a z-slab caller sums the
+ *     ranks' counts).  PIFCM_EINVAL for PIFCM_F32.  Async.
+ *   pifcm_fcm_hist: FCM iterations from the centres c0 (dev fp32 [4]) on the
+ *     counts of a volume with raw range mm (dev uint32 {min, max}, as
+ *     pifcm_minmax_u8 / pifcm_normalize write it) until max|du| < cfg->eps
+ *     (the first iteration never stops, R14) or cfg->max_iter.  Writes c_prev
+ *     (dev fp32 [4]: the centres the last iteration's memberships used),
+ *     c_out (dev fp32 [4]: Eq. 3 centres after it) and stats (dev fp64 [4]:
+ *     {J, max|du|, iterations, converged}).  ws: >= the size
+ *     pifcm_fcm_hist_workspace_size gives for dtype (device, 256-B aligned).
+ *     Async; a non-finite J sets the status read by the next sync call.
+ *   pifcm_fcm_memberships: U (dev fp32 [nz][ny][nx][4]) = the Eq. 2 rows of
+ *     x (dev [nz][ny][pitch]) at the centres c (dev [4]) with lambda = xi = 0:
+ *     with c = c_prev, the memberships of the FCM start.  Async. */
+int pifcm_value_hist(pifcm_ctx *ctx, const void *vol, int32_t dtype, int64_t n, int64_t *counts,
+                     pifcm_stream stream);
+int pifcm_fcm_hist_workspace_size(int32_t dtype, size_t *bytes);
+int pifcm_fcm_hist(pifcm_ctx *ctx, const pifcm_ifcm_cfg *cfg, int32_t dtype, const uint32_t *mm,
+                   const int64_t *counts, const float *c0, float *c_prev, float *c_out, double *stats, void *ws,
+                   size_t ws_bytes, pifcm_stream stream);
+int pifcm_fcm_memberships(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, float m, const float *x,
+                          const float *c, float *U, pifcm_stream stream);
+
 /* Defuzzification (R13): labels = argmax_j u_ij, ties to the
  * lowest j.  U dev fp32 [nz][ny][nx][4], labels dev u8.  Async. */
 int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float *U,

@@ -260,17 +260,58 @@ class Context:
                           list(r.centers)[:cfg.C])
 
     # ------------------------------------------------------------ pipeline parts
-    def normalize(self, vol: torch.Tensor, want_hist=True, stream=None):
+    def normalize(self, vol: torch.Tensor, want_hist=True, stream=None, mm=None):
         """pifcm_normalize: device u8 / uint16 / float32 volume [nz, ny, nx] ->
-        (x [nz, ny, pitch] f32, R15 histogram int64 [256] or None)."""
+        (x [nz, ny, pitch] f32, R15 histogram int64 [256] or None).
+        mm (optional device int32 tensor of >= 64 elements) receives the raw
+        {min, max} in its first two entries (pifcm_fcm_hist's range)."""
         nz, ny, nx = vol.shape
         g = _grid(nx, ny, nz)
         x = torch.empty((nz, ny, g.pitch), dtype=torch.float32, device=vol.device)
         hist = torch.empty(256, dtype=torch.int64, device=vol.device) if want_hist else None
-        ws = torch.empty(256, dtype=torch.uint8, device=vol.device)
+        ws = torch.empty(256, dtype=torch.uint8, device=vol.device) if mm is None else mm
+        if ws.numel() * ws.element_size() < 256:
+            raise ValueError("mm must hold >= 256 bytes")
         self._ck(self.lib.pifcm_normalize(self._h, ct.byref(g), _ptr(vol), dtype_code(vol), _ptr(x), _ptr(hist),
                                           _ptr(ws), 256, _stream(stream)))
         return x, hist
+
+    # --------------------------------------- FCM start on the value histogram
+    def value_hist(self, vol: torch.Tensor, counts: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """pifcm_value_hist: counts[v] += voxels of raw value v (uint8 -> 256,
+        uint16 -> 65536 entries, int64).  A new zeroed tensor if counts is None."""
+        code = dtype_code(vol)
+        if counts is None:
+            counts = torch.zeros(256 if code == _abi.U8 else 65536, dtype=torch.int64, device=vol.device)
+        self._ck(self.lib.pifcm_value_hist(self._h, _ptr(vol), code, vol.numel(), _ptr(counts), _stream(stream)))
+        return counts
+
+    def fcm_hist(self, counts: torch.Tensor, mm: torch.Tensor, c0: torch.Tensor, cfg: IfcmConfig, stream=None):
+        """pifcm_fcm_hist -> (c_prev [4], c_out [4], stats [4] = {J, du, iters, converged}),
+        all device tensors."""
+        code = _abi.U8 if counts.numel() == 256 else _abi.U16
+        n = ct.c_size_t()
+        self._ck(self.lib.pifcm_fcm_hist_workspace_size(code, ct.byref(n)))
+        ws = torch.empty(n.value, dtype=torch.uint8, device=counts.device)
+        c_prev = torch.zeros(4, dtype=torch.float32, device=counts.device)
+        c_out = torch.zeros(4, dtype=torch.float32, device=counts.device)
+        stats = torch.zeros(4, dtype=torch.float64, device=counts.device)
+        self._ck(self.lib.pifcm_fcm_hist(self._h, ct.byref(cfg.c()), code, _ptr(mm), _ptr(counts), _ptr(c0),
+                                         _ptr(c_prev), _ptr(c_out), _ptr(stats), _ptr(ws), n.value,
+                                         _stream(stream)))
+        return c_prev, c_out, stats
+
+    def fcm_memberships(self, x: torch.Tensor, c: torch.Tensor, C: int, m: float, nx: int,
+                        U: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """pifcm_fcm_memberships: U [nz*ny*nx, 4] = Eq. 2 rows of x (pitched
+        [nz, ny, pitch]) at the centres c with lambda = xi = 0."""
+        nz, ny, pitch = x.shape
+        if U is None:
+            U = torch.empty((nz * ny * nx, 4), dtype=torch.float32, device=x.device)
+        g = _grid(nx, ny, nz, pitch)
+        self._ck(self.lib.pifcm_fcm_memberships(self._h, ct.byref(g), C, m, _ptr(x), _ptr(c), _ptr(U),
+                                                _stream(stream)))
+        return U
 
     def normalize_u8(self, vol: torch.Tensor, want_hist=True, stream=None):
         if vol.dtype != torch.uint8:

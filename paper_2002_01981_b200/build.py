@@ -48,12 +48,17 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    # per object: recompile when the object is missing or older than its
+    # source, any header or this script (headers are not tracked per source)
+    hdr_t = max([os.path.getmtime(f) for f in headers()] + [os.path.getmtime(__file__)])
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
+            continue
         cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-Xptxas", "-v" if verbose else "-O3",
                "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
-        objs.append(obj)
     for src, p in procs:
         out, _ = p.communicate()
         if p.returncode != 0:

@@ -435,7 +435,7 @@ __global__ void k_normalize(const T *vol, int nx, int ny, int nz, int pitch, con
             if (dtype == PIFCM_F32)
                 v = (float)(((double)t - lo) / (hi - lo));
             else
-                v = __fdiv_rn((float)((int)t - (int)lo), (float)((int)hi - (int)lo));
+                v = normalize_q((int)t, (int)lo, (int)hi);
         }
         x[e] = v;
     }

@@ -117,10 +117,27 @@ void prange(const pifcm_pso_cfg *p, int *p0, int *pl) {
     else { *p0 = p->p_begin; *pl = p->p_end - p->p_begin; }
 }
 
+// Scratch of the value-histogram FCM: x, count and previous row per value.
+size_t fcm_hist_ws_bytes(int nvals) {
+    return align_up(sizeof(float) * nvals, 256) + align_up(sizeof(double) * nvals, 256) +
+           align_up(sizeof(float4) * nvals, 256);
+}
+FcmHistArgs fcm_hist_args(void *ws, int nvals) {
+    FcmHistArgs a{};
+    char *b = static_cast<char *>(ws);
+    a.nvals = nvals;
+    a.xs = reinterpret_cast<float *>(b);
+    b += align_up(sizeof(float) * nvals, 256);
+    a.ns = reinterpret_cast<double *>(b);
+    b += align_up(sizeof(double) * nvals, 256);
+    a.up = reinterpret_cast<float4 *>(b);
+    return a;
+}
+
 // Workspace layout (all offsets 256-byte aligned).
 struct Layout {
     size_t x, vol, lab, hist, mm, c0, slots, hdr, dhdr, pos, vel, pbf, pbx, fit, evalpos, cur, nxt,
-        gbc, cent, part, stats, lamxi, cnt, hf, shc, total;
+        gbc, cent, part, stats, lamxi, cnt, hf, shc, vcnt, fhws, cprev, fstats, total;
     int nslots, P, Pl, p0, nblk, mode;
     long long nvox;
 };
@@ -169,6 +186,11 @@ Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg 
     L.cnt = take(sizeof(unsigned) * (Pl > 1 ? Pl : 1));
     L.hf = L.mode == PIFCM_FIT_CHAINED ? take(0) : take(sizeof(float4) * 2 * (size_t)L.nvox);
     L.shc = take(sizeof(float) * 4);
+    // the FCM start on the value histogram (any quantised dtype)
+    L.vcnt = take(sizeof(int64_t) * 65536);
+    L.fhws = take(fcm_hist_ws_bytes(65536));
+    L.cprev = take(sizeof(float) * 4);
+    L.fstats = take(sizeof(double) * 4);
     L.total = o;
     return L;
 }
@@ -659,6 +681,58 @@ int pifcm_gmm_init(pifcm_ctx *ctx, int32_t C, const int64_t *hist, float *c0, vo
     return PIFCM_OK;
 }
 
+int pifcm_value_hist(pifcm_ctx *ctx, const void *vol, int32_t dtype, int64_t n, int64_t *counts,
+                     pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    if (dtype != PIFCM_U8 && dtype != PIFCM_U16)
+        return fail(ctx, PIFCM_EINVAL, "value histogram of dtype %d: only PIFCM_U8 / PIFCM_U16", dtype);
+    if (n < 0) return fail(ctx, PIFCM_EINVAL, "n = %lld < 0", (long long)n);
+    if (n > 0 && (!vol || !counts)) return fail(ctx, PIFCM_EINVAL, "vol and counts must be non-NULL");
+    if (n == 0) return PIFCM_OK;
+    LAUNCH(ctx, 1, launch_value_hist(vol, dtype, n, counts, reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_fcm_hist_workspace_size(int32_t dtype, size_t *bytes) {
+    if (!bytes || (dtype != PIFCM_U8 && dtype != PIFCM_U16)) return PIFCM_EINVAL;
+    *bytes = fcm_hist_ws_bytes(dtype == PIFCM_U8 ? 256 : 65536);
+    return PIFCM_OK;
+}
+
+int pifcm_fcm_hist(pifcm_ctx *ctx, const pifcm_ifcm_cfg *cfg, int32_t dtype, const uint32_t *mm,
+                   const int64_t *counts, const float *c0, float *c_prev, float *c_out, double *stats, void *ws,
+                   size_t ws_bytes, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if (!cfg) return fail(ctx, PIFCM_EINVAL, "cfg must be non-NULL");
+    if ((r = check_cfg(ctx, cfg))) return r;
+    if (dtype != PIFCM_U8 && dtype != PIFCM_U16)
+        return fail(ctx, PIFCM_EINVAL, "value-histogram FCM of dtype %d: only PIFCM_U8 / PIFCM_U16", dtype);
+    if (!mm || !counts || !c0 || !c_prev || !c_out || !stats)
+        return fail(ctx, PIFCM_EINVAL, "mm, counts, c0, c_prev, c_out and stats must be non-NULL");
+    const int nvals = dtype == PIFCM_U8 ? 256 : 65536;
+    if ((r = check_ws(ctx, ws, ws_bytes, fcm_hist_ws_bytes(nvals)))) return r;
+    FcmHistArgs fa = fcm_hist_args(ws, nvals);
+    fa.counts = counts; fa.mm = mm; fa.c0 = c0; fa.max_iter = cfg->max_iter; fa.eps = cfg->eps;
+    fa.m = cfg->m; fa.inv_m1 = 1.0f / (cfg->m - 1.0f); fa.c_prev = c_prev; fa.c_out = c_out; fa.stats = stats;
+    fa.status = nullptr;
+    LAUNCH(ctx, 1, launch_fcm_hist(fa, cfg->C, cfg->m == 2.0f, reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_fcm_memberships(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, float m, const float *x,
+                          const float *c, float *U, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    int r;
+    if ((r = check_grid(ctx, grid))) return r;
+    if (C < 2 || C > kMaxC) return fail(ctx, PIFCM_EINVAL, "C = %d outside [2, 4]", C);
+    if (!(m > 1.0f)) return fail(ctx, PIFCM_EINVAL, "m = %g must be > 1", (double)m);
+    if (!x || !c || !U) return fail(ctx, PIFCM_EINVAL, "x, c and U must be non-NULL");
+    LAUNCH(ctx, 1, launch_fcm_memberships(x, grid->nx, grid->ny, grid->nz, (int)grid->pitch, c, C, m,
+                                          reinterpret_cast<float4 *>(U), reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
 int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float *U, uint8_t *labels,
                  pifcm_stream stream) {
     if (!ctx) return PIFCM_EINVAL;
@@ -754,13 +828,29 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     CK(ctx, cudaMemsetAsync(s.hdr, 0, sizeof(int) * 16, st));
     CK(ctx, cudaMemsetAsync(at<unsigned>(ws, L.cnt), 0, sizeof(unsigned) * (L.Pl > 1 ? L.Pl : 1), st));
     int fcm_slot = 0, fcm_iters = 0;
-    if ((r = run_until(ctx, &g, cfg, x, slots, L.nvox, 1, 0, cent, lamxi, false, true, partials, stats, status,
-                       at<unsigned>(ws, L.cnt), st, &fcm_slot, &fcm_iters)))
-        return r;
-    // keep the FCM result in slot 0 (the PSO start slot)
-    if (fcm_slot != 0)
-        CK(ctx, cudaMemcpyAsync(slots, slots + (long long)fcm_slot * L.nvox, sizeof(float4) * (size_t)L.nvox,
-                                cudaMemcpyDeviceToDevice, st));
+    const bool vh = dtype != PIFCM_F32;
+    if (vh) {
+        // quantised input: the FCM loop on the value histogram (R24), then
+        // the memberships of every voxel once, into slot 0 (the PSO start)
+        const int nvals = dtype == PIFCM_U8 ? 256 : 65536;
+        int64_t *vcnt = at<int64_t>(ws, L.vcnt);
+        CK(ctx, cudaMemsetAsync(vcnt, 0, sizeof(int64_t) * nvals, st));
+        LAUNCH(ctx, 1, launch_value_hist(vol, dtype, L.nvox, vcnt, st));
+        FcmHistArgs fa = fcm_hist_args(at<void>(ws, L.fhws), nvals);
+        fa.counts = vcnt; fa.mm = mm; fa.c0 = c0; fa.max_iter = cfg->max_iter; fa.eps = cfg->eps;
+        fa.m = cfg->m; fa.inv_m1 = 1.0f / (cfg->m - 1.0f); fa.c_prev = at<float>(ws, L.cprev);
+        fa.c_out = cent; fa.stats = at<double>(ws, L.fstats); fa.status = status;
+        LAUNCH(ctx, 1, launch_fcm_hist(fa, cfg->C, cfg->m == 2.0f, st));
+        LAUNCH(ctx, 1, launch_fcm_memberships(x, nx, ny, nz, g.pitch, fa.c_prev, cfg->C, cfg->m, slots, st));
+    } else {
+        if ((r = run_until(ctx, &g, cfg, x, slots, L.nvox, 1, 0, cent, lamxi, false, true, partials, stats, status,
+                           at<unsigned>(ws, L.cnt), st, &fcm_slot, &fcm_iters)))
+            return r;
+        // keep the FCM result in slot 0 (the PSO start slot)
+        if (fcm_slot != 0)
+            CK(ctx, cudaMemcpyAsync(slots, slots + (long long)fcm_slot * L.nvox, sizeof(float4) * (size_t)L.nvox,
+                                    cudaMemcpyDeviceToDevice, st));
+    }
     CK(ctx, cudaMemcpyAsync(c0, cent, sizeof(float) * 4, cudaMemcpyDeviceToDevice, st));
     CK(ctx, cudaEventRecord(ev[2], st));
     // Alg. 1 steps 3-10: PSO (c0 now holds the FCM centres for pso_init)
@@ -797,8 +887,11 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     int stat = 0;
     CK(ctx, cudaMemcpyAsync(cfin, cent, sizeof cfin, cudaMemcpyDeviceToHost, st));
     CK(ctx, cudaMemcpyAsync(&stat, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    double fst[4] = {0.0, 0.0, 0.0, 0.0};
+    if (vh) CK(ctx, cudaMemcpyAsync(fst, at<double>(ws, L.fstats), sizeof fst, cudaMemcpyDeviceToHost, st));
     CK(ctx, cudaStreamSynchronize(st));
     CK(ctx, cudaGetLastError());
+    if (vh) fcm_iters = (int)fst[2];
     if (stat) return fail(ctx, stat, "non-finite cost during the pipeline");
     if (rep) {
         memset(rep, 0, sizeof *rep);

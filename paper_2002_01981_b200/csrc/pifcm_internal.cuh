@@ -135,6 +135,31 @@ struct P2PPut {
     unsigned epoch;
 };
 
+// x of a quantised value v for the volume range [lo, hi] (Alg. 2 step 1,
+// PAPER:173-174; R16: a constant volume maps to 0): the integer difference
+// and one correctly rounded fp32 division.  k_normalize and the
+// value-histogram FCM (fcm_hist.cu) both use it, so they see the same x.
+__device__ __forceinline__ float normalize_q(int v, int lo, int hi) {
+    return hi > lo ? __fdiv_rn((float)(v - lo), (float)(hi - lo)) : 0.f;
+}
+
+// The FCM start on the value histogram (fcm_hist.cu).
+struct FcmHistArgs {
+    const int64_t *counts;  // [nvals] voxels per raw value (u8: 256, u16: 65536)
+    int nvals;
+    const unsigned *mm;     // {min, max} raw values of the volume
+    const float *c0;        // [4] start centres
+    int max_iter;
+    float eps, m, inv_m1;
+    float *xs;              // scratch [nvals]: x of the occupied values
+    double *ns;             // scratch [nvals]: their counts
+    float4 *up;             // scratch [nvals]: their rows of the previous iteration
+    float *c_prev;          // [4] out: the centres the last iteration's rows used
+    float *c_out;           // [4] out: the centres after the last iteration (Eq. 3)
+    double *stats;          // [4] out: {J, max|du|, iterations, converged}
+    int *status;            // nullable: PIFCM_ENUMERIC on a non-finite J
+};
+
 // ---------------------------------------------------------------- launchers
 // All return cudaGetLastError() of the launch.
 cudaError_t launch_step(const StepArgs &a, int C, bool stencil, int P, cudaStream_t st);
@@ -158,6 +183,10 @@ cudaError_t launch_normalize_u8(const uint8_t *vol, int nx, int ny, int nz, int 
                                 const unsigned int *mm, float *x, cudaStream_t st);
 cudaError_t launch_hist_u8(const uint8_t *vol, long long n, const unsigned int *mm,
                            int64_t *hist, cudaStream_t st);
+cudaError_t launch_value_hist(const void *vol, int dtype, long long n, int64_t *counts, cudaStream_t st);
+cudaError_t launch_fcm_hist(const FcmHistArgs &a, int C, bool m2, cudaStream_t st);
+cudaError_t launch_fcm_memberships(const float *x, int nx, int ny, int nz, int pitch, const float *c, int C,
+                                   float m, float4 *U, cudaStream_t st);
 cudaError_t launch_gmm(const int64_t *hist, int C, int max_iter, float *c0, cudaStream_t st);
 cudaError_t launch_argmax(const float4 *U, long long n, int C, uint8_t *labels,
                           cudaStream_t st);

@@ -10,6 +10,10 @@
 
 #include "pifcm_internal.cuh"
 
+#ifndef PIFCM_KGATE
+#define PIFCM_KGATE 0
+#endif
+
 namespace pifcm {
 __device__ __forceinline__ float rcp_approx(float v) {
     float r;
@@ -251,12 +255,28 @@ __device__ __forceinline__ Memb memb_compute(float xv, const float2 (&c2)[2], co
         const float2 uu = __fmul2_rn(wq, make_float2(invS, invS));  // Eq. 2
         r.u[2 * q] = uu.x;
         r.u[2 * q + 1] = uu.y;
-        // u (1 - u) / |a| with the unfloored factor: a clamped factor (a << 0)
-        // contributes little (its u is ~0 or ~1), an uncertain clamp (|a| ~ 0)
-        // makes K huge, an unclamped small factor is weighed by 1/a
-        const float2 ia = make_float2(rcp_approx(fabsf(Ar[q].x)), rcp_approx(fabsf(Ar[q].y)));
-        const float2 t = __fmul2_rn(__fmul2_rn(uu, __fadd2_rn(make_float2(1.f, 1.f), make_float2(-uu.x, -uu.y))), ia);
-        Kp[q] = t.x + ((2 * q + 1 < C) ? t.y : 0.f);
+    }
+#if PIFCM_KGATE
+    // K <= sum_j u_j (1 - u_j) / min_j |a_j| <= (1 - 1/C) / min_j |a_j|
+    // (times 1/(m-1)): when that bound is below kKMax the voxel is not in the
+    // band and K need not be formed (NaN factors fall through to K)
+    float amin = fminf(fabsf(Ar[0].x), fabsf(Ar[0].y));
+    if (NP > 1) amin = fminf(amin, fminf(fabsf(Ar[NP - 1].x), fabsf(Ar[NP - 1].y)));
+    const bool kneed = !(amin * kKMax >= 0.75f * (M2 ? 1.0f : inv_m1));
+#else
+    const bool kneed = true;
+#endif
+    if (kneed) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            const float2 uu = make_float2(r.u[2 * q], r.u[2 * q + 1]);
+            // u (1 - u) / |a| with the unfloored factor: a clamped factor (a << 0)
+            // contributes little (its u is ~0 or ~1), an uncertain clamp (|a| ~ 0)
+            // makes K huge, an unclamped small factor is weighed by 1/a
+            const float2 ia = make_float2(rcp_approx(fabsf(Ar[q].x)), rcp_approx(fabsf(Ar[q].y)));
+            const float2 t = __fmul2_rn(__fmul2_rn(uu, __fadd2_rn(make_float2(1.f, 1.f), make_float2(-uu.x, -uu.y))), ia);
+            Kp[q] = t.x + ((2 * q + 1 < C) ? t.y : 0.f);
+        }
     }
     if (NP == 1) { r.u[2] = 0.f; r.u[3] = 0.f; }
     r.K = M2 ? Kp[0] + Kp[1] : (Kp[0] + Kp[1]) * inv_m1;

@@ -182,6 +182,7 @@ class ShardedSegmenter:
         self.Ub = torch.empty((1, nvox, 4), dtype=torch.float32, device=self.dev)
         self.Ua = torch.zeros((1, nvox, 4), dtype=torch.float32, device=self.dev)
         self.cen = torch.empty((1, 4), dtype=torch.float32, device=self.dev)
+        self.mm = torch.zeros(64, dtype=torch.int32, device=self.dev)  # normalise's raw {min, max}
         self.engine = None
         world = dist.get_world_size() if dist is not None else 1
         tz = ctx.slab_chunk(self.nx, self.ny, self.nz)
@@ -205,15 +206,18 @@ class ShardedSegmenter:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
         # Alg. 2 step 1 + Alg. 1 step 2: normalise, GMM, FCM start (lambda = xi = 0)
-        x, hist = ctx.normalize_u8(vol)
+        if vol.dtype not in (torch.uint8, torch.uint16):
+            raise TypeError("the particle-sharded pipeline takes uint8 / uint16 volumes")
+        x, hist = ctx.normalize(vol, mm=self.mm)
         c0 = ctx.gmm_init(hist, cfg.C)
         ev[1].record()
-        self.cen.copy_(c0.view(1, 4))
-        self.Ua.zero_()
-        zero = torch.zeros((1, 2), dtype=torch.float64, device=self.dev)
+        # FCM start on the value histogram (R24), exactly as pifcm_segment
+        counts = ctx.value_hist(vol)
+        c_prev, c_fcm4, fst = ctx.fcm_hist(counts, self.mm, c0, cfg)
+        ctx.fcm_memberships(x, c_prev, cfg.C, cfg.m, nx, U=self.Ub[0])
+        self.cen.copy_(c_fcm4.view(1, 4))
         stats = torch.zeros((1, 4), dtype=torch.float64, device=self.dev)
-        ctx.iterate(x, self.Ua, self.Ub, self.cen, zero, cfg, iters=cfg.max_iter, stats=stats, nx=nx)
-        fcm_iters = int(stats[0, 2].item())
+        fcm_iters = int(fst[2].item())
         ev[2].record()
         # Alg. 1 steps 3-10: sharded PSO from (U_fcm, c_fcm)
         g = _grid(nx, ny, nz)
@@ -731,15 +735,22 @@ class SlabSegmenter:
             self._allreduce(hist, d.ReduceOp.SUM)
         c0 = ctx.gmm_init(hist, cfg.C)
         ev[1].record()
-        # Alg. 1 step 2: FCM start (lambda = xi = 0) from U = 0 (the first step
-        # reads no neighbourhood: its terms are multiplied by 0)
+        # Alg. 1 step 2: FCM start on the global value histogram (R24): the
+        # ranks' counts are summed, every rank runs the identical FCM loop and
+        # writes the memberships of its own planes (halo planes zero; the PSO
+        # exchanges them)
         sl = self.ifcm
         sl.set_x(x)
-        sl.load_local(torch.zeros_like(sl.Ua), c0.view(1, 4))
-        zero = torch.zeros((1, 2), dtype=torch.float64, device=self.dev)
-        sl.run(zero, cfg.max_iter, eps=cfg.eps)
-        fcm_iters = int(sl.stats[0, 2].item())
-        c_fcm = sl.centers[0].clone()
+        counts = ctx.value_hist(own)
+        if g.world > 1:
+            self._allreduce(counts, d.ReduceOp.SUM)
+        c_prev, c_fcm, fst = ctx.fcm_hist(counts, mm, c0, cfg)
+        pl = self.nx * self.ny
+        U0 = sl.Ua[0]
+        U0[:pl].zero_()
+        U0[pl * (g.nz + 1):].zero_()
+        ctx.fcm_memberships(x[1: g.nz + 1], c_prev, cfg.C, cfg.m, self.nx, U=U0[pl: pl * (g.nz + 1)])
+        fcm_iters = int(fst[2].item())
         ev[2].record()
         # Alg. 1 steps 3-10: PSO over slabs from (U_fcm, c_fcm)
         sw = self.swarm
