@@ -151,7 +151,7 @@ def run_reference(args, rank, world):
     oracle.build_oracle()
     c5 = args.workload == "C5"
     vol = _volume("C5" if c5 else "C3")
-    workload = WORKLOAD_C5.format(P=64 if world >= 2 else 32) if c5 else WORKLOAD
+    workload = WORKLOAD_C5.format(P=64) if c5 else WORKLOAD
     x = oracle.normalize_u8(vol)
     c0 = oracle.gmm_init(oracle.histogram_u8(vol), C)
     U, c, _ = oracle.fcm_run(x, c0, max_iter=1)
@@ -205,13 +205,22 @@ def run_ours(args, rank, world, local_rank):
     c5 = args.workload == "C5"
     vol = _volume("C5" if c5 else "C3")
     nz, ny, nx = vol.shape
-    # C5: P = 64 as configured when the slot pool fits (>= 2 GPUs: 129 slots of
-    # the slab); one GPU holds 65 slots of the whole 512^3 volume (140 GB): P = 32
-    Pw = (64 if world >= 2 else 32) if c5 else P
+    # C5: P = 64 as configured.  The CHAINED slot pool is 2P + 1 slab states
+    # (129 x 2.16 GB at one GPU); where that does not fit, the particles are
+    # evaluated in batches of eval_batch states over P + eval_batch + 1 slots
+    # (bit-identical results, pifcm_pso_cfg.eval_batch)
+    Pw = 64 if c5 else P
     Pw = _env_int("PIFCM_BENCH_P", Pw)  # test hook (a smaller swarm), reported in config
+    eval_batch = 0
+    if c5:
+        slot = (-(-nz // world) + 2) * ny * nx * 16
+        free, _ = torch.cuda.mem_get_info(dev)
+        avail = free - 8 * slot - (2 << 30)  # slab IFCM states, x, volume, labels, records
+        if (2 * Pw + 1) * slot > avail:
+            eval_batch = max(1, int(avail // slot) - Pw - 1)
     workload = WORKLOAD_C5.format(P=Pw) if c5 else WORKLOAD
     cfg = IfcmConfig(C=C, m=2.0, q_mode=0, eps=1e-5, max_iter=100)
-    pso = PsoConfig(P=Pw, ring_k=1, max_gen=GENS, patience=0, seed=12345)
+    pso = PsoConfig(P=Pw, ring_k=1, max_gen=GENS, patience=0, seed=12345, eval_batch=eval_batch)
     vol_d = torch.as_tensor(vol, device=dev)
     vol_h = torch.as_tensor(vol).pin_memory()
     lab_h = torch.empty(vol.shape, dtype=torch.uint8).pin_memory()
@@ -368,8 +377,9 @@ def run_ours(args, rank, world, local_rank):
             "q_mode": "literal", "eps": 1e-5, "fitness": "chained",
             "parallelism": f"z-slabs/{world}" if c5 else f"particles/{world}",
             "l2": ("inputs larger than L2 (the membership slot pool is "
-                   f"{(2 * Pw + 1) * nx * ny * nz * 16 / 1e9:.1f} GB; every generation streams "
-                   f"{Pw * nx * ny * nz * 32 / 1e9:.1f} GB)"),
+                   f"{((Pw + eval_batch + 1) if eval_batch else (2 * Pw + 1)) * nx * ny * nz * 16 / world / 1e9:.1f}"
+                   f" GB per GPU; every generation streams {Pw * nx * ny * nz * 32 / 1e9:.1f} GB)"),
+            "eval_batch": eval_batch,
             "pso_wall_ms": last["t_pso"] * 1e3, "segment_wall_ms": last["t_total"] * 1e3,
             "fcm_iters": last["fcm_iters"], "final_iters": last["final_iters"],
             "lambda_star": last["lambda"], "xi_star": last["xi"],

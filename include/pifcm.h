@@ -128,6 +128,11 @@ typedef struct {
     int32_t fitness_mode; /* pifcm_fitness (ANCHORED / LEADER: P <= 128)           */
     int32_t p_begin;    /* this process evaluates particles [p_begin, p_end)      */
     int32_t p_end;      /*   (particle sharding; 0,0 means all P)                 */
+    int32_t eval_batch; /* CHAINED: evaluate this process's particles in launches of
+                           eval_batch states, reusing the slots the previous batch
+                           released: Pl + eval_batch + 1 state slots instead of
+                           2 Pl + 1 (0 or >= Pl: one launch).  Results are
+                           bit-identical for any value.                           */
 } pifcm_pso_cfg;
 
 /* Host-side summary of a PSO run (Alg. 1 step 10). */

@@ -38,7 +38,7 @@ class PsoCfg(ct.Structure):
     _fields_ = [("P", ct.c_int32), ("ring_k", ct.c_int32), ("max_gen", ct.c_int32),
                 ("patience", ct.c_int32), ("tol", ct.c_double), ("v0", ct.c_double),
                 ("vmax", ct.c_double), ("seed", ct.c_uint64), ("fitness_mode", ct.c_int32),
-                ("p_begin", ct.c_int32), ("p_end", ct.c_int32)]
+                ("p_begin", ct.c_int32), ("p_end", ct.c_int32), ("eval_batch", ct.c_int32)]
 
 
 class PsoResult(ct.Structure):

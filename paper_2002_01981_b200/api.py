@@ -53,10 +53,11 @@ class PsoConfig:
     p_begin: int = 0
     p_end: int = 0
     fitness: int = 0  # 0 CHAINED (R11), 1 ANCHORED, 2 LEADER (R22)
+    eval_batch: int = 0  # CHAINED: states per evaluation launch (0 = all; fewer slots otherwise)
 
     def c(self) -> _abi.PsoCfg:
         return _abi.PsoCfg(self.P, self.ring_k, self.max_gen, self.patience, self.tol, self.v0,
-                           self.vmax, self.seed, self.fitness, self.p_begin, self.p_end)
+                           self.vmax, self.seed, self.fitness, self.p_begin, self.p_end, self.eval_batch)
 
 
 def dtype_code(vol: torch.Tensor) -> int:

@@ -270,17 +270,20 @@ __global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs 
                     s.hdr[kHGbestSlot] = -1;
                 }
             }
-            // free-slot assignment for the next evaluation
-            unsigned int used[(2 * 1024 + 1 + 31) / 32];
-            const int nw = (a.nslots + 31) / 32;
-            for (int w = 0; w < nw; ++w) used[w] = 0u;
-            for (int q = 0; q < a.Pl; ++q) used[s.cur[q] >> 5] |= 1u << (s.cur[q] & 31);
-            const int gs = s.hdr[kHGbestSlot];
-            if (gs >= 0) used[gs >> 5] |= 1u << (gs & 31);
-            int next_free = 0;
-            for (int q = 0; q < a.Pl; ++q) {
-                while (used[next_free >> 5] & (1u << (next_free & 31))) ++next_free;
-                s.nxt[q] = next_free++;
+            // free-slot assignment for the next evaluation (batched: per batch,
+            // by k_assign_batch before each evaluation launch)
+            if (!a.batched) {
+                unsigned int used[(2 * 1024 + 1 + 31) / 32];
+                const int nw = (a.nslots + 31) / 32;
+                for (int w = 0; w < nw; ++w) used[w] = 0u;
+                for (int q = 0; q < a.Pl; ++q) used[s.cur[q] >> 5] |= 1u << (s.cur[q] & 31);
+                const int gs = s.hdr[kHGbestSlot];
+                if (gs >= 0) used[gs >> 5] |= 1u << (gs & 31);
+                int next_free = 0;
+                for (int q = 0; q < a.Pl; ++q) {
+                    while (used[next_free >> 5] & (1u << (next_free & 31))) ++next_free;
+                    s.nxt[q] = next_free++;
+                }
             }
         } else {
             // ANCHORED: slot 0 = the shared start, slot 1 = the gbest snapshot
@@ -332,6 +335,34 @@ __global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs 
             s.pos[2 * p + d] = fmin(fmax(__dadd_rn(x, v), 0.0), 1.0);
         }
     }
+}
+
+// Batched CHAINED evaluation (pifcm_pso_cfg.eval_batch): before the launch of
+// local particles [b0, b0 + nb), their output slots = the lowest slots that
+// hold no live state: live = the new states of the particles evaluated
+// earlier in this generation (nxt[q], q < b0), the current states of the rest
+// (cur[q], q >= b0) and the pinned gbest snapshot -- at most Pl + 1 slots, so
+// Pl + nb + 1 slots always suffice.
+__global__ void k_assign_batch(SwarmDev s, int Pl, int b0, int nb, int nslots) {
+    if (threadIdx.x != 0 || s.hdr[kHStop]) return;
+    unsigned int used[(2 * 1024 + 1 + 31) / 32];
+    const int nw = (nslots + 31) / 32;
+    for (int w = 0; w < nw; ++w) used[w] = 0u;
+    for (int q = 0; q < Pl; ++q) {
+        const int sl = q < b0 ? s.nxt[q] : s.cur[q];
+        used[sl >> 5] |= 1u << (sl & 31);
+    }
+    const int gs = s.hdr[kHGbestSlot];
+    if (gs >= 0) used[gs >> 5] |= 1u << (gs & 31);
+    int next_free = 0;
+    for (int q = b0; q < b0 + nb; ++q) {
+        while (used[next_free >> 5] & (1u << (next_free & 31))) ++next_free;
+        s.nxt[q] = next_free++;
+    }
+}
+cudaError_t launch_assign_batch(SwarmDev s, int Pl, int b0, int nb, int nslots, cudaStream_t st) {
+    k_assign_batch<<<1, 32, 0, st>>>(s, Pl, b0, nb, nslots);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pso_update(const PsoUpdateArgs &a, cudaStream_t st) {

@@ -138,7 +138,7 @@ FcmHistArgs fcm_hist_args(void *ws, int nvals) {
 struct Layout {
     size_t x, vol, lab, hist, mm, c0, slots, hdr, dhdr, pos, vel, pbf, pbx, fit, evalpos, cur, nxt,
         gbc, cent, part, stats, lamxi, cnt, hf, shc, vcnt, fhws, cprev, fstats, total;
-    int nslots, P, Pl, p0, nblk, mode;
+    int nslots, P, Pl, p0, nblk, mode, eb;  // eb: states per evaluation launch (CHAINED)
     long long nvox;
 };
 
@@ -153,7 +153,11 @@ Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg 
     // CHAINED: every particle's state, the slot its next evaluation writes and
     // the pinned gbest; ANCHORED: the shared start + the gbest snapshot;
     // LEADER: the shared state, its successor and the pinned gbest
-    L.nslots = L.mode == PIFCM_FIT_CHAINED ? 2 * Pl + 1 : (L.mode == PIFCM_FIT_LEADER ? 3 : 2);
+    // (batched CHAINED evaluation: every particle's state, one batch of new
+    // states, the pinned gbest)
+    L.eb = (pso && pso->eval_batch > 0 && pso->eval_batch < Pl) ? pso->eval_batch : Pl;
+    L.nslots = L.mode == PIFCM_FIT_CHAINED ? (L.eb < Pl ? Pl + L.eb + 1 : 2 * Pl + 1)
+                                           : (L.mode == PIFCM_FIT_LEADER ? 3 : 2);
     L.nblk = step_nblk_max(g->nx, g->ny, g->nz);
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
@@ -506,10 +510,19 @@ int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     SwarmDev s = swarm_of(ws, L);
     float4 *slots = at<float4>(ws, L.slots);
-    if (L.mode == PIFCM_FIT_CHAINED)
-        return run_step(ctx, grid, cfg, x, slots, slots, s.cur, s.nxt, s.centers, s.pos + 2 * L.p0, true, 0,
-                        L.Pl, at<double>(ws, L.part), s.fit + L.p0, nullptr, 0.f, s.hdr + kHStatus,
-                        s.hdr + kHStop, st, L.nslots, at<unsigned>(ws, L.cnt));
+    if (L.mode == PIFCM_FIT_CHAINED) {
+        const int nblk = step_nblk(grid->nx, grid->ny, grid->nz, true, L.Pl);
+        for (int b0 = 0; b0 < L.Pl; b0 += L.eb) {
+            const int nb = L.Pl - b0 < L.eb ? L.Pl - b0 : L.eb;
+            if (L.eb < L.Pl) LAUNCH(ctx, 1, launch_assign_batch(s, L.Pl, b0, nb, L.nslots, st));
+            r = run_step(ctx, grid, cfg, x, slots, slots, s.cur + b0, s.nxt + b0, s.centers + 4 * b0,
+                         s.pos + 2 * (L.p0 + b0), true, 0, nb, at<double>(ws, L.part) + (size_t)b0 * nblk * kNR,
+                         s.fit + L.p0 + b0, nullptr, 0.f, s.hdr + kHStatus, s.hdr + kHStop, st, L.nslots,
+                         at<unsigned>(ws, L.cnt) + b0);
+            if (r) return r;
+        }
+        return PIFCM_OK;
+    }
     // ANCHORED / LEADER: H, F of the shared state (ANCHORED: once per run, the
     // pass is skipped once hdr[kHHfValid] is set), then all particles' J
     float4 *hf = at<float4>(ws, L.hf);
@@ -549,6 +562,7 @@ int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cf
     a.s = swarm_of(ws, L);
     a.P = L.P; a.Pl = L.Pl; a.p0 = L.p0; a.ring_k = pso->ring_k; a.patience = pso->patience;
     a.nslots = L.nslots; a.tol = pso->tol; a.vmax = pso->vmax; a.mode = L.mode;
+    a.batched = L.eb < L.Pl ? 1 : 0;
     a.key0 = (uint32_t)(pso->seed & 0xFFFFFFFFu); a.key1 = (uint32_t)(pso->seed >> 32);
     LAUNCH(ctx, 1, launch_pso_update(a, st));
     if (L.mode == PIFCM_FIT_CHAINED) return PIFCM_OK;
@@ -1134,15 +1148,24 @@ int pifcm_slab_pso_eval(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm
     a.nx = slab->nx; a.ny = slab->ny; a.nz = slab->nz + 2; a.pitch = slab->pitch;
     a.nvox = L.nvox;
     a.z_lo = 1; a.nz_t = slab->nz; a.goff = slab->z0 - 1; a.nz_g = slab->nz_total;
-    a.U_in = slots; a.U_out = slots; a.in_idx = s.cur; a.out_idx = s.nxt;
-    a.centers = s.centers; a.lam_xi = s.pos; a.partials = records;
+    a.U_in = slots; a.U_out = slots;
     a.stop = s.hdr + kHStop;
     a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f); a.q_mode = cfg->q_mode;
     a.n_in_states = L.nslots;
     a.counters = nullptr;  // records are combined across ranks by pifcm_slab_pso_finalize
     a.C = cfg->C;
-    return timed_step(ctx, a, cfg->C, true, L.Pl, (long long)slab->nx * slab->ny * slab->nz,
-                      reinterpret_cast<cudaStream_t>(stream));
+    int nrec = 0;
+    if ((r = pifcm_slab_records(slab, &nrec))) return fail(ctx, r, "invalid slab grid");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    for (int b0 = 0; b0 < L.Pl; b0 += L.eb) {  // batches of eval_batch states (see pifcm_pso_eval)
+        const int nb = L.Pl - b0 < L.eb ? L.Pl - b0 : L.eb;
+        if (L.eb < L.Pl) LAUNCH(ctx, 1, launch_assign_batch(s, L.Pl, b0, nb, L.nslots, st));
+        a.in_idx = s.cur + b0; a.out_idx = s.nxt + b0;
+        a.centers = s.centers + 4 * b0; a.lam_xi = s.pos + 2 * b0;
+        a.partials = records + (size_t)b0 * nrec * kNR;
+        if ((r = timed_step(ctx, a, cfg->C, true, nb, (long long)slab->nx * slab->ny * slab->nz, st))) return r;
+    }
+    return PIFCM_OK;
 }
 
 int pifcm_slab_pso_finalize(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,

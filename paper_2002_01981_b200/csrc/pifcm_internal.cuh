@@ -113,6 +113,7 @@ struct PsoUpdateArgs {
     SwarmDev s;
     int P, Pl, p0, ring_k, patience, nslots;
     int mode;  // pifcm_fitness: CHAINED / ANCHORED / LEADER
+    int batched;  // CHAINED with batched evaluation: next slots assigned per batch (k_assign_batch)
     double tol, vmax;
     uint32_t key0, key1;
 };
@@ -173,6 +174,7 @@ cudaError_t launch_fixup_copy(const float4 *scratch, float4 *out, long long nvox
 cudaError_t launch_pso_init(SwarmDev s, int P, int Pl, int p0, double v0, uint32_t k0,
                             uint32_t k1, const float *c0, int nslots, cudaStream_t st);
 cudaError_t launch_pso_update(const PsoUpdateArgs &a, cudaStream_t st);
+cudaError_t launch_assign_batch(SwarmDev s, int Pl, int b0, int nb, int nslots, cudaStream_t st);
 cudaError_t launch_minmax(const void *vol, int dtype, long long n, unsigned int *mm, cudaStream_t st);
 cudaError_t launch_normalize(const void *vol, int dtype, int nx, int ny, int nz, int pitch,
                              const unsigned int *mm, float *x, cudaStream_t st);

@@ -11,7 +11,7 @@
 #include "pifcm_internal.cuh"
 
 #ifndef PIFCM_KGATE
-#define PIFCM_KGATE 0
+#define PIFCM_KGATE 1
 #endif
 
 namespace pifcm {

@@ -166,3 +166,43 @@ def test_segment_determinism(ctx):
     b = ctx.segment(vt, cfg, pso, want_U=True)
     assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
     assert a[2]["J"] == b[2]["J"]
+
+
+@pytest.mark.parametrize("eb", [1, 3, 5])
+def test_eval_batch_bit_identical(ctx, eb):
+    """pifcm_pso_cfg.eval_batch: CHAINED evaluation in launches of eb states
+    over a pool of P + eb + 1 slots gives the same pipeline, bit for bit, as
+    one launch over 2P + 1 slots."""
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    vol, _ = _small_case(C=4, shape=(9, 26, 30), seed=8)
+    vt = torch.as_tensor(vol, device="cuda:0")
+    cfg = IfcmConfig(C=4)
+    base = PsoConfig(P=7, max_gen=4, patience=0, seed=3)
+    bat = PsoConfig(P=7, max_gen=4, patience=0, seed=3, eval_batch=eb)
+    nz, ny, nx = vol.shape
+    slot = nz * ny * nx * 16
+    assert ctx.workspace_size(nx, ny, nz, cfg, base) - ctx.workspace_size(nx, ny, nz, cfg, bat) >= (7 - eb) * slot
+    la, Ua, ra = ctx.segment(vt, cfg, base, want_U=True)
+    lb, Ub, rb = ctx.segment(vt, cfg, bat, want_U=True)
+    assert torch.equal(la, lb) and torch.equal(Ua, Ub)
+    for k in ("lambda", "xi", "J", "generations", "gbest_particle", "fcm_iters", "final_iters", "centers"):
+        assert ra[k] == rb[k], k
+
+
+def test_eval_batch_slab_bit_identical(ctx):
+    """The same for the z-slab swarm (SlabSegmenter, one rank)."""
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    from paper_2002_01981_b200.dist import SlabSegmenter
+    vol, _ = _small_case(C=4, shape=(21, 24, 27), seed=9)
+    vt = torch.as_tensor(vol, device="cuda:0")
+    out = []
+    for eb in (0, 2):
+        seg = SlabSegmenter(ctx, IfcmConfig(C=4), PsoConfig(P=5, max_gen=3, patience=0, seed=17, eval_batch=eb),
+                            vol.shape)
+        seg.keep_trace = True
+        rep = seg.segment(vt)
+        out.append((seg.labels.cpu().numpy(), rep, np.stack([t.numpy() for t in seg.trace])))
+    (la, ra, ta), (lb, rb, tb) = out
+    assert (la == lb).all() and (ta == tb).all()
+    for k in ("lambda", "xi", "J", "generations", "gbest_particle", "final_iters", "centers"):
+        assert ra[k] == rb[k], k
