@@ -23,6 +23,7 @@ __all__ = [
     "normalize_u8", "histogram_u8", "normalize", "histogram", "gmm_init", "philox4x32_10", "philox_pair",
     "pso_init", "pso_move", "pso_update", "pso_run", "ifcm_run", "fcm_run", "segment_u8",
     "num_threads", "set_num_threads", "PsoResult", "SegmentResult",
+    "ifcm_step_planes", "histogram_u8_range", "segment_slice_u8", "SliceResult",
 ]
 
 
@@ -93,6 +94,11 @@ def _declare(L):
     L.orc_segment_u8.argtypes = [_u8p, i, i, i, i, d, i, i, d, d, i, i, i, i, i, d, d, d, u64,
                                  _u8p, _dp, _dp, _dp, _dp, _ip, _ip, _dp, i]
     L.orc_segment_u8.restype = i
+    L.orc_ifcm_step_planes.argtypes = [_dp, i, i, i, i, i, i, d, d, d, i, i, d, _dp, _dp, _dp, _dp, _dp, _dp]
+    L.orc_histogram_u8_range.argtypes = [_u8p, l, i, i, _i64p]
+    L.orc_segment_slice_u8.argtypes = [_u8p, i, i, i, i, i, d, i, d, i, i, i, i, i, d, d, d, u64,
+                                       _u8p, _dp, _dp, _dp, _dp, _ip, _ip, _dp, _ip]
+    L.orc_segment_slice_u8.restype = i
     L.orc_num_threads.restype = i
     L.orc_set_num_threads.argtypes = [i]
 
@@ -136,6 +142,30 @@ def ifcm_step(x, U, c, lam, xi, m=2.0, q_mode=0, v=1, h=1.0):
     _L().orc_ifcm_step(_p(x), nx, ny, nz, C, m, lam, xi, q_mode, v, h, _p(U), _p(c),
                        _p(Un), _p(cn), ct.byref(J), ct.byref(du))
     return Un, cn, J.value, du.value
+
+
+def ifcm_step_planes(x, U, c, lam, xi, zt0, zt1, m=2.0, q_mode=0, v=1, h=1.0):
+    """One IFCM step of the target planes [zt0, zt1) only (R25): the other rows
+    are copied; c, J, maxdu over the target planes."""
+    x = _f64(x)
+    nz, ny, nx = x.shape
+    U = _f64(U)
+    C = U.shape[1]
+    c = _f64(c)
+    Un = np.empty_like(U)
+    cn = np.empty(C, np.float64)
+    J = ct.c_double()
+    du = ct.c_double()
+    _L().orc_ifcm_step_planes(_p(x), nx, ny, nz, zt0, zt1, C, m, lam, xi, q_mode, v, h, _p(U), _p(c),
+                              _p(Un), _p(cn), ct.byref(J), ct.byref(du))
+    return Un, cn, J.value, du.value
+
+
+def histogram_u8_range(vol, lo, hi):
+    vol = np.ascontiguousarray(vol, dtype=np.uint8).ravel()
+    h = np.empty(256, np.int64)
+    _L().orc_histogram_u8_range(_p(vol, _u8p), vol.size, int(lo), int(hi), _p(h, _i64p))
+    return h
 
 
 def ifcm_voxels(x, U, c, lam, xi, idx, m=2.0, q_mode=0, v=1, h=1.0):
@@ -359,3 +389,41 @@ def segment_u8(vol, C, P, max_gen, seed, m=2.0, q_mode=0, v=1, h=1.0, eps=1e-5, 
                            _p(lx), ct.byref(J), ct.byref(gens), ct.byref(fi), _p(ci), fitness_mode)
     return SegmentResult(lab.reshape(nz, ny, nx), U, c, lx[0], lx[1], J.value, gens.value,
                          fi.value, ci)
+
+
+@dataclass
+class SliceResult:
+    labels: np.ndarray   # [ny, nx]
+    U: np.ndarray        # [ny*nx, C]
+    c: np.ndarray
+    lam: float
+    xi: float
+    J: float
+    generations: int
+    final_iters: int
+    c_init: np.ndarray
+    fcm_iters: int
+
+
+def segment_slice_u8(vol, z, C, P, max_gen, seed, m=2.0, q_mode=0, eps=1e-5, max_iter=100, ring_k=1,
+                     patience=0, tol=1e-4, v0=0.1, vmax=0.5):
+    """The literal slice mode (R25, orc_segment_slice_u8): segment slice z of a
+    u8 volume [nz, ny, nx] with its 3D neighbourhood."""
+    vol = np.ascontiguousarray(vol, dtype=np.uint8)
+    nz, ny, nx = vol.shape
+    n = nx * ny
+    lab = np.empty(n, np.uint8)
+    U = np.empty((n, C))
+    c = np.empty(C)
+    lx = np.empty(2)
+    J = ct.c_double()
+    gens = ct.c_int()
+    fi = ct.c_int()
+    ci = np.empty(C)
+    fc = ct.c_int()
+    r = _L().orc_segment_slice_u8(_p(vol, _u8p), nx, ny, nz, int(z), C, m, q_mode, eps, max_iter, P, ring_k,
+                                  max_gen, patience, tol, v0, vmax, seed, _p(lab, _u8p), _p(U), _p(c), _p(lx),
+                                  ct.byref(J), ct.byref(gens), ct.byref(fi), _p(ci), ct.byref(fc))
+    if r != 0:
+        raise ValueError(f"slice {z} outside [0, {nz})")
+    return SliceResult(lab.reshape(ny, nx), U, c, lx[0], lx[1], J.value, gens.value, fi.value, ci, fc.value)

@@ -145,11 +145,14 @@ static void ifcm_voxel(const double *x, int nx, int ny, int nz, int C, double m,
  * Alg. 2 steps 6-8): Jacobi update of every membership row from
  * the previous U (R7), then Eq. 3 centres from the new U (R6), then Eq. 1 cost
  * with the same Eq. 4 distances (R8), and max |u_new - u_old|.
+ * Only the rows of the target planes [zt0, zt1) are updated and summed; the
+ * other planes' rows are copied (they are neighbours only -- the literal slice
+ * mode, R25).  orc_ifcm_step = all planes.
  * If c_new is NULL the centres are not updated. */
-void orc_ifcm_step(const double *x, int nx, int ny, int nz, int C, double m,
-                   double lam, double xi, int q_mode, int v, double h,
-                   const double *U_old, const double *c_old,
-                   double *U_new, double *c_new, double *J_out, double *maxdu_out) {
+void orc_ifcm_step_planes(const double *x, int nx, int ny, int nz, int zt0, int zt1, int C, double m,
+                          double lam, double xi, int q_mode, int v, double h,
+                          const double *U_old, const double *c_old,
+                          double *U_new, double *c_new, double *J_out, double *maxdu_out) {
     double W[8];
     orc_shell_weights(v, h, W);
     double *pnum = (double *)calloc((size_t)nz * C, sizeof(double));
@@ -159,9 +162,14 @@ void orc_ifcm_step(const double *x, int nx, int ny, int nz, int C, double m,
 #pragma omp parallel for schedule(dynamic, 1)
     for (int Z = 0; Z < nz; ++Z) {
         double u[8], d2[8], H[8], F[8];
+        const int target = Z >= zt0 && Z < zt1;
         for (int Y = 0; Y < ny; ++Y)
             for (int X = 0; X < nx; ++X) {
                 const long i = ((long)Z * ny + Y) * nx + X;
+                if (!target) {
+                    for (int j = 0; j < C; ++j) U_new[i * C + j] = U_old[i * C + j];
+                    continue;
+                }
                 ifcm_voxel(x, nx, ny, nz, C, m, lam, xi, q_mode, v, W, U_old, c_old,
                            X, Y, Z, u, d2, H, F);
                 for (int j = 0; j < C; ++j) {
@@ -185,6 +193,14 @@ void orc_ifcm_step(const double *x, int nx, int ny, int nz, int C, double m,
     if (J_out) *J_out = J;
     if (maxdu_out) *maxdu_out = mdu;
     free(pnum); free(pden); free(pJ); free(pdu);
+}
+
+void orc_ifcm_step(const double *x, int nx, int ny, int nz, int C, double m,
+                   double lam, double xi, int q_mode, int v, double h,
+                   const double *U_old, const double *c_old,
+                   double *U_new, double *c_new, double *J_out, double *maxdu_out) {
+    orc_ifcm_step_planes(x, nx, ny, nz, 0, nz, C, m, lam, xi, q_mode, v, h, U_old, c_old, U_new, c_new, J_out,
+                         maxdu_out);
 }
 
 /* Per-voxel evaluation at a list of voxels (for sampled parity at full size):
@@ -289,12 +305,18 @@ void orc_normalize_u8(const uint8_t *vol, long N, double *x) {
 /* R15: 256-bin histogram of the normalised volume, computed in integers:
  * bin = floor(((v - min) * 255 + (max - min) / 2) / (max - min)), i.e. the
  * nearest of 256 evenly spaced levels b/255.  Constant volume -> all in bin 0. */
+void orc_histogram_u8_range(const uint8_t *vol, long N, int mn, int mx, int64_t *hist);
 void orc_histogram_u8(const uint8_t *vol, long N, int64_t *hist) {
     int mn = 255, mx = 0;
     for (long i = 0; i < N; ++i) {
         if (vol[i] < mn) mn = vol[i];
         if (vol[i] > mx) mx = vol[i];
     }
+    orc_histogram_u8_range(vol, N, mn, mx, hist);
+}
+/* The same bins for values vol[0..N) of a volume whose range is [mn, mx]
+ * (the slice of R25 binned on the whole volume's levels). */
+void orc_histogram_u8_range(const uint8_t *vol, long N, int mn, int mx, int64_t *hist) {
     for (int b = 0; b < 256; ++b) hist[b] = 0;
     const int rng = mx - mn;
     for (long i = 0; i < N; ++i) {
@@ -604,6 +626,12 @@ void orc_pso_update(int P, int ring_k, uint32_t gen, uint64_t seed, double vmax,
 /* the (U, c) its evaluation produced; per-generation traces for testing.      */
 /* Pin: partial (PSO invariants and worked example); end-to-end trajectory     */
 /* parity unpinned (only oracle-vs-GPU agreement).                             */
+static int pso_core(const double *x, int nx, int ny, int nz, int zt0, int zt1, int C, double m, int q_mode,
+                    int v, double h, const double *U0, const double *c0,
+                    int P, int ring_k, int max_gen, int patience, double tol, double v0,
+                    double vmax, uint64_t seed, double *best_lx, double *best_J, double *best_U,
+                    double *best_c, double *trace_pos, double *trace_f, int *trace_gbest, int fitness_mode);
+
 int orc_pso_run(const double *x, int nx, int ny, int nz, int C, double m, int q_mode,
                 int v, double h, const double *U0, const double *c0,
                 int P, int ring_k, int max_gen, int patience, double tol, double v0,
@@ -613,6 +641,16 @@ int orc_pso_run(const double *x, int nx, int ny, int nz, int C, double m, int q_
                 double *trace_pos /*[max_gen][P][2] nullable*/,
                 double *trace_f /*[max_gen][P] nullable*/,
                 int *trace_gbest /*[max_gen] nullable*/, int fitness_mode) {
+    return pso_core(x, nx, ny, nz, 0, nz, C, m, q_mode, v, h, U0, c0, P, ring_k, max_gen, patience, tol, v0,
+                    vmax, seed, best_lx, best_J, best_U, best_c, trace_pos, trace_f, trace_gbest, fitness_mode);
+}
+
+/* The PSO of orc_pso_run over the target planes [zt0, zt1) (R25). */
+static int pso_core(const double *x, int nx, int ny, int nz, int zt0, int zt1, int C, double m, int q_mode,
+                    int v, double h, const double *U0, const double *c0,
+                    int P, int ring_k, int max_gen, int patience, double tol, double v0,
+                    double vmax, uint64_t seed, double *best_lx, double *best_J, double *best_U,
+                    double *best_c, double *trace_pos, double *trace_f, int *trace_gbest, int fitness_mode) {
     const long N = (long)nx * ny * nz;
     const int shared = (fitness_mode == 1 || fitness_mode == 2);
     double *pos = (double *)malloc(sizeof(double) * 2 * P);
@@ -642,7 +680,7 @@ int orc_pso_run(const double *x, int nx, int ny, int nz, int C, double m, int q_
         for (int p = 0; p < P; ++p) {
             double cn[8], J, du;
             const int sp = shared ? 0 : p;
-            orc_ifcm_step(x, nx, ny, nz, C, m, pos[2 * p], pos[2 * p + 1], q_mode, v, h,
+            orc_ifcm_step_planes(x, nx, ny, nz, zt0, zt1, C, m, pos[2 * p], pos[2 * p + 1], q_mode, v, h,
                           Us + (size_t)sp * N * C, cs + (size_t)sp * C, Ut, cn, &J, &du);
             if (!shared) {
                 memcpy(Us + (size_t)p * N * C, Ut, sizeof(double) * (size_t)N * C);
@@ -662,7 +700,7 @@ int orc_pso_run(const double *x, int nx, int ny, int nz, int C, double m, int q_
             /* the state the gbest's evaluation produced this generation (the
              * evaluation is deterministic, so it is recomputed rather than kept) */
             double J, du;
-            orc_ifcm_step(x, nx, ny, nz, C, m, eval_pos[2 * gbest], eval_pos[2 * gbest + 1], q_mode, v, h,
+            orc_ifcm_step_planes(x, nx, ny, nz, zt0, zt1, C, m, eval_pos[2 * gbest], eval_pos[2 * gbest + 1], q_mode, v, h,
                           Us, cs, Ut, cg, &J, &du);
         }
         if (improved) {
@@ -697,16 +735,24 @@ int orc_pso_run(const double *x, int nx, int ny, int nz, int C, double m, int q_
 /* IFCM (or FCM when lam = xi = 0) iterated until max|du| < eps or max_iter
  * (Alg. 1 step 11; R14).  U and c are updated in place.
  * Returns the number of iterations run. */
+static int ifcm_run_planes(const double *x, int nx, int ny, int nz, int zt0, int zt1, int C, double m,
+                           double lam, double xi, int q_mode, int v, double h, double eps, int max_iter,
+                           double *U, double *c, double *J_out);
 int orc_ifcm_run(const double *x, int nx, int ny, int nz, int C, double m, double lam,
                  double xi, int q_mode, int v, double h, double eps, int max_iter,
                  double *U, double *c, double *J_out) {
+    return ifcm_run_planes(x, nx, ny, nz, 0, nz, C, m, lam, xi, q_mode, v, h, eps, max_iter, U, c, J_out);
+}
+static int ifcm_run_planes(const double *x, int nx, int ny, int nz, int zt0, int zt1, int C, double m,
+                           double lam, double xi, int q_mode, int v, double h, double eps, int max_iter,
+                           double *U, double *c, double *J_out) {
     const long N = (long)nx * ny * nz;
     double *Ut = (double *)malloc(sizeof(double) * (size_t)N * C);
     int it = 0;
     double J = 0.0;
     for (it = 1; it <= max_iter; ++it) {
         double cn[8], du;
-        orc_ifcm_step(x, nx, ny, nz, C, m, lam, xi, q_mode, v, h, U, c, Ut, cn, &J, &du);
+        orc_ifcm_step_planes(x, nx, ny, nz, zt0, zt1, C, m, lam, xi, q_mode, v, h, U, c, Ut, cn, &J, &du);
         memcpy(U, Ut, sizeof(double) * (size_t)N * C);
         memcpy(c, cn, sizeof(double) * C);
         if (du < eps) break;
@@ -821,5 +867,64 @@ static int segment_core(const double *xin, const int64_t *histin, int nx, int ny
     *gens_out = gens;
     *final_iters_out = fi;
     free(U); free(Ub);
+    return 0;
+}
+
+/* The literal slice mode (R25; Alg. 1 with its input z: "The z
+ * slice is assigned to a new variable"; "running through each voxel
+ * in the slice of a particular z axis image"): the whole volume is normalised
+ * (Alg. 2 step 1); the R15 histogram of slice z on the volume's levels feeds the
+ * GMM; FCM runs on the slice; the rows of the neighbouring planes z - 1, z + 1
+ * (where they exist) are the Eq. 2 memberships at the FCM centres c1 and stay
+ * fixed; the PSO (CHAINED) and the final IFCM update only slice z (3D
+ * neighbourhood, Eq. 3 / Eq. 1 over the slice).  Outputs: labels [ny][nx] and
+ * optionally U_out [ny*nx][C] of the slice.  Pins: nz = 1 equals
+ * orc_segment_u8; the plane-restricted step equals the whole step on the
+ * target rows (tests/test_oracle_pso.py); end to end parity unpinned. */
+int orc_segment_slice_u8(const uint8_t *vol, int nx, int ny, int nz, int z, int C, double m, int q_mode,
+                         double eps, int max_iter, int P, int ring_k, int max_gen, int patience, double tol,
+                         double v0, double vmax, uint64_t seed, uint8_t *labels, double *U_out, double *c_out,
+                         double *lam_xi_out, double *J_out, int *gens_out, int *final_iters_out,
+                         double *c_init_out, int *fcm_iters_out) {
+    if (z < 0 || z >= nz) return -1;
+    const long N = (long)nx * ny * nz, pl = (long)nx * ny;
+    double *x = (double *)malloc(sizeof(double) * (size_t)N);
+    orc_normalize_u8(vol, N, x);
+    int mn = 255, mx = 0;
+    for (long i = 0; i < N; ++i) {
+        if (vol[i] < mn) mn = vol[i];
+        if (vol[i] > mx) mx = vol[i];
+    }
+    int64_t hist[256];
+    orc_histogram_u8_range(vol + (long)z * pl, pl, mn, mx, hist);
+    double c0[8], c1[8], cb[8], lx[2], Jb = 0.0;
+    orc_gmm_init(hist, C, 100, c0);
+    if (c_init_out) memcpy(c_init_out, c0, sizeof(double) * C);
+    /* the neighbourhood planes of slice z: sub-volume [zs0, zs1), target t */
+    const int zs0 = z > 0 ? z - 1 : 0, zs1 = z + 2 < nz ? z + 2 : nz, nzs = zs1 - zs0, t = z - zs0;
+    const double *xs = x + (long)zs0 * pl;
+    double *Us = (double *)malloc(sizeof(double) * (size_t)nzs * pl * C);
+    double *Ub = (double *)malloc(sizeof(double) * (size_t)nzs * pl * C);
+    const int fi0 = orc_fcm_run(xs + (long)t * pl, pl, C, m, eps, max_iter, c0, Us + (long)t * pl * C, c1);
+    if (fcm_iters_out) *fcm_iters_out = fi0;
+    for (int k = 0; k < nzs; ++k) {
+        if (k == t) continue;
+        double cn[8], Jh, duh;
+        orc_fcm_step(xs + (long)k * pl, pl, C, m, c1, NULL, Us + (long)k * pl * C, cn, &Jh, &duh);
+    }
+    const int gens = pso_core(xs, nx, ny, nzs, t, t + 1, C, m, q_mode, 1, 1.0, Us, c1, P, ring_k, max_gen,
+                              patience, tol, v0, vmax, seed, lx, &Jb, Ub, cb, NULL, NULL, NULL, 0);
+    double Jf = 0.0;
+    const int fi = ifcm_run_planes(xs, nx, ny, nzs, t, t + 1, C, m, lx[0], lx[1], q_mode, 1, 1.0, eps,
+                                   max_iter, Ub, cb, &Jf);
+    orc_argmax(Ub + (long)t * pl * C, pl, C, labels);
+    if (U_out) memcpy(U_out, Ub + (long)t * pl * C, sizeof(double) * (size_t)pl * C);
+    memcpy(c_out, cb, sizeof(double) * C);
+    lam_xi_out[0] = lx[0];
+    lam_xi_out[1] = lx[1];
+    *J_out = Jb;
+    *gens_out = gens;
+    *final_iters_out = fi;
+    free(x); free(Us); free(Ub);
     return 0;
 }
