@@ -338,6 +338,24 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
                   int32_t z_slice, void *ws, size_t ws_bytes, uint8_t *labels, float *U_out,
                   pifcm_report *rep, pifcm_stream stream);
 
+/* The literal slice mode (DESIGN R25; Alg. 1 with its input z, PAPER:93, 110:
+ * "The z slice is assigned to a new variable"; the step runs
+ * "through each voxel in the slice of a particular z axis image"): segment
+ * slice z of a u8 volume with its 3D neighbourhood.  The volume is normalised
+ * (Alg. 2 step 1); the R15 histogram of slice z on the volume's levels feeds
+ * the GMM; FCM runs on the slice; the rows of planes z - 1, z + 1 (where they
+ * exist) are the Eq. 2 memberships at the FCM centres and stay fixed; the
+ * CHAINED PSO and the final IFCM update slice z only (Eq. 3 / Eq. 1 over the
+ * slice).  v = 1, CHAINED, single process (eval_batch allowed).  Sync.
+ *   vol     dev u8 [nz][ny][nx];  0 <= z < nz
+ *   labels  dev u8 [ny][nx] out;  U_out dev fp32 [ny][nx][4] out, nullable
+ *   ws      >= pifcm_segment_slice_workspace_size bytes (dev, 256-B aligned) */
+int pifcm_segment_slice_workspace_size(int32_t nx, int32_t ny, int32_t nz, int32_t z, const pifcm_ifcm_cfg *cfg,
+                                       const pifcm_pso_cfg *pso, size_t *bytes);
+int pifcm_segment_slice(pifcm_ctx *ctx, const uint8_t *vol, int32_t nx, int32_t ny, int32_t nz, int32_t z,
+                        const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes,
+                        uint8_t *labels, float *U_out, pifcm_report *rep, pifcm_stream stream);
+
 /* The same pipeline with HOST buffers (vol host u8, labels host u8): copies
  * the volume in, runs pifcm_segment, copies the labels out.  Sync. */
 int pifcm_segment_host(pifcm_ctx *ctx, const uint8_t *vol_host, int32_t nx, int32_t ny,

@@ -107,6 +107,10 @@ SIGNATURES = {
                                  ct.c_int32, _vp, ct.c_size_t, _vp, _vp, ct.POINTER(Report), _vp]),
     "pifcm_segment_host": (ct.c_int, [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int32, _C, _P, _vp,
                                       ct.c_size_t, _vp, ct.POINTER(Report), _vp]),
+    "pifcm_segment_slice_workspace_size": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, _C, _P,
+                                                       ct.POINTER(ct.c_size_t)]),
+    "pifcm_segment_slice": (ct.c_int, [_vp, _vp, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, _C, _P, _vp,
+                                       ct.c_size_t, _vp, _vp, ct.POINTER(Report), _vp]),
     "pifcm_minmax_u8": (ct.c_int, [_vp, _vp, ct.c_int64, _vp, _vp]),
     "pifcm_normalize_u8_range": (ct.c_int, [_vp, _G, _vp, _vp, _vp, _vp]),
     "pifcm_hist_u8": (ct.c_int, [_vp, _vp, ct.c_int64, _vp, _vp, _vp]),

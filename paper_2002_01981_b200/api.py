@@ -349,6 +349,26 @@ class Context:
                                         _ptr(U), ct.byref(rep), _stream(stream)))
         return labels, U, report_dict(rep, cfg.C)
 
+    def segment_slice(self, vol: torch.Tensor, z: int, cfg: IfcmConfig, pso: PsoConfig, want_U=False,
+                      stream=None):
+        """pifcm_segment_slice (literal slice mode, R25): slice z of a device
+        uint8 volume [nz, ny, nx] with its 3D neighbourhood -> (labels [ny, nx],
+        U [ny*nx, 4] or None, report)."""
+        if vol.dtype != torch.uint8:
+            raise TypeError("the slice mode takes uint8 volumes")
+        nz, ny, nx = vol.shape
+        n = ct.c_size_t()
+        self._ck(self.lib.pifcm_segment_slice_workspace_size(nx, ny, nz, z, ct.byref(cfg.c()), ct.byref(pso.c()),
+                                                             ct.byref(n)))
+        ws = torch.empty(n.value, dtype=torch.uint8, device=vol.device)
+        labels = torch.empty((ny, nx), dtype=torch.uint8, device=vol.device)
+        U = torch.empty((ny * nx, 4), dtype=torch.float32, device=vol.device) if want_U else None
+        rep = _abi.Report()
+        self._ck(self.lib.pifcm_segment_slice(self._h, _ptr(vol.contiguous()), nx, ny, nz, z, ct.byref(cfg.c()),
+                                              ct.byref(pso.c()), _ptr(ws), n.value, _ptr(labels), _ptr(U),
+                                              ct.byref(rep), _stream(stream)))
+        return labels, U, report_dict(rep, cfg.C)
+
     def segment_host(self, vol_host: torch.Tensor, cfg: IfcmConfig, pso: PsoConfig, ws,
                      labels_host: torch.Tensor, stream=None):
         """pifcm_segment_host: host (pinned) u8 volume in, host u8 labels out."""

@@ -950,9 +950,11 @@ static int check_slab(pifcm_ctx *ctx, const pifcm_grid *g) {
     if (g->nz_total < 1) return fail(ctx, PIFCM_EINVAL, "slab calls need nz_total >= 1");
     if (g->z0 < 0 || g->z0 + g->nz > g->nz_total)
         return fail(ctx, PIFCM_EINVAL, "slab [%d, %d) outside [0, %d)", g->z0, g->z0 + g->nz, g->nz_total);
+    // (a single-plane slab -- the slice mode, R25 -- is one chunk at any z0)
     const int tz = slab_tz(g->nx, g->ny, g->nz_total);
-    if (g->z0 % tz != 0) return fail(ctx, PIFCM_EINVAL, "slab z0 = %d is not a multiple of %d", g->z0, tz);
-    if (g->z0 + g->nz != g->nz_total && g->nz % tz != 0)
+    if (g->nz > 1 && g->z0 % tz != 0)
+        return fail(ctx, PIFCM_EINVAL, "slab z0 = %d is not a multiple of %d", g->z0, tz);
+    if (g->nz > 1 && g->z0 + g->nz != g->nz_total && g->nz % tz != 0)
         return fail(ctx, PIFCM_EINVAL, "a slab other than the last must hold a multiple of %d planes", tz);
     if ((long long)g->nx * g->ny * (g->nz + 2) >= (1LL << 31)) return fail(ctx, PIFCM_EINVAL, "slab too large");
     return PIFCM_OK;
@@ -1331,6 +1333,220 @@ int pifcm_slab_p2p_run(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_
     *epoch = e;
     *cur = c;
     *iters_done = t > iters ? iters : t;
+    return PIFCM_OK;
+}
+
+// ============================================================== ABI: slice mode
+// The literal slice mode (R25; Alg. 1 with its input z):
+// slice z is segmented with its 3D neighbourhood; the neighbour planes z - 1,
+// z + 1 carry the FCM start's memberships at its centres c1, fixed.  The slice
+// is a single-plane slab (pifcm_slab_* calls, nz = 1, z0 = z): its state slots
+// hold the two halo planes, refilled with the fixed rows before every
+// evaluation; the final IFCM iterates the slab step + finalisation.
+namespace {
+struct SliceLayout {
+    Layout L;           // the slab PSO workspace (offset 0)
+    size_t xs, hlo, hhi, A, B, rec, mm, hist, vcnt, fhws, c0, cprev, c1, cent, lamxi, stats, fstats, status, total;
+    long long plane;
+    int nrec;
+};
+SliceLayout slice_layout(const pifcm_grid *sg, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso) {
+    SliceLayout S{};
+    const pifcm_grid pg{sg->nx, sg->ny, 3, sg->pitch, 0, 0};
+    S.L = layout(&pg, cfg, pso);
+    S.plane = (long long)sg->nx * sg->ny;
+    const int tz = slab_tz(sg->nx, sg->ny, sg->nz_total);
+    S.nrec = ((sg->nx + kTX - 1) / kTX) * ((sg->ny + kTY - 1) / kTY) * ((1 + tz - 1) / tz);
+    size_t o = S.L.total;
+    auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
+    S.xs = take(sizeof(float) * 3 * (size_t)sg->ny * sg->pitch);
+    S.hlo = take(sizeof(float4) * (size_t)S.plane);
+    S.hhi = take(sizeof(float4) * (size_t)S.plane);
+    S.A = take(sizeof(float4) * 3 * (size_t)S.plane);
+    S.B = take(sizeof(float4) * 3 * (size_t)S.plane);
+    S.rec = take(sizeof(double) * kNR * (size_t)S.nrec * (pso->P > 1 ? pso->P : 1));
+    S.mm = take(sizeof(unsigned) * 2);
+    S.hist = take(sizeof(int64_t) * 256);
+    S.vcnt = take(sizeof(int64_t) * 256);
+    S.fhws = take(fcm_hist_ws_bytes(256));
+    S.c0 = take(sizeof(float) * 4);
+    S.cprev = take(sizeof(float) * 4);
+    S.c1 = take(sizeof(float) * 4);
+    S.cent = take(sizeof(float) * 4);
+    S.lamxi = take(sizeof(double) * 2);
+    S.stats = take(sizeof(double) * 4);
+    S.fstats = take(sizeof(double) * 4);
+    S.status = take(sizeof(int) * 4);
+    S.total = o;
+    return S;
+}
+int slice_check(pifcm_ctx *ctx, int32_t nx, int32_t ny, int32_t nz, int32_t z, const pifcm_ifcm_cfg *cfg,
+                const pifcm_pso_cfg *pso, pifcm_grid *sg) {
+    if (nx < 1 || ny < 1 || nz < 1) return fail(ctx, PIFCM_EINVAL, "grid dims must be >= 1");
+    if (z < 0 || z >= nz) return fail(ctx, PIFCM_EINVAL, "slice z = %d outside [0, %d)", z, nz);
+    *sg = pifcm_grid{nx, ny, 1, (nx + 3) / 4 * 4, z, nz};
+    int r;
+    if ((r = check_slab(ctx, sg)) || (r = check_cfg(ctx, cfg)) || (r = check_pso(ctx, pso))) return r;
+    if (cfg->v != 1) return fail(ctx, PIFCM_EINVAL, "slice mode: v = 1 (one neighbour plane per side)");
+    if (pso->fitness_mode != PIFCM_FIT_CHAINED) return fail(ctx, PIFCM_EINVAL, "slice mode: CHAINED fitness");
+    if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
+        return fail(ctx, PIFCM_EINVAL, "slice mode is single-process");
+    return PIFCM_OK;
+}
+}  // namespace
+
+int pifcm_segment_slice_workspace_size(int32_t nx, int32_t ny, int32_t nz, int32_t z, const pifcm_ifcm_cfg *cfg,
+                                       const pifcm_pso_cfg *pso, size_t *bytes) {
+    if (!bytes) return PIFCM_EINVAL;
+    pifcm_grid sg;
+    int r = slice_check(nullptr, nx, ny, nz, z, cfg, pso, &sg);
+    if (r) return r;
+    *bytes = slice_layout(&sg, cfg, pso).total;
+    return PIFCM_OK;
+}
+
+int pifcm_segment_slice(pifcm_ctx *ctx, const uint8_t *vol, int32_t nx, int32_t ny, int32_t nz, int32_t z,
+                        const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes,
+                        uint8_t *labels, float *U_out, pifcm_report *rep, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    pifcm_grid sg;
+    int r = slice_check(ctx, nx, ny, nz, z, cfg, pso, &sg);
+    if (r) return r;
+    if (!vol || !labels) return fail(ctx, PIFCM_EINVAL, "vol and labels must be non-NULL");
+    const SliceLayout S = slice_layout(&sg, cfg, pso);
+    if ((r = check_ws(ctx, ws, ws_bytes, S.total))) return r;
+    CK(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    cudaEvent_t *ev = ctx->ev;
+    const long long plane = S.plane, N = plane * nz;
+    const int pitch = sg.pitch;
+    float *xs = at<float>(ws, S.xs);
+    float4 *hlo = at<float4>(ws, S.hlo), *hhi = at<float4>(ws, S.hhi), *A = at<float4>(ws, S.A),
+           *B = at<float4>(ws, S.B);
+    unsigned *mm = at<unsigned>(ws, S.mm);
+    int *status = at<int>(ws, S.status);
+    const bool lo_in = z > 0, hi_in = z + 1 < nz;
+    CK(ctx, cudaEventRecord(ev[0], st));
+    CK(ctx, cudaMemsetAsync(status, 0, sizeof(int) * 4, st));
+    // Alg. 2 step 1: the volume's range; x of planes z - 1, z, z + 1 (0 outside)
+    LAUNCH(ctx, 2, launch_minmax(vol, PIFCM_U8, N, mm, st));
+    for (int k = 0; k < 3; ++k) {
+        const int gz = z - 1 + k;
+        float *xk = xs + (size_t)k * ny * pitch;
+        if (gz < 0 || gz >= nz)
+            CK(ctx, cudaMemsetAsync(xk, 0, sizeof(float) * (size_t)ny * pitch, st));
+        else
+            LAUNCH(ctx, 1, launch_normalize(vol + (long long)gz * plane, PIFCM_U8, nx, ny, 1, pitch, mm, xk, st));
+    }
+    // Alg. 1 steps 1-2: R15 histogram of the slice on the volume's levels, GMM,
+    // FCM on the slice (value histogram, R24)
+    int64_t *hist = at<int64_t>(ws, S.hist), *vcnt = at<int64_t>(ws, S.vcnt);
+    LAUNCH(ctx, 2, launch_hist(vol + (long long)z * plane, PIFCM_U8, plane, mm, hist, st));
+    float *c0 = at<float>(ws, S.c0), *cprev = at<float>(ws, S.cprev), *c1 = at<float>(ws, S.c1),
+          *cent = at<float>(ws, S.cent);
+    LAUNCH(ctx, 1, launch_gmm(hist, cfg->C, 100, c0, st));
+    float cinit[4];
+    CK(ctx, cudaMemcpyAsync(cinit, c0, sizeof cinit, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaEventRecord(ev[1], st));
+    CK(ctx, cudaMemsetAsync(vcnt, 0, sizeof(int64_t) * 256, st));
+    LAUNCH(ctx, 1, launch_value_hist(vol + (long long)z * plane, PIFCM_U8, plane, vcnt, st));
+    FcmHistArgs fa = fcm_hist_args(at<void>(ws, S.fhws), 256);
+    fa.counts = vcnt; fa.mm = mm; fa.c0 = c0; fa.max_iter = cfg->max_iter; fa.eps = cfg->eps;
+    fa.m = cfg->m; fa.inv_m1 = 1.0f / (cfg->m - 1.0f); fa.c_prev = cprev; fa.c_out = c1;
+    fa.stats = at<double>(ws, S.fstats); fa.status = status;
+    LAUNCH(ctx, 1, launch_fcm_hist(fa, cfg->C, cfg->m == 2.0f, st));
+    // the start state: slice rows from the FCM's last iteration, the fixed
+    // neighbour rows = Eq. 2 at c1 (zero outside the volume)
+    LAUNCH(ctx, 1, launch_fcm_memberships(xs + (size_t)ny * pitch, nx, ny, 1, pitch, cprev, cfg->C, cfg->m,
+                                          A + plane, st));
+    if (lo_in) LAUNCH(ctx, 1, launch_fcm_memberships(xs, nx, ny, 1, pitch, c1, cfg->C, cfg->m, hlo, st));
+    else CK(ctx, cudaMemsetAsync(hlo, 0, sizeof(float4) * plane, st));
+    if (hi_in)
+        LAUNCH(ctx, 1, launch_fcm_memberships(xs + 2 * (size_t)ny * pitch, nx, ny, 1, pitch, c1, cfg->C, cfg->m,
+                                              hhi, st));
+    else CK(ctx, cudaMemsetAsync(hhi, 0, sizeof(float4) * plane, st));
+    CK(ctx, cudaMemcpyAsync(A, hlo, sizeof(float4) * plane, cudaMemcpyDeviceToDevice, st));
+    CK(ctx, cudaMemcpyAsync(A + 2 * plane, hhi, sizeof(float4) * plane, cudaMemcpyDeviceToDevice, st));
+    CK(ctx, cudaEventRecord(ev[2], st));
+    // Alg. 1 steps 3-10: CHAINED PSO over the slice
+    const Layout &L = S.L;
+    double *rec = at<double>(ws, S.rec);
+    if ((r = pifcm_slab_pso_init(ctx, &sg, cfg, pso, reinterpret_cast<float *>(A), c1, ws, L.total, stream)))
+        return r;
+    SwarmDev s = swarm_of(ws, L);
+    float4 *slots = at<float4>(ws, L.slots);
+    for (int gen = 0; gen < pso->max_gen; ++gen) {
+        // the neighbour planes of every current state (new states carry stale halos)
+        LAUNCH(ctx, 1, launch_halo_copy(hlo, 0, slots, L.nvox, plane, L.Pl, false, st, nullptr, s.cur));
+        LAUNCH(ctx, 1, launch_halo_copy(hhi, 0, slots + 2 * plane, L.nvox, plane, L.Pl, false, st, nullptr, s.cur));
+        if ((r = pifcm_slab_pso_eval(ctx, &sg, cfg, pso, xs, ws, L.total, rec, stream))) return r;
+        if ((r = pifcm_slab_pso_finalize(ctx, &sg, cfg, pso, ws, L.total, 1, S.nrec, nullptr, rec, stream)))
+            return r;
+        if ((r = pifcm_slab_pso_update(ctx, &sg, cfg, pso, ws, L.total, stream))) return r;
+        if (pso->patience > 0 && (gen + 1) % 4 == 0) {
+            int32_t stopped = 0;
+            pifcm_pso_result tmp;
+            if ((r = pifcm_slab_pso_result_get(ctx, &sg, cfg, pso, ws, &tmp, &stopped, stream))) return r;
+            if (stopped) break;
+        }
+    }
+    pifcm_pso_result pres;
+    if ((r = pifcm_slab_pso_result_get(ctx, &sg, cfg, pso, ws, &pres, nullptr, stream))) return r;
+    CK(ctx, cudaEventRecord(ev[3], st));
+    // Alg. 1 step 11: final IFCM of the slice from the gbest state
+    if ((r = pifcm_slab_pso_gbest_state(ctx, &sg, cfg, pso, ws, reinterpret_cast<float *>(A), cent, stream)))
+        return r;
+    for (float4 *T : {A, B}) {
+        CK(ctx, cudaMemcpyAsync(T, hlo, sizeof(float4) * plane, cudaMemcpyDeviceToDevice, st));
+        CK(ctx, cudaMemcpyAsync(T + 2 * plane, hhi, sizeof(float4) * plane, cudaMemcpyDeviceToDevice, st));
+    }
+    double *lamxi = at<double>(ws, S.lamxi), *stats = at<double>(ws, S.stats);
+    LAUNCH(ctx, 1, launch_set_lamxi(lamxi, s.dhdr, st));
+    CK(ctx, cudaMemsetAsync(stats, 0, sizeof(double) * 4, st));
+    int fin_iters = cfg->max_iter;
+    for (int t = 1; t <= cfg->max_iter; ++t) {
+        const float4 *src = (t % 2 == 1) ? A : B;
+        float4 *dst = (t % 2 == 1) ? B : A;
+        if ((r = pifcm_slab_step(ctx, &sg, cfg, xs, reinterpret_cast<const float *>(src),
+                                 reinterpret_cast<float *>(dst), cent, lamxi, 1, stats, rec, stream)))
+            return r;
+        LAUNCH(ctx, 1, launch_slab_finalize(cfg->C, 1, 1, S.nrec, nullptr, rec, cent, stats, nullptr, cfg->eps,
+                                            status, st));
+        if (t % 16 == 0 || t == cfg->max_iter) {
+            double h[4];
+            CK(ctx, cudaMemcpyAsync(h, stats, sizeof h, cudaMemcpyDeviceToHost, st));
+            CK(ctx, cudaStreamSynchronize(st));
+            if (h[3] != 0.0) { fin_iters = (int)h[2]; break; }
+        }
+    }
+    const float4 *Ufin = (fin_iters % 2 == 1) ? B : A;
+    CK(ctx, cudaEventRecord(ev[4], st));
+    LAUNCH(ctx, 1, launch_argmax(Ufin + plane, plane, cfg->C, labels, st));
+    if (U_out)
+        CK(ctx, cudaMemcpyAsync(U_out, Ufin + plane, sizeof(float4) * (size_t)plane, cudaMemcpyDeviceToDevice, st));
+    CK(ctx, cudaEventRecord(ev[5], st));
+    float cfin[4];
+    int stat = 0;
+    double fst[4];
+    CK(ctx, cudaMemcpyAsync(cfin, cent, sizeof cfin, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(&stat, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaMemcpyAsync(fst, at<double>(ws, S.fstats), sizeof fst, cudaMemcpyDeviceToHost, st));
+    CK(ctx, cudaStreamSynchronize(st));
+    CK(ctx, cudaGetLastError());
+    if (stat) return fail(ctx, stat, "non-finite cost during the slice pipeline");
+    if (rep) {
+        memset(rep, 0, sizeof *rep);
+        rep->pso = pres;
+        rep->fcm_iters = (int)fst[2];
+        rep->final_iters = fin_iters;
+        for (int j = 0; j < 4; ++j) { rep->centers[j] = cfin[j]; rep->c_init[j] = cinit[j]; }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[0], ev[1]); rep->t_norm = ms * 1e-3;
+        cudaEventElapsedTime(&ms, ev[1], ev[2]); rep->t_init = ms * 1e-3;
+        cudaEventElapsedTime(&ms, ev[2], ev[3]); rep->t_pso = ms * 1e-3;
+        cudaEventElapsedTime(&ms, ev[3], ev[4]); rep->t_final = ms * 1e-3;
+        cudaEventElapsedTime(&ms, ev[0], ev[5]); rep->t_total = ms * 1e-3;
+    }
     return PIFCM_OK;
 }
 

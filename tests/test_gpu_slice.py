@@ -1,0 +1,76 @@
+"""The literal slice mode (pifcm_segment_slice, DESIGN R25; Alg. 1 input z,
+PAPER:93, 110, 144) against the oracle's orc_segment_slice_u8, through the C
+ABI: same GMM start, same FCM start, the same PSO trajectory (bit-identical
+lambda*, xi*), labels of the slice identical on >= 99.9 % of its voxels where
+the final IFCM is well conditioned."""
+import numpy as np
+import pytest
+import torch
+
+from inputs import add_noise_u8, brainweb_phantom, cube_phantom
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2002_01981_b200 import Context
+    return Context(0)
+
+
+CASES = [
+    # C, volume maker, z, P, G, seed
+    (3, lambda: cube_phantom(30, 26, 9, (0.1, 0.5, 0.9))[0], 4, 5, 3, 1),
+    (4, lambda: cube_phantom(33, 29, 7)[0], 0, 4, 3, 2),        # first plane: one neighbour plane
+    (4, lambda: cube_phantom(33, 29, 7)[0], 6, 4, 3, 3),        # last plane
+    (4, lambda: brainweb_phantom(45, 54, 45)[0], 22, 6, 4, 4),
+    (3, lambda: cube_phantom(40, 36, 1, (0.1, 0.5, 0.9))[0], 0, 6, 4, 5),  # 2D: the whole pipeline
+]
+
+
+@pytest.mark.parametrize("C,maker,z,P,G,seed", CASES)
+def test_slice_parity(ctx, orc, C, maker, z, P, G, seed):
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    vol = add_noise_u8(maker(), 7.0, seed)
+    cfg = IfcmConfig(C=C)
+    pso = PsoConfig(P=P, max_gen=G, patience=0, seed=seed)
+    lab, U, rep = ctx.segment_slice(torch.as_tensor(vol, device="cuda:0"), z, cfg, pso, want_U=True)
+    r = orc.segment_slice_u8(vol, z, C=C, P=P, max_gen=G, seed=seed)
+    assert np.abs(np.array(rep["c_init"]) - r.c_init).max() < 1e-6
+    assert abs(rep["fcm_iters"] - r.fcm_iters) <= 1
+    assert rep["lambda"] == r.lam and rep["xi"] == r.xi
+    assert rep["generations"] == G
+    assert abs(rep["J"] - r.J) <= 1e-4 * r.J
+    if min(r.lam, r.xi) > 0.95:
+        pytest.skip(f"ill-conditioned final IFCM at lambda*={r.lam:.3f}, xi*={r.xi:.3f}")
+    agree = (lab.cpu().numpy() == r.labels).mean()
+    assert agree >= 0.999, agree
+    assert np.allclose(rep["centers"], r.c, rtol=1e-3)
+
+
+def test_slice_2d_equals_segment(ctx):
+    """nz = 1: the slice mode is the whole pipeline (same kernels on the same
+    plane), labels identical."""
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    vol = add_noise_u8(cube_phantom(48, 40, 1)[0], 9.0, 7)
+    vt = torch.as_tensor(vol, device="cuda:0")
+    cfg, pso = IfcmConfig(C=4), PsoConfig(P=6, max_gen=3, patience=0, seed=5)
+    ls, _, rs = ctx.segment_slice(vt, 0, cfg, pso)
+    lv, _, rv = ctx.segment(vt, cfg, pso)
+    assert rs["lambda"] == rv["lambda"] and rs["xi"] == rv["xi"]
+    assert (ls.cpu().numpy() == lv[0].cpu().numpy()).mean() >= 0.999
+
+
+def test_slice_eval_batch_and_errors(ctx):
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    from paper_2002_01981_b200.api import PifcmError
+    vol = add_noise_u8(cube_phantom(28, 24, 6)[0], 7.0, 3)
+    vt = torch.as_tensor(vol, device="cuda:0")
+    cfg = IfcmConfig(C=4)
+    a = ctx.segment_slice(vt, 2, cfg, PsoConfig(P=5, max_gen=3, patience=0, seed=2), want_U=True)
+    b = ctx.segment_slice(vt, 2, cfg, PsoConfig(P=5, max_gen=3, patience=0, seed=2, eval_batch=2), want_U=True)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    with pytest.raises(PifcmError):
+        ctx.segment_slice(vt, 6, cfg, PsoConfig(P=5, max_gen=3))
+    with pytest.raises(PifcmError):
+        ctx.segment_slice(vt, 1, IfcmConfig(C=4, v=2), PsoConfig(P=5, max_gen=3))
