@@ -32,6 +32,10 @@ sys.path.insert(0, ROOT)
 WORKLOAD = "C3: BrainWeb-shaped 181x217x181 synthetic phantom (CSF/GM/WM), 9% noise, C=4, 26-neighbour 3D IFCM, PSO 32 particles x 30 generations"
 WORKLOAD_C5 = ("C5: 512x512x512 synthetic noisy volume (4 nested cubes, 7% noise), C=4, z-slab sharded "
                "(halo exchange + record all-gather), PSO {P} particles x 30 generations")
+WORKLOAD_C2 = ("C2: 854x854 2D synthetic noisy image (4 nested squares, 7% noise), C=4, 8-neighbour IFCM, "
+               "PSO 20 particles x 30 generations")
+# PAPER:250 (Table 7, 3DPIFCM-GPU on a TITAN X, whole algorithm, 854x854): context only
+PAPER_C2_SECONDS = 170.60
 METRIC = "voxel-iterations/s (x particles)"
 SHAPE = (181, 217, 181)  # (nz, ny, nx) with nx = 181, ny = 217, nz = 181
 C, P, GENS = 4, 32, 30
@@ -150,8 +154,9 @@ def run_reference(args, rank, world):
     import oracle
     oracle.build_oracle()
     c5 = args.workload == "C5"
-    vol = _volume("C5" if c5 else "C3")
-    workload = WORKLOAD_C5.format(P=64) if c5 else WORKLOAD
+    vol = _volume(args.workload)
+    workload = (WORKLOAD_C5.format(P=64) if c5 else
+                (WORKLOAD_C2 if args.workload == "C2" else WORKLOAD))
     x = oracle.normalize_u8(vol)
     c0 = oracle.gmm_init(oracle.histogram_u8(vol), C)
     U, c, _ = oracle.fcm_run(x, c0, max_iter=1)
@@ -203,13 +208,14 @@ def run_ours(args, rank, world, local_rank):
         dist = tdist
     ctx = Context(dev_index)
     c5 = args.workload == "C5"
-    vol = _volume("C5" if c5 else "C3")
+    c2 = args.workload == "C2"
+    vol = _volume(args.workload)
     nz, ny, nx = vol.shape
     # C5: P = 64 as configured.  The CHAINED slot pool is 2P + 1 slab states
     # (129 x 2.16 GB at one GPU); where that does not fit, the particles are
     # evaluated in batches of eval_batch states over P + eval_batch + 1 slots
     # (bit-identical results, pifcm_pso_cfg.eval_batch)
-    Pw = 64 if c5 else P
+    Pw = 64 if c5 else (20 if c2 else P)
     Pw = _env_int("PIFCM_BENCH_P", Pw)  # test hook (a smaller swarm), reported in config
     eval_batch = 0
     if c5:
@@ -218,7 +224,7 @@ def run_ours(args, rank, world, local_rank):
         avail = free - 8 * slot - (2 << 30)  # slab IFCM states, x, volume, labels, records
         if (2 * Pw + 1) * slot > avail:
             eval_batch = max(1, int(avail // slot) - Pw - 1)
-    workload = WORKLOAD_C5.format(P=Pw) if c5 else WORKLOAD
+    workload = WORKLOAD_C5.format(P=Pw) if c5 else (WORKLOAD_C2 if c2 else WORKLOAD)
     cfg = IfcmConfig(C=C, m=2.0, q_mode=0, eps=1e-5, max_iter=100)
     pso = PsoConfig(P=Pw, ring_k=1, max_gen=GENS, patience=0, seed=12345, eval_batch=eval_batch)
     vol_d = torch.as_tensor(vol, device=dev)
@@ -325,7 +331,7 @@ def run_ours(args, rank, world, local_rank):
     hbm, hbm_kind = _peaks()
     achieved = (k_bytes / k_n) / ((k_ms / k_n) * 1e-3) / 1e9 if k_n else None
     traffic = None
-    if not c5:  # the committed ncu capture is of the C3 P = 32 launch
+    if not c5 and not c2:  # the committed ncu capture is of the C3 P = 32 launch
         try:
             with open(PROFILE_SUMMARY) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
@@ -345,7 +351,8 @@ def run_ours(args, rank, world, local_rank):
         else:   # whole volume, this rank's particles
             vox = float(nx * ny * nz)
             p_launch = (k_bytes / k_n - 4.0 * vox) / (32.0 * vox)
-        instr_per_vp = 245.0 + 52.0 / max(p_launch, 1.0)
+        # (2D, 8 neighbours: SURVEY 8(d) counts ~110)
+        instr_per_vp = 245.0 + 52.0 / max(p_launch, 1.0) if nz > 1 else 110.0
         vp_per_s = p_launch * vox / ((k_ms / k_n) * 1e-3)
         peak_alu = 148 * 128 * 1.965e9 / 1e12
         alu_view = {"bound": "alu", "achieved": vp_per_s * instr_per_vp / 1e12, "peak": peak_alu,
@@ -384,6 +391,9 @@ def run_ours(args, rank, world, local_rank):
             "fcm_iters": last["fcm_iters"], "final_iters": last["final_iters"],
             "lambda_star": last["lambda"], "xi_star": last["xi"],
         },
+        **({"paper_context": {"what": "PAPER:250 Table 7: 3DPIFCM-GPU on a TITAN X, whole algorithm, 854x854 "
+                                      "(particles / generations not stated)", "seconds": PAPER_C2_SECONDS,
+                              "ours_seconds": ms_max / args.steps * 1e-3}} if c2 else {}),
         "roofline": {
             "bound": "hbm",
             "kernel": ("k_step_stencil, one launch = one PSO generation (all P particles' fused IFCM steps"
@@ -427,8 +437,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--workload", default="C3", choices=["C3", "C5"],
-                    help="C3 (default, the BASELINE metric's config) or C5 (512^3, z-slab sharded)")
+    ap.add_argument("--workload", default="C3", choices=["C3", "C2", "C5"],
+                    help="C3 (default, the BASELINE metric's config), C2 (854x854 2D, the paper's Table 7 "
+                         "image) or C5 (512^3, z-slab sharded)")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)

@@ -13,3 +13,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step_stencil -s 1 -c 1 \
     -f -o gpurun_out/kstep_${TAG} python tools/profile_step.py eval 2 > gpurun_out/ncu_full_${TAG}.log 2>&1
 tail -3 gpurun_out/ncu_full_${TAG}.log
+timeout 900 python bench.py --workload C5 --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_c5_${TAG}.json 2> gpurun_out/bench_c5_${TAG}.err
+tail -c 1500 gpurun_out/bench_c5_${TAG}.json
+timeout 600 python bench.py --workload C2 --steps 5 --warmup 3 > gpurun_out/bench_c2_${TAG}.json 2> gpurun_out/bench_c2_${TAG}.err
+tail -c 1500 gpurun_out/bench_c2_${TAG}.json
