@@ -46,6 +46,10 @@ constexpr int kStages = 4;          // plane ring: z-1, z, z+1 resident, z+2 lan
 constexpr int kTZ = PIFCM_TZ;       // planes per CTA (z-chunk) for deep grids
 constexpr int kTZMin = 8;           // smallest z-chunk used to fill a wave
 constexpr int kStepThreads = kTX * kWarpsY;
+#ifndef PIFCM_TYB2D
+#define PIFCM_TYB2D 4
+#endif
+constexpr int kTYB2D = PIFCM_TYB2D;  // 2D step: tiles per CTA (a column in y)
 
 // Pointwise (FCM, lambda = xi = 0) step.
 constexpr int kPwThreads = 256;

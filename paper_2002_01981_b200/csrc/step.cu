@@ -483,6 +483,203 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
 }
 
 // ----------------------------------------------------------------------------
+// 2D step (nz = 1: the 8-neighbourhood of Eq. 9 in one plane -- the paper's
+// Table 7 images, config C2).  The 3D kernel would stream two zero-filled
+// neighbour planes through its ring and spend two thirds of its Eq. 5 work on
+// them; here one TMA load brings the haloed tile, Eq. 5 runs over the three
+// in-plane columns only and the Eq. 7 numerator is the in-plane sum S of
+// plane_SR (faces W1 = 1, corners W2).  The epilogue is the 3D kernel's.
+#ifndef PIFCM_2D_MINBLOCKS
+#define PIFCM_2D_MINBLOCKS 4
+#endif
+// A CTA walks a column of kTYB2D tiles in y, the next tile's TMA load in
+// flight while the current one is computed (two smem buffers).
+template <int C, bool M2, bool DU>
+__global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
+    k_step_2d(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, const StepArgs a) {
+    constexpr int NP = (C + 1) / 2;
+    // TMA destinations: 128-byte aligned stages (as the 3D ring)
+    __shared__ __align__(128) unsigned char sbuf[2 * (kUStagePad + kXStagePad)];
+    __shared__ __align__(8) uint64_t bar[2];
+    float4 *sUb[2] = {reinterpret_cast<float4 *>(sbuf), reinterpret_cast<float4 *>(sbuf + kUStagePad)};
+    float *sXb[2] = {reinterpret_cast<float *>(sbuf + 2 * kUStagePad),
+                     reinterpret_cast<float *>(sbuf + 2 * kUStagePad + kXStagePad)};
+    const int p = blockIdx.z;
+    if (a.stop && *a.stop) return;
+    if (a.stats && a.stats[4 * p + 3] != 0.0) return;
+    const int txi = blockIdx.x % a.tiles_x;
+    const int ty0 = (blockIdx.x / a.tiles_x) * kTYB2D;
+    const int ntile = min(kTYB2D, a.tiles_y - ty0);
+    const int x0 = txi * kTX;
+    const int tid = threadIdx.x;
+    const int tx = tid & 31, ty = tid >> 5;
+    const int slot = a.in_idx ? a.in_idx[p] : p;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int k) {
+        const int b = k & 1, y0k = (ty0 + k) * kTY;
+        mbar_expect_tx(&bar[b], kUStageBytes + kXStageBytes);
+        tma_load_4d(sUb[b], &tmU, &bar[b], 4 * (x0 - 1), y0k - 1, 0, slot);
+        tma_load_3d(sXb[b], &tmX, &bar[b], x0 - kXOff, y0k - 1, 0);
+    };
+    if (tid == 0) {
+        issue(0);
+        if (ntile > 1) issue(1);
+    }
+    float4 *Uout = a.U_out + (long long)(a.out_idx ? a.out_idx[p] : p) * a.nvox;
+    float2 c2[2];
+    c2[0] = make_float2(a.centers[4 * p + 0], a.centers[4 * p + 1]);
+    c2[1] = make_float2(a.centers[4 * p + 2], a.centers[4 * p + 3]);
+    const float lam = (float)a.lam_xi[2 * p], xi = (float)a.lam_xi[2 * p + 1];
+    const float2 nlam2 = make_float2(-lam, -lam), nxi2 = make_float2(-xi, -xi);
+    const float w2 = a.q_mode == 0 ? 4.0f : 2.0f, w3 = a.q_mode == 0 ? 9.0f : 3.0f;  // Eq. 7 q2 (R1)
+    const float2 w22 = make_float2(w2, w2), w32 = make_float2(w3, w3);
+    const int gx = x0 + tx;
+    const int px = (gx > 0) + (gx < a.nx - 1);
+    float2 num2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float2 den2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float Jacc = 0.f, duacc = 0.f;
+
+    for (int k = 0; k < ntile; ++k) {
+        const int b = k & 1;
+        const float4 *sU = sUb[b];
+        const float *sX = sXb[b];
+        const int y0 = (ty0 + k) * kTY;
+        float invQ[kRY];
+        unsigned vmask = 0u;
+#pragma unroll
+        for (int r = 0; r < kRY; ++r) {
+            const int gy = y0 + ty * kRY + r;
+            const int py = (gy > 0) + (gy < a.ny - 1);
+            const float Qs = (float)(px + py) + w2 * (float)(px * py);  // Eq. 7 denominator, pz = 0
+            invQ[r] = Qs > 0.f ? 1.0f / Qs : 0.f;
+            if (gx < a.nx && gy < a.ny) vmask |= 1u << r;
+        }
+        mbar_wait(&bar[b], (k >> 1) & 1);
+
+        float xr[kRY];
+#pragma unroll
+        for (int r = 0; r < kRY; ++r) xr[r] = sX[(ty * kRY + 1 + r) * kSXP + tx + kXOff];
+        // Eq. 5 numerators over the 8 in-plane neighbours: every loaded row
+        // updates up to 3 of the thread's voxels; g (Eq. 6) two voxels per FADD2
+        float2 hn[kRY][NP];
+#pragma unroll
+        for (int r = 0; r < kRY; ++r)
+#pragma unroll
+            for (int q = 0; q < NP; ++q) hn[r][q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx)
+#pragma unroll
+            for (int t = 0; t < kRY + 2; ++t) {
+                const float4 uk4 = sU[(ty * kRY + t) * kSX + tx + 1 + dx];
+                const float xk = sX[(ty * kRY + t) * kSXP + tx + kXOff + dx];
+                const float2 u01 = make_float2(uk4.x, uk4.y), u23 = make_float2(uk4.z, uk4.w);
+                float gv[kRY];
+#pragma unroll
+                for (int r = 0; r < kRY; r += 2) {
+                    const int dy0 = t - 1 - r, dy1 = t - 2 - r;
+                    const bool v0 = dy0 >= -1 && dy0 <= 1 && !(dx == 0 && dy0 == 0);
+                    const bool v1 = dy1 >= -1 && dy1 <= 1 && !(dx == 0 && dy1 == 0);
+                    if (v0 && v1) {
+                        const float2 d = __fadd2_rn(make_float2(xr[r], xr[r + 1]), make_float2(-xk, -xk));
+                        gv[r] = d.x;
+                        gv[r + 1] = d.y;
+                    } else if (v0) {
+                        gv[r] = xr[r] - xk;
+                    } else if (v1) {
+                        gv[r + 1] = xr[r + 1] - xk;
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < kRY; ++r) {
+                    const int dy = t - 1 - r;
+                    if (dy < -1 || dy > 1) continue;
+                    if (dx == 0 && dy == 0) continue;  // Eq. 9: k != i
+                    const float g = fabsf(gv[r]);
+                    const float2 g2 = make_float2(g, g);
+                    hn[r][0] = __ffma2_rn(u01, g2, hn[r][0]);
+                    if (NP > 1) hn[r][NP - 1] = __ffma2_rn(u23, g2, hn[r][NP - 1]);
+                }
+            }
+        // Eq. 7 numerator: the in-plane sum S = W1 E + W2 K of v = u^2
+        float2 Fn[kRY][NP], Rd[kRY][NP], dummy[kRY][NP];
+        plane_SR<NP, 0>(sU, ty, tx, w22, w32, Fn, Rd, dummy);
+
+        float4 *Urow = Uout + (long long)(y0 + ty * kRY) * a.nx + gx;
+        unsigned band_bits = 0u;
+#pragma unroll
+        for (int r = 0; r < kRY; ++r) {
+            float G = hn[r][0].x + hn[r][0].y;
+            if (C > 2) G += hn[r][NP - 1].x;
+            if (C > 3) G += hn[r][NP - 1].y;  // = sum_k g_ik (rows of U sum to 1)
+            const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
+            float2 A[2], Ar[2];
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const float2 H = __fmul2_rn(hn[r][q], make_float2(invG, invG));          // Eq. 5
+                const float2 F = __fmul2_rn(Fn[r][q], make_float2(invQ[r], invQ[r]));    // Eq. 7
+                Ar[q] = __ffma2_rn(H, nlam2, __ffma2_rn(F, nxi2, make_float2(1.f, 1.f))); // Eq. 4
+                A[q].x = fmaxf(Ar[q].x, kAFloor);                                          // R4
+                A[q].y = fmaxf(Ar[q].y, kAFloor);
+            }
+            if (NP == 1) { A[1] = make_float2(1.f, 1.f); Ar[1] = A[1]; }
+            const Memb mb = memb_compute<C, M2>(xr[r], c2, A, a.m, a.inv_m1, Ar);
+            const bool valid = (vmask >> r) & 1u;
+            const bool band = valid && !(mb.K <= kKMax);  // ill-conditioned: fp64 pass below
+            band_bits |= band ? (1u << r) : 0u;
+            if (valid && !band) {
+                memb_accumulate<C, M2>(mb, xr[r], a.m, num2, den2, Jacc);
+                const float4 un = make_float4(mb.u[0], mb.u[1], mb.u[2], mb.u[3]);
+                if (DU) {
+                    const float4 uo = sU[(ty * kRY + 1 + r) * kSX + tx + 1];
+                    duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
+                                               fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
+                }
+                Urow[(long long)r * a.nx] = un;
+            }
+        }
+        // ill-conditioned voxels: the warp re-evaluates them in fp64 (nz = 1:
+        // the out-of-plane neighbours are out of bounds and never read)
+        unsigned lanes = __ballot_sync(0xffffffffu, band_bits != 0u);
+        while (lanes) {
+            const int L = __ffs(lanes) - 1;
+            lanes &= lanes - 1;
+            unsigned bits = __shfl_sync(0xffffffffu, band_bits, L);
+            while (bits) {
+                const int r = __ffs(bits) - 1;
+                bits &= bits - 1;
+                const int row = ty * kRY + 1 + r;
+                const int gxL = x0 + L, gy = y0 + ty * kRY + r;
+                const float4 a4 = attraction_coop<C>(sU, sU, sU, sX, sX, sX, row, L, gxL, gy, 0, a.nx, a.ny, 1,
+                                                     a.lam_xi[2 * p], a.lam_xi[2 * p + 1], w2, w3);
+                if (tx == L) {
+                    const float2 A[2] = {make_float2(a4.x, a4.y), make_float2(a4.z, a4.w)};
+                    const float xv = sX[row * kSXP + L + kXOff];
+                    const float4 un = membership2<C, M2>(xv, c2, A, a.m, a.inv_m1, num2, den2, Jacc);
+                    if (DU) {
+                        const float4 uo = sU[row * kSX + L + 1];
+                        duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
+                                                   fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
+                    }
+                    Uout[(long long)gy * a.nx + gxL] = un;
+                }
+            }
+        }
+        // every warp is done with buffer b: refill it with tile k + 2
+        __syncthreads();
+        if (tid == 0 && k + 2 < ntile) issue(k + 2);
+    }
+    float num[kMaxC] = {num2[0].x, num2[0].y, num2[1].x, num2[1].y};
+    float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
+    block_partials<kWarpsY>(num, den, Jacc, duacc, a.partials + ((long long)p * a.nblk + blockIdx.x) * kNR);
+    finalize_if_last<kStepThreads>(a, p, a.nblk);
+}
+
+// ----------------------------------------------------------------------------
 // Pointwise step for lambda = xi = 0 (plain FCM, Alg. 2 step 5):
 // Eq. 4 reduces to (x_i - c_j)^2, no neighbourhood is read.
 template <int C, bool M2>
@@ -600,6 +797,7 @@ int slab_tz(int nx, int ny, int nz) {
 int step_nblk(int nx, int ny, int nz, bool stencil, int P) {
     if (!stencil) return pw_blocks((long long)nx * ny * nz);
     const int tx = (nx + kTX - 1) / kTX, ty = (ny + kTY - 1) / kTY;
+    if (nz == 1) return tx * ((ty + kTYB2D - 1) / kTYB2D);  // k_step_2d: columns of kTYB2D tiles
     return tx * ty * step_zchunks(nx, ny, nz, P);
 }
 
@@ -662,8 +860,19 @@ static cudaError_t launch_stencil(const StepArgs &a, int P, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+template <int C, bool M2, bool DU>
+static cudaError_t launch_2d(const StepArgs &a, int P, cudaStream_t st) {
+    CUtensorMap mU, mX;
+    if (!make_maps(a, &mU, &mX)) return cudaErrorInvalidValue;
+    dim3 grid(a.tiles_x * ((a.tiles_y + kTYB2D - 1) / kTYB2D), 1, P);
+    k_step_2d<C, M2, DU><<<grid, kStepThreads, 0, st>>>(mU, mX, a);
+    return cudaGetLastError();
+}
+
 template <int C, bool M2>
 static cudaError_t launch_t(const StepArgs &a, bool stencil, int P, cudaStream_t st) {
+    if (stencil && a.nz == 1 && a.nz_g == 1 && !a.hf)  // a plain 2D image (8-neighbourhood)
+        return a.want_du ? launch_2d<C, M2, true>(a, P, st) : launch_2d<C, M2, false>(a, P, st);
     if (stencil) {
         if (a.hf) return M2 ? launch_stencil<C, true, false, true>(a, P, st) : cudaErrorInvalidValue;
         return a.want_du ? launch_stencil<C, M2, true>(a, P, st) : launch_stencil<C, M2, false>(a, P, st);
@@ -699,6 +908,8 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
         a.zchunks = (a.nz_t + a.tz - 1) / a.tz;
         a.nblk = a.tiles_x * a.tiles_y * a.zchunks;
     }
+    if (stencil && a.nz == 1 && a.nz_g == 1 && !a.hf && a.v == 1)  // plain 2D image: k_step_2d's blocks
+        a.nblk = step_nblk(a.nx, a.ny, 1, true, P);
     if (stencil && a.v == 2) return launch_step_v2(a, C, P, st);
     const bool m2 = (a.m == 2.0f) || a.hf != nullptr;  // the H, F pass does not depend on m
     switch (C) {

@@ -53,7 +53,9 @@ CASES = [
     ((1, 1, 1), 2, 2.0, 0),         # no neighbours: H = F = 0
     ((7, 1, 1), 3, 2.0, 0),         # a line along z
     ((1, 40, 1), 2, 2.0, 1),
-    ((1, 96, 97), 4, 2.0, 0),       # 2D, 8-neighbourhood
+    ((1, 96, 97), 4, 2.0, 0),       # 2D, 8-neighbourhood (k_step_2d)
+    ((1, 70, 130), 3, 1.5, 1),      # 2D, several tiles, ragged, general m
+    ((1, 140, 41), 4, 2.0, 0),      # 2D, 9 tile rows: CTA columns of 4 + 4 + 1 tiles
 ]
 
 
