@@ -576,10 +576,14 @@ __device__ __forceinline__ void block_sum_vec(double (&v)[NV], double (*sh)[NV])
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max_iter, float *c0) {
+// C is a template parameter so that the per-component work of a bin (the
+// exp, the normalisation, the moments) is unrolled: the C chains run
+// interleaved instead of back to back (the loop is latency-bound, one block).
+template <int C>
+__global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int max_iter, float *c0) {
     __shared__ double sh1[8][2 * kMaxC + 2];
     __shared__ double sh2[8][kMaxC];
-    double mu[kMaxC], s2[kMaxC], w[kMaxC];
+    double mu[C], s2[C], w[C];
     const int b = threadIdx.x;
     const double y = (double)b / 255.0;
     const double n = (double)hist[b];
@@ -594,7 +598,9 @@ __global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max
         if (threadIdx.x < C) c0[threadIdx.x] = (float)((double)threadIdx.x / (double)(C - 1));
         return;
     }
-    for (int j = 0; j < kMaxC; ++j) {
+    const double invN = 1.0 / Ntot;
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
         mu[j] = ((double)j + 0.5) / (double)C;
         s2[j] = 1.0 / (4.0 * (double)C * (double)C);
         w[j] = 1.0 / (double)C;
@@ -602,8 +608,9 @@ __global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max
     const double two_pi = 6.283185307179586476925286766559;
     for (int it = 0; it < max_iter; ++it) {
         // E step: responsibilities of this bin (R15)
-        double r[kMaxC];
+        double r[C];
         double sum = 0.0;
+#pragma unroll
         for (int j = 0; j < C; ++j) {
             const double d = y - mu[j];
             r[j] = w[j] * exp(-d * d / (2.0 * s2[j])) / sqrt(two_pi * s2[j]);
@@ -611,26 +618,35 @@ __global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max
         }
         if (!(sum > 0.0)) {
             int jb = 0;
+#pragma unroll
             for (int j = 1; j < C; ++j)
                 if (fabs(y - mu[j]) < fabs(y - mu[jb])) jb = j;
+#pragma unroll
             for (int j = 0; j < C; ++j) r[j] = (j == jb) ? 1.0 : 0.0;
             sum = 1.0;
         }
+        const double isum = 1.0 / sum;
         double v1[2 * kMaxC + 2];
 #pragma unroll
         for (int i = 0; i < 2 * kMaxC + 2; ++i) v1[i] = 0.0;
+#pragma unroll
         for (int j = 0; j < C; ++j) {
-            const double rr = (n > 0.0) ? r[j] / sum : 0.0;
+            const double rr = (n > 0.0) ? r[j] * isum : 0.0;
             r[j] = rr;
             v1[j] = n * rr;              // N_j
             v1[kMaxC + j] = n * rr * y;  // sum y
         }
         block_sum_vec<2 * kMaxC + 2>(v1, sh1);
-        double newmu[kMaxC];
-        for (int j = 0; j < C; ++j) newmu[j] = (v1[j] > 1e-12) ? v1[kMaxC + j] / v1[j] : mu[j];
+        double newmu[C], iN[C];
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+            iN[j] = v1[j] > 1e-12 ? 1.0 / v1[j] : 0.0;
+            newmu[j] = (v1[j] > 1e-12) ? v1[kMaxC + j] * iN[j] : mu[j];
+        }
         double v2[kMaxC];
 #pragma unroll
         for (int j = 0; j < kMaxC; ++j) v2[j] = 0.0;
+#pragma unroll
         for (int j = 0; j < C; ++j) {
             const double d = y - newmu[j];
             v2[j] = n * r[j] * d * d;
@@ -638,10 +654,11 @@ __global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max
         block_sum_vec<kMaxC>(v2, sh2);
         // M step (every thread holds the same sums, so every thread updates)
         double shift = 0.0;
+#pragma unroll
         for (int j = 0; j < C; ++j) {
             if (v1[j] > 1e-12) {
-                w[j] = v1[j] / Ntot;
-                s2[j] = fmax(v2[j] / v1[j], 1e-6);
+                w[j] = v1[j] * invN;
+                s2[j] = fmax(v2[j] * iN[j], 1e-6);
             }
             shift = fmax(shift, fabs(newmu[j] - mu[j]));
             mu[j] = newmu[j];
@@ -649,7 +666,8 @@ __global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max
         if (shift < 1e-9) break;
     }
     if (threadIdx.x == 0) {
-        double m[kMaxC];
+        double m[C];
+#pragma unroll
         for (int j = 0; j < C; ++j) m[j] = mu[j];
         for (int i = 1; i < C; ++i) {
             const double t = m[i];
@@ -666,7 +684,12 @@ __global__ void __launch_bounds__(256) k_gmm(const int64_t *hist, int C, int max
 }
 
 cudaError_t launch_gmm(const int64_t *hist, int C, int max_iter, float *c0, cudaStream_t st) {
-    k_gmm<<<1, 256, 0, st>>>(hist, C, max_iter, c0);
+    switch (C) {
+        case 2: k_gmm<2><<<1, 256, 0, st>>>(hist, max_iter, c0); break;
+        case 3: k_gmm<3><<<1, 256, 0, st>>>(hist, max_iter, c0); break;
+        case 4: k_gmm<4><<<1, 256, 0, st>>>(hist, max_iter, c0); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 

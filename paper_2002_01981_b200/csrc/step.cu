@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
 // in-plane columns only and the Eq. 7 numerator is the in-plane sum S of
 // plane_SR (faces W1 = 1, corners W2).  The epilogue is the 3D kernel's.
 #ifndef PIFCM_2D_MINBLOCKS
-#define PIFCM_2D_MINBLOCKS 4
+#define PIFCM_2D_MINBLOCKS 5
 #endif
 // A CTA walks a column of kTYB2D tiles in y, the next tile's TMA load in
 // flight while the current one is computed (two smem buffers).
