@@ -32,6 +32,8 @@ sys.path.insert(0, ROOT)
 WORKLOAD = "C3: BrainWeb-shaped 181x217x181 synthetic phantom (CSF/GM/WM), 9% noise, C=4, 26-neighbour 3D IFCM, PSO 32 particles x 30 generations"
 WORKLOAD_C5 = ("C5: 512x512x512 synthetic noisy volume (4 nested cubes, 7% noise), C=4, z-slab sharded "
                "(halo exchange + record all-gather), PSO {P} particles x 30 generations")
+WORKLOAD_C4 = ("C4: batch of 16 BrainWeb-shaped 181x217x181 volumes (seeds 100..115, noise 3/5/7/9%), C=4, "
+               "26-neighbour 3D IFCM, PSO 32 particles x 30 generations each, particles sharded over the GPUs")
 WORKLOAD_C2 = ("C2: 854x854 2D synthetic noisy image (4 nested squares, 7% noise), C=4, 8-neighbour IFCM, "
                "PSO 20 particles x 30 generations")
 # PAPER:250 (Table 7, 3DPIFCM-GPU on a TITAN X, whole algorithm, 854x854): context only
@@ -209,6 +211,7 @@ def run_ours(args, rank, world, local_rank):
     ctx = Context(dev_index)
     c5 = args.workload == "C5"
     c2 = args.workload == "C2"
+    c4 = args.workload == "C4"
     vol = _volume(args.workload)
     nz, ny, nx = vol.shape
     # C5: P = 64 as configured.  The CHAINED slot pool is 2P + 1 slab states
@@ -224,7 +227,7 @@ def run_ours(args, rank, world, local_rank):
         avail = free - 8 * slot - (2 << 30)  # slab IFCM states, x, volume, labels, records
         if (2 * Pw + 1) * slot > avail:
             eval_batch = max(1, int(avail // slot) - Pw - 1)
-    workload = WORKLOAD_C5.format(P=Pw) if c5 else (WORKLOAD_C2 if c2 else WORKLOAD)
+    workload = WORKLOAD_C5.format(P=Pw) if c5 else (WORKLOAD_C2 if c2 else (WORKLOAD_C4 if c4 else WORKLOAD))
     cfg = IfcmConfig(C=C, m=2.0, q_mode=0, eps=1e-5, max_iter=100)
     pso = PsoConfig(P=Pw, ring_k=1, max_gen=GENS, patience=0, seed=12345, eval_batch=eval_batch)
     vol_d = torch.as_tensor(vol, device=dev)
@@ -263,6 +266,39 @@ def run_ours(args, rank, world, local_rank):
         def step_host():
             return ctx.segment_host(vol_h, cfg, pso, ws, lab_h)
 
+    if c4:  # one step = the whole batch of 16 volumes, one segmentation each
+        from inputs import config_volume
+        vols = [config_volume("C4", k=k)[0] for k in range(16)]
+        vols_d = [torch.as_tensor(v, device=dev) for v in vols]
+        vols_h = [torch.as_tensor(v).pin_memory() for v in vols]
+        one_dev, one_host = step, step_host
+
+        def _merge(rs):
+            out = dict(rs[-1])
+            out["units"] = sum(r["fcm_iters"] + Pw * r["generations"] + r["final_iters"] for r in rs)
+            out["t_pso"] = sum(r["t_pso"] for r in rs)
+            out["t_total"] = sum(r["t_total"] for r in rs)
+            return out
+
+        def step():
+            nonlocal vol_d
+            rs = []
+            for v in vols_d:
+                vol_d = v
+                rs.append(one_dev())
+            return _merge(rs)
+
+        def step_host():
+            nonlocal vol_h
+            rs = []
+            for v in vols_h:
+                vol_h = v
+                rs.append(one_host())
+            return _merge(rs)
+
+    def units(r):
+        return r["units"] if "units" in r else r["fcm_iters"] + Pw * r["generations"] + r["final_iters"]
+
     # ---- warm-up
     rep = None
     for _ in range(args.warmup):
@@ -298,7 +334,7 @@ def run_ours(args, rank, world, local_rank):
     s_ms, s_n, s_bytes = ctx.timing_read(batched=False)    # final IFCM: one state per launch
     ctx.timing_enable(False)
     for r in reps:
-        vp = nx * ny * nz * (r["fcm_iters"] + Pw * r["generations"] + r["final_iters"])
+        vp = nx * ny * nz * units(r)
         vp_total += vp
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -314,7 +350,7 @@ def run_ours(args, rank, world, local_rank):
     vp_e2e = 0.0
     for _ in range(args.steps):
         r = step_host()
-        vp_e2e += nx * ny * nz * (r["fcm_iters"] + Pw * r["generations"] + r["final_iters"])
+        vp_e2e += nx * ny * nz * units(r)
     h1.record(stream)
     barrier()
     te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
@@ -419,7 +455,8 @@ def run_ours(args, rank, world, local_rank):
         },
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "voxel-iterations/s (x particles)",
-                "h2d_bytes_per_step": int(vol.size), "d2h_bytes_per_step": int(vol.size)},
+                "h2d_bytes_per_step": int(vol.size) * (16 if c4 else 1),
+                "d2h_bytes_per_step": int(vol.size) * (16 if c4 else 1)},
         "gpu_launches": launches,
         "clocks": clk,
     }
@@ -437,9 +474,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--workload", default="C3", choices=["C3", "C2", "C5"],
+    ap.add_argument("--workload", default="C3", choices=["C3", "C2", "C4", "C5"],
                     help="C3 (default, the BASELINE metric's config), C2 (854x854 2D, the paper's Table 7 "
-                         "image) or C5 (512^3, z-slab sharded)")
+                         "image), C4 (16 C3-shaped volumes per step) or C5 (512^3, z-slab sharded)")
     args = ap.parse_args()
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)

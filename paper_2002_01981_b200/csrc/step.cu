@@ -47,6 +47,9 @@ constexpr int kStepMinBlocks = PIFCM_STEP_MINBLOCKS;  // CTAs per SM the registe
 #define PIFCM_RING 5
 #endif
 constexpr int kRing = PIFCM_RING;  // planes in flight: z-1, z, z+1 in use, the rest prefetching
+#ifndef PIFCM_FOLD
+#define PIFCM_FOLD 1  // 3D step: Eq. 5 / Eq. 7 denominators folded into the Eq. 4 weights (+0.6 %)
+#endif
 constexpr int kStencilSmem = kRing * (kUStagePad + kXStagePad) + 128;
 
 // Warp-cooperative fp64 re-evaluation of the Eq. 4 factors of one voxel (the
@@ -409,11 +412,21 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
                 }
                 continue;
             }
+#if PIFCM_FOLD
+            // Eq. 4 with the Eq. 5 / Eq. 7 denominators folded into the
+            // weights: a = 1 + Hn (-lam / G) + Fn (-xi / Qs)
+            const float sl = -lam * invG, sx = -xi * invQ[r];
+#endif
 #pragma unroll
             for (int q = 0; q < NP; ++q) {
+#if PIFCM_FOLD
+                Ar[q] = __ffma2_rn(hn[r][q], make_float2(sl, sl),
+                                   __ffma2_rn(Fn[r][q], make_float2(sx, sx), make_float2(1.f, 1.f)));
+#else
                 const float2 H = __fmul2_rn(hn[r][q], make_float2(invG, invG));          // Eq. 5
                 const float2 F = __fmul2_rn(Fn[r][q], make_float2(invQ[r], invQ[r]));    // Eq. 7
                 Ar[q] = __ffma2_rn(H, nlam2, __ffma2_rn(F, nxi2, make_float2(1.f, 1.f))); // Eq. 4
+#endif
                 A[q].x = fmaxf(Ar[q].x, kAFloor);                                          // R4
                 A[q].y = fmaxf(Ar[q].y, kAFloor);
             }
