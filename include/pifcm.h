@@ -315,6 +315,21 @@ int pifcm_fcm_hist(pifcm_ctx *ctx, const pifcm_ifcm_cfg *cfg, int32_t dtype, con
 int pifcm_fcm_memberships(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, float m, const float *x,
                           const float *c, float *U, pifcm_stream stream);
 
+/* incS ("incorrect segmentation"; DESIGN R26) of labels
+ * against a phantom's truth: cluster j is mapped to the class of its centre's
+ * rank (ascending, ties to the lower index; classes numbered by ascending
+ * intensity level) and *count (dev int64) = the voxels whose mapped label
+ * differs from the truth (exact integer).  labels, truth dev u8 [n];
+ * centers dev fp32 [4].  Async. */
+int pifcm_incs(pifcm_ctx *ctx, const uint8_t *labels, const uint8_t *truth, int64_t n, int32_t C,
+               const float *centers, int64_t *count, pifcm_stream stream);
+/* Eq. 11, host arithmetic: J[a] = 1/k sum_i alpha q_ia +
+ * (1 - alpha) s_ia with q, s the incS and seconds of algorithm a at size i,
+ * min-max normalised over the A algorithms at each size (a constant row
+ * contributes 0).  incs, secs host [k][A]; J host [A].  PIFCM_EINVAL on bad
+ * sizes or alpha outside [0, 1]. */
+int pifcm_eq11(const double *incs, const double *secs, int32_t k, int32_t A, double alpha, double *J);
+
 /* Defuzzification (R13): labels = argmax_j u_ij, ties to the
  * lowest j.  U dev fp32 [nz][ny][nx][4], labels dev u8.  Async. */
 int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float *U,

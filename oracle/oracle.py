@@ -23,7 +23,7 @@ __all__ = [
     "normalize_u8", "histogram_u8", "normalize", "histogram", "gmm_init", "philox4x32_10", "philox_pair",
     "pso_init", "pso_move", "pso_update", "pso_run", "ifcm_run", "fcm_run", "segment_u8",
     "num_threads", "set_num_threads", "PsoResult", "SegmentResult",
-    "ifcm_step_planes", "histogram_u8_range", "segment_slice_u8", "SliceResult",
+    "ifcm_step_planes", "histogram_u8_range", "segment_slice_u8", "SliceResult", "incs", "eq11",
 ]
 
 
@@ -99,6 +99,9 @@ def _declare(L):
     L.orc_segment_slice_u8.argtypes = [_u8p, i, i, i, i, i, d, i, d, i, i, i, i, i, d, d, d, u64,
                                        _u8p, _dp, _dp, _dp, _dp, _ip, _ip, _dp, _ip]
     L.orc_segment_slice_u8.restype = i
+    L.orc_incs.argtypes = [_u8p, _u8p, l, i, _dp]
+    L.orc_incs.restype = l
+    L.orc_eq11.argtypes = [_dp, _dp, i, i, d, _dp]
     L.orc_num_threads.restype = i
     L.orc_set_num_threads.argtypes = [i]
 
@@ -427,3 +430,21 @@ def segment_slice_u8(vol, z, C, P, max_gen, seed, m=2.0, q_mode=0, eps=1e-5, max
     if r != 0:
         raise ValueError(f"slice {z} outside [0, {nz})")
     return SliceResult(lab.reshape(ny, nx), U, c, lx[0], lx[1], J.value, gens.value, fi.value, ci, fc.value)
+
+
+def incs(labels, truth, centers):
+    """incS (R26): voxels whose label, mapped to a class by its centre's rank, differs from truth."""
+    lab = np.ascontiguousarray(labels, dtype=np.uint8).ravel()
+    tru = np.ascontiguousarray(truth, dtype=np.uint8).ravel()
+    c = _f64(centers)
+    return int(_L().orc_incs(_p(lab, _u8p), _p(tru, _u8p), lab.size, c.shape[0], _p(c)))
+
+
+def eq11(incs_tab, secs_tab, alpha):
+    """Eq. 11 cost per algorithm from [k sizes][A algorithms] tables of incS and seconds."""
+    q = _f64(incs_tab)
+    t = _f64(secs_tab)
+    k, A = q.shape
+    J = np.empty(A)
+    _L().orc_eq11(_p(q), _p(t), k, A, float(alpha), _p(J))
+    return J

@@ -928,3 +928,46 @@ int orc_segment_slice_u8(const uint8_t *vol, int nx, int ny, int nz, int z, int 
     free(x); free(Us); free(Ub);
     return 0;
 }
+
+/* incS ("incorrect segmentation", defined in the paper's
+ * ref. [1]) on a phantom with known truth (R26): cluster j is mapped to the
+ * tissue class of its rank among the centres (ascending; ties to the lower
+ * index), classes being numbered by ascending intensity level; incS = the
+ * number of voxels whose mapped label differs from the truth label. */
+long orc_incs(const uint8_t *labels, const uint8_t *truth, long N, int C, const double *centers) {
+    int rank[8];
+    for (int j = 0; j < C; ++j) {
+        int r = 0;
+        for (int k = 0; k < C; ++k)
+            if (centers[k] < centers[j] || (centers[k] == centers[j] && k < j)) ++r;
+        rank[j] = r;
+    }
+    long bad = 0;
+    for (long i = 0; i < N; ++i)
+        if (rank[labels[i]] != truth[i]) ++bad;
+    return bad;
+}
+
+/* Eq. 11: the speed / quality trade-off of A algorithms over
+ * k image sizes, J_a(alpha) = 1/k sum_i alpha (incS_ia - min_i incS) /
+ * (max_i incS - min_i incS) + (1 - alpha) (S_ia - min_i S) / (max_i S - min_i S),
+ * min / max over the algorithms at size i; a term whose max equals its min
+ * is 0 (R26).  incs, secs: [k][A] row-major. */
+void orc_eq11(const double *incs, const double *secs, int k, int A, double alpha, double *J) {
+    for (int a = 0; a < A; ++a) J[a] = 0.0;
+    for (int i = 0; i < k; ++i) {
+        double lo_q = incs[i * A], hi_q = incs[i * A], lo_s = secs[i * A], hi_s = secs[i * A];
+        for (int a = 1; a < A; ++a) {
+            if (incs[i * A + a] < lo_q) lo_q = incs[i * A + a];
+            if (incs[i * A + a] > hi_q) hi_q = incs[i * A + a];
+            if (secs[i * A + a] < lo_s) lo_s = secs[i * A + a];
+            if (secs[i * A + a] > hi_s) hi_s = secs[i * A + a];
+        }
+        for (int a = 0; a < A; ++a) {
+            const double q = hi_q > lo_q ? (incs[i * A + a] - lo_q) / (hi_q - lo_q) : 0.0;
+            const double t = hi_s > lo_s ? (secs[i * A + a] - lo_s) / (hi_s - lo_s) : 0.0;
+            J[a] += alpha * q + (1.0 - alpha) * t;
+        }
+    }
+    for (int a = 0; a < A; ++a) J[a] /= (double)k;
+}

@@ -99,6 +99,9 @@ SIGNATURES = {
     "pifcm_normalize_u8": (ct.c_int, [_vp, _G, _vp, _vp, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_gmm_init": (ct.c_int, [_vp, ct.c_int32, _vp, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_argmax": (ct.c_int, [_vp, _G, ct.c_int32, _vp, _vp, _vp]),
+    "pifcm_incs": (ct.c_int, [_vp, _vp, _vp, ct.c_int64, ct.c_int32, _vp, _vp, _vp]),
+    "pifcm_eq11": (ct.c_int, [ct.POINTER(ct.c_double), ct.POINTER(ct.c_double), ct.c_int32, ct.c_int32,
+                              ct.c_double, ct.POINTER(ct.c_double)]),
     "pifcm_value_hist": (ct.c_int, [_vp, _vp, ct.c_int32, ct.c_int64, _vp, _vp]),
     "pifcm_fcm_hist_workspace_size": (ct.c_int, [ct.c_int32, ct.POINTER(ct.c_size_t)]),
     "pifcm_fcm_hist": (ct.c_int, [_vp, _C, ct.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ct.c_size_t, _vp]),

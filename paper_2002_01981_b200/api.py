@@ -324,6 +324,16 @@ class Context:
         self._ck(self.lib.pifcm_gmm_init(self._h, C, _ptr(hist), _ptr(c0), None, 0, _stream(stream)))
         return c0
 
+    def incs(self, labels: torch.Tensor, truth: torch.Tensor, centers: torch.Tensor, C: int, stream=None) -> int:
+        """pifcm_incs (R26): voxels whose label, mapped to a class by its
+        centre's rank, differs from the phantom truth."""
+        cnt = torch.zeros(1, dtype=torch.int64, device=labels.device)
+        c = torch.zeros(4, dtype=torch.float32, device=labels.device)
+        c[:C] = centers.reshape(-1)[:C].to(labels.device, torch.float32)
+        self._ck(self.lib.pifcm_incs(self._h, _ptr(labels.contiguous()), _ptr(truth.contiguous()), labels.numel(),
+                                     C, _ptr(c), _ptr(cnt), _stream(stream)))
+        return int(cnt.item())
+
     def argmax(self, U: torch.Tensor, nx, ny, nz, C, stream=None) -> torch.Tensor:
         labels = torch.empty((nz, ny, nx), dtype=torch.uint8, device=U.device)
         g = _grid(nx, ny, nz)
@@ -515,6 +525,20 @@ def slab_chunk(nx, ny, nz_total, lib=None) -> int:
     if rc != 0:
         raise PifcmError(rc, "pifcm_slab_chunk: invalid dimensions")
     return tz.value
+
+
+def eq11(incs_tab, secs_tab, alpha: float, lib=None) -> list:
+    """pifcm_eq11: the Eq. 11 cost of each algorithm from [k sizes][A algorithms]
+    tables of incS and seconds (host arithmetic in libpifcm.so)."""
+    lib = lib or _abi.load()
+    k, A = len(incs_tab), len(incs_tab[0])
+    q = (ct.c_double * (k * A))(*[float(v) for row in incs_tab for v in row])
+    t = (ct.c_double * (k * A))(*[float(v) for row in secs_tab for v in row])
+    J = (ct.c_double * A)()
+    rc = lib.pifcm_eq11(q, t, k, A, float(alpha), J)
+    if rc != 0:
+        raise PifcmError(rc, "pifcm_eq11: invalid tables or alpha")
+    return list(J)
 
 
 def report_dict(rep: _abi.Report, C: int) -> dict:

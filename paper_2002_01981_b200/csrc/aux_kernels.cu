@@ -693,6 +693,41 @@ cudaError_t launch_gmm(const int64_t *hist, int C, int max_iter, float *c0, cuda
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- incS
+// incS (R26) on a phantom with known truth: cluster j maps to
+// the class of its centre's rank (ascending, ties to the lower index); count
+// of voxels whose mapped label differs from the truth (integer, exact).
+__global__ void k_incs(const uint8_t *labels, const uint8_t *truth, long long n, int C, const float *centers,
+                       unsigned long long *count) {
+    __shared__ int rank[kMaxC];
+    if (threadIdx.x < C) {
+        const int j = threadIdx.x;
+        int r = 0;
+        for (int k = 0; k < C; ++k)
+            if (centers[k] < centers[j] || (centers[k] == centers[j] && k < j)) ++r;
+        rank[j] = r;
+    }
+    __syncthreads();
+    unsigned long long bad = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int l = labels[i];
+        bad += (l >= C || rank[l] != (int)truth[i]) ? 1ull : 0ull;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(count, bad);
+}
+cudaError_t launch_incs(const uint8_t *labels, const uint8_t *truth, long long n, int C, const float *centers,
+                        int64_t *count, cudaStream_t st) {
+    if (cudaMemsetAsync(count, 0, sizeof(int64_t), st) != cudaSuccess) return cudaGetLastError();
+    long long b = (n + 255) / 256;
+    if (b > 148 * 8) b = 148 * 8;
+    if (b < 1) b = 1;
+    k_incs<<<(int)b, 256, 0, st>>>(labels, truth, n, C, centers, reinterpret_cast<unsigned long long *>(count));
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- argmax
 // Defuzzification (R13): strict > in cluster order, so ties go
 // to the lowest index.

@@ -747,6 +747,37 @@ int pifcm_fcm_memberships(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, flo
     return PIFCM_OK;
 }
 
+int pifcm_incs(pifcm_ctx *ctx, const uint8_t *labels, const uint8_t *truth, int64_t n, int32_t C,
+               const float *centers, int64_t *count, pifcm_stream stream) {
+    if (!ctx) return PIFCM_EINVAL;
+    if (C < 2 || C > kMaxC) return fail(ctx, PIFCM_EINVAL, "C = %d outside [2, 4]", C);
+    if (n < 0) return fail(ctx, PIFCM_EINVAL, "n = %lld < 0", (long long)n);
+    if (!count || !centers || (n > 0 && (!labels || !truth)))
+        return fail(ctx, PIFCM_EINVAL, "labels, truth, centers and count must be non-NULL");
+    LAUNCH(ctx, 1, launch_incs(labels, truth, n, C, centers, count, reinterpret_cast<cudaStream_t>(stream)));
+    return PIFCM_OK;
+}
+
+int pifcm_eq11(const double *incs, const double *secs, int32_t k, int32_t A, double alpha, double *J) {
+    if (!incs || !secs || !J || k < 1 || A < 1 || !(alpha >= 0.0 && alpha <= 1.0)) return PIFCM_EINVAL;
+    for (int a = 0; a < A; ++a) J[a] = 0.0;
+    for (int i = 0; i < k; ++i) {
+        const double *q = incs + (size_t)i * A, *t = secs + (size_t)i * A;
+        double qlo = q[0], qhi = q[0], tlo = t[0], thi = t[0];
+        for (int a = 1; a < A; ++a) {
+            qlo = q[a] < qlo ? q[a] : qlo;
+            qhi = q[a] > qhi ? q[a] : qhi;
+            tlo = t[a] < tlo ? t[a] : tlo;
+            thi = t[a] > thi ? t[a] : thi;
+        }
+        for (int a = 0; a < A; ++a)  // min-max normalisation per size; a constant row contributes 0 (R26)
+            J[a] += alpha * (qhi > qlo ? (q[a] - qlo) / (qhi - qlo) : 0.0) +
+                    (1.0 - alpha) * (thi > tlo ? (t[a] - tlo) / (thi - tlo) : 0.0);
+    }
+    for (int a = 0; a < A; ++a) J[a] /= (double)k;
+    return PIFCM_OK;
+}
+
 int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float *U, uint8_t *labels,
                  pifcm_stream stream) {
     if (!ctx) return PIFCM_EINVAL;

@@ -194,6 +194,8 @@ cudaError_t launch_fcm_hist(const FcmHistArgs &a, int C, bool m2, cudaStream_t s
 cudaError_t launch_fcm_memberships(const float *x, int nx, int ny, int nz, int pitch, const float *c, int C,
                                    float m, float4 *U, cudaStream_t st);
 cudaError_t launch_gmm(const int64_t *hist, int C, int max_iter, float *c0, cudaStream_t st);
+cudaError_t launch_incs(const uint8_t *labels, const uint8_t *truth, long long n, int C, const float *centers,
+                        int64_t *count, cudaStream_t st);
 cudaError_t launch_argmax(const float4 *U, long long n, int C, uint8_t *labels,
                           cudaStream_t st);
 cudaError_t launch_gather_gbest(const float4 *slots, long long nvox, const int *hdr,

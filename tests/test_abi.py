@@ -73,3 +73,21 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "pifcm_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_eq11_host_matches_oracle(orc):
+    """pifcm_eq11 is host arithmetic in libpifcm.so (no GPU): equal to the
+    oracle's Eq. 11 on random tables and on the hand-worked example."""
+    import numpy as np
+    from paper_2002_01981_b200.api import PifcmError, eq11
+    g = np.random.default_rng(4)
+    q = g.integers(0, 1000, size=(7, 5)).astype(float)
+    t = g.random((7, 5)) * 100
+    q[3] = 42.0  # a constant row
+    for alpha in (0.0, 0.7, 1.0):
+        assert np.allclose(eq11(q.tolist(), t.tolist(), alpha), orc.eq11(q, t, alpha), rtol=0, atol=1e-15)
+    J = eq11([[10.0, 30.0, 20.0], [5.0, 5.0, 5.0]], [[1.0, 3.0, 2.0], [4.0, 2.0, 3.0]], 0.7)
+    assert np.allclose(J, [0.15, 0.5, 0.325], rtol=0, atol=1e-15)
+    import pytest
+    with pytest.raises(PifcmError):
+        eq11([[1.0]], [[1.0]], 1.5)

@@ -74,3 +74,24 @@ def test_slice_eval_batch_and_errors(ctx):
         ctx.segment_slice(vt, 6, cfg, PsoConfig(P=5, max_gen=3))
     with pytest.raises(PifcmError):
         ctx.segment_slice(vt, 1, IfcmConfig(C=4, v=2), PsoConfig(P=5, max_gen=3))
+
+
+def test_incs_vs_oracle(ctx, orc):
+    """pifcm_incs (R26) against the oracle's count: pipeline labels on a noisy
+    phantom with its truth (bit-exact integer), random labels with permuted
+    centres."""
+    from paper_2002_01981_b200 import IfcmConfig, PsoConfig
+    img, truth = cube_phantom(40, 36, 12)
+    vol = add_noise_u8(img, 9.0, 12)
+    vt = torch.as_tensor(vol, device="cuda:0")
+    lab, _, rep = ctx.segment(vt, IfcmConfig(C=4), PsoConfig(P=4, max_gen=3, patience=0, seed=1))
+    c = torch.tensor(rep["centers"], dtype=torch.float32)
+    n = ctx.incs(lab, torch.as_tensor(truth, device="cuda:0"), c, 4)
+    assert n == orc.incs(lab.cpu().numpy(), truth, np.array(rep["centers"], np.float32).astype(np.float64))
+    assert 0 <= n <= truth.size  # (J-fitness drives lambda, xi to 1, where quality is not what is tested)
+    g = np.random.default_rng(2)
+    rl = g.integers(0, 4, size=truth.shape).astype(np.uint8)
+    pc = np.array([0.9, 0.1, 0.65, 0.35], np.float32)
+    n2 = ctx.incs(torch.as_tensor(rl, device="cuda:0"), torch.as_tensor(truth, device="cuda:0"),
+                  torch.as_tensor(pc), 4)
+    assert n2 == orc.incs(rl, truth, pc.astype(np.float64))

@@ -80,3 +80,31 @@ def test_slice_mode_properties(orc):
         assert 0.0 <= s.lam <= 1.0 and 0.0 <= s.xi <= 1.0 and s.generations == 3
     with pytest.raises(ValueError):
         orc.segment_slice_u8(vol, 7, C=4, P=4, max_gen=3, seed=2)
+
+
+def test_incs_pins(orc):
+    """incS (R26): zero for the truth itself under sorted centres, invariant
+    under relabelling the clusters together with their centres, and equal to
+    a direct count on random labels."""
+    g = np.random.default_rng(3)
+    truth = g.integers(0, 4, size=500).astype(np.uint8)
+    c = np.array([0.1, 0.35, 0.65, 0.9])
+    assert orc.incs(truth, truth, c) == 0
+    perm = np.array([2, 0, 3, 1])               # cluster j holds class perm[j]
+    lab = np.argsort(perm)[truth].astype(np.uint8)
+    assert orc.incs(lab, truth, c[perm]) == 0
+    lab = g.integers(0, 4, size=500).astype(np.uint8)
+    assert orc.incs(lab, truth, c[perm]) == int((perm[lab] != truth).sum())
+    # ties: equal centres rank by index
+    assert orc.incs(np.array([0, 1], np.uint8), np.array([0, 1], np.uint8), np.array([0.5, 0.5])) == 0
+
+
+def test_eq11_worked_example(orc):
+    """Eq. 11 by hand: 2 sizes x 3 algorithms, alpha = 0.7."""
+    q = np.array([[10.0, 30.0, 20.0], [5.0, 5.0, 5.0]])
+    t = np.array([[1.0, 3.0, 2.0], [4.0, 2.0, 3.0]])
+    J = orc.eq11(q, t, 0.7)
+    # size 0: q -> (0, 1, .5), t -> (0, 1, .5); size 1: q constant -> 0, t -> (1, 0, .5)
+    want = np.array([(0.0 + 0.3 * 1.0) / 2, (0.7 + 0.3 + 0.0) / 2, (0.35 + 0.15 + 0.15) / 2])
+    assert np.allclose(J, want, rtol=0, atol=1e-15)
+    assert np.allclose(orc.eq11(q, t, 1.0), [0.0, 0.5, 0.25])
