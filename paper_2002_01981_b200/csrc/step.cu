@@ -557,6 +557,7 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
     float2 den2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     float Jacc = 0.f, duacc = 0.f;
 
+#pragma unroll 1  // one copy of the tile body (an unrolled loop overflows the instruction cache)
     for (int k = 0; k < ntile; ++k) {
         const int b = k & 1;
         const float4 *sU = sUb[b];
