@@ -107,8 +107,7 @@ int check_pso(pifcm_ctx *ctx, const pifcm_pso_cfg *p) {
 
 // mode / shell combinations the device path implements
 int check_pso_cfg(pifcm_ctx *ctx, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg *p) {
-    if (p->fitness_mode != PIFCM_FIT_CHAINED && c->v != 1)
-        return fail(ctx, PIFCM_EINVAL, "ANCHORED / LEADER fitness with v = %d is not implemented", c->v);
+    (void)ctx; (void)c; (void)p;  // every fitness mode runs with v = 1 and v = 2
     return PIFCM_OK;
 }
 
@@ -537,6 +536,7 @@ int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
         a.lam_xi = at<double>(ws, L.lamxi);
         a.stop = L.mode == PIFCM_FIT_ANCHORED ? s.hdr + kHHfValid : s.hdr + kHStop;
         a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f); a.q_mode = cfg->q_mode;
+        set_shells(a, cfg);
         a.n_in_states = L.nslots;
         a.C = cfg->C;
         a.hf = hf;

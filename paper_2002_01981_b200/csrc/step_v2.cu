@@ -140,7 +140,9 @@ __device__ __forceinline__ float4 attraction_coop_v2(const float4 *const (&Us)[5
     return make_float4(out[0], out[1], out[2], out[3]);
 }
 
-template <int C, bool M2, bool DU, bool QL>
+// HF: the ANCHORED / LEADER pass -- write the shell-weighted H and F of
+// every voxel (two float4, as the v = 1 kernel's HF instance) instead of a step.
+template <int C, bool M2, bool DU, bool QL, bool HF = false>
 __global__ void __launch_bounds__(kStepThreads, kV2MinBlocks)
     k_step_v2(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, const StepArgs a) {
     constexpr int NP = (C + 1) / 2;
@@ -293,6 +295,21 @@ __global__ void __launch_bounds__(kStepThreads, kV2MinBlocks)
                 A[q].y = fmaxf(Ar[q].y, kAFloor);
             }
             if (NP == 1) { A[1] = make_float2(1.f, 1.f); Ar[1] = A[1]; }
+            if (HF) {  // particle-invariant H, F of this state (Eq. 5, 7, 10)
+                if ((vmask >> r) & 1u) {
+                    float2 Hh[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                    float2 Ff[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        Hh[q] = __ffma2_rn(hn[1][r][q], make_float2(h2, h2), __fmul2_rn(hn[0][r][q], make_float2(h1, h1)));
+                        Ff[q] = __ffma2_rn(fn[1][r][q], make_float2(f2, f2), __fmul2_rn(fn[0][r][q], make_float2(f1, f1)));
+                    }
+                    float4 *o = a.hf + 2 * ((long long)z * plane + (long long)gy * a.nx + gx);
+                    o[0] = make_float4(Hh[0].x, Hh[0].y, Hh[1].x, Hh[1].y);
+                    o[1] = make_float4(Ff[0].x, Ff[0].y, Ff[1].x, Ff[1].y);
+                }
+                continue;
+            }
             const Memb mb = memb_compute<C, M2>(xr[r], c2, A, a.m, a.inv_m1, Ar);
             const bool valid = (vmask >> r) & 1u;
             const bool band = valid && !(mb.K <= kKMax);
@@ -345,6 +362,7 @@ __global__ void __launch_bounds__(kStepThreads, kV2MinBlocks)
         }
     }
 #undef PIFCM_ISSUE2
+    if (HF) return;  // no reductions: H, F only
     float num[kMaxC] = {num2[0].x, num2[0].y, num2[1].x, num2[1].y};
     float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
     const int blk = blockIdx.x + gridDim.x * blockIdx.y;
@@ -383,14 +401,14 @@ static bool make_maps2(const StepArgs &a, CUtensorMap *mU, CUtensorMap *mX) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int C, bool M2, bool DU, bool QL>
+template <int C, bool M2, bool DU, bool QL, bool HF = false>
 static cudaError_t launch_v2_t(const StepArgs &a, int P, cudaStream_t st) {
     // the dynamic shared-memory opt-in is per device: remember it per device
     static unsigned long long attr_set = 0ull;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
     if (dev < 64 && !(attr_set & (1ull << dev))) {
-        const cudaError_t e = cudaFuncSetAttribute(k_step_v2<C, M2, DU, QL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        const cudaError_t e = cudaFuncSetAttribute(k_step_v2<C, M2, DU, QL, HF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    kV2Smem);
         if (e != cudaSuccess) return e;
         attr_set |= 1ull << dev;
@@ -398,21 +416,22 @@ static cudaError_t launch_v2_t(const StepArgs &a, int P, cudaStream_t st) {
     CUtensorMap mU, mX;
     if (!make_maps2(a, &mU, &mX)) return cudaErrorInvalidValue;
     dim3 grid(a.tiles_x * a.tiles_y, a.zchunks, P);
-    k_step_v2<C, M2, DU, QL><<<grid, kStepThreads, kV2Smem, st>>>(mU, mX, a);
+    k_step_v2<C, M2, DU, QL, HF><<<grid, kStepThreads, kV2Smem, st>>>(mU, mX, a);
     return cudaGetLastError();
 }
 
 template <int C, bool M2>
 static cudaError_t launch_v2_c(const StepArgs &a, int P, cudaStream_t st) {
     const bool ql = a.q_mode == 0;
+    if (a.hf) return ql ? launch_v2_t<C, true, false, true, true>(a, P, st)
+                        : launch_v2_t<C, true, false, false, true>(a, P, st);
     if (a.want_du) return ql ? launch_v2_t<C, M2, true, true>(a, P, st) : launch_v2_t<C, M2, true, false>(a, P, st);
     return ql ? launch_v2_t<C, M2, false, true>(a, P, st) : launch_v2_t<C, M2, false, false>(a, P, st);
 }
 
 // The decomposition fields of `a` (tiles, z-chunks, nblk) are set by launch_step.
 cudaError_t launch_step_v2(const StepArgs &a, int C, int P, cudaStream_t st) {
-    if (a.hf) return cudaErrorInvalidValue;  // no fitness-mode H, F pass for v = 2
-    const bool m2 = (a.m == 2.0f);
+    const bool m2 = (a.m == 2.0f) || a.hf != nullptr;  // the H, F pass does not depend on m
     switch (C) {
         case 2: return m2 ? launch_v2_c<2, true>(a, P, st) : launch_v2_c<2, false>(a, P, st);
         case 3: return m2 ? launch_v2_c<3, true>(a, P, st) : launch_v2_c<3, false>(a, P, st);

@@ -29,7 +29,7 @@ def _case(C=3, shape=(10, 24, 28), seed=4):
     return add_noise_u8(img, 7.0, seed), lab
 
 
-def _swarm(ctx, orc, P, seed, mode, C=3, shape=(10, 24, 28)):
+def _swarm(ctx, orc, P, seed, mode, C=3, shape=(10, 24, 28), v=1):
     from paper_2002_01981_b200 import IfcmConfig, PsoConfig, to_aos, to_pitched_x
     from paper_2002_01981_b200.api import _grid
     vol, _ = _case(C, shape)
@@ -38,7 +38,7 @@ def _swarm(ctx, orc, P, seed, mode, C=3, shape=(10, 24, 28)):
     U0, c0 = Uf.astype(np.float32), cf.astype(np.float32)
     nz, ny, nx = x.shape
     dev = torch.device("cuda:0")
-    cfg = IfcmConfig(C=C)
+    cfg = IfcmConfig(C=C, v=v)
     pso = PsoConfig(P=P, max_gen=50, patience=0, seed=seed, fitness=mode)
     xt, Ut = to_pitched_x(x, dev), to_aos(U0, dev)
     c4 = torch.zeros(4, device=dev)
@@ -49,17 +49,17 @@ def _swarm(ctx, orc, P, seed, mode, C=3, shape=(10, 24, 28)):
     return x, U0, c0, cfg, pso, xt, Ut, ws, g
 
 
-@pytest.mark.parametrize("mode,G,P,seed", [(ANCHORED, 6, 6, 777), (ANCHORED, 4, 40, 5), (LEADER, 3, 6, 91),
-                                           (LEADER, 3, 33, 12)])
-def test_mode_eval_parity(ctx, orc, mode, G, P, seed):
+@pytest.mark.parametrize("mode,G,P,seed,v", [(ANCHORED, 6, 6, 777, 1), (ANCHORED, 4, 40, 5, 1), (LEADER, 3, 6, 91, 1),
+                                             (LEADER, 3, 33, 12, 1), (ANCHORED, 4, 6, 777, 2), (LEADER, 3, 6, 91, 2)])
+def test_mode_eval_parity(ctx, orc, mode, G, P, seed, v):
     """Every generation's fitness vector within 1e-5 of the oracle's (ANCHORED
     evaluates every generation from the same start; LEADER's shared state
     drifts by fp32 rounding: 1e-5 for generation 0, 1e-4 after), identical
     gbest sequence and (lambda*, xi*), and the gbest snapshot of Alg. 1 step
     10 within 1e-4."""
-    x, U0, c0, cfg, pso, xt, Ut, ws, g = _swarm(ctx, orc, P, seed, mode)
+    x, U0, c0, cfg, pso, xt, Ut, ws, g = _swarm(ctx, orc, P, seed, mode, v=v)
     fit = ctx.pso_fitness(g, cfg, pso, ws)
-    r = orc.pso_run(x, U0, c0, P=P, max_gen=G, seed=seed, fitness_mode=mode)
+    r = orc.pso_run(x, U0, c0, P=P, max_gen=G, seed=seed, fitness_mode=mode, v=v)
     for gen in range(G):
         ctx.pso_eval(g, cfg, pso, xt, ws)
         f = fit.cpu().numpy()
@@ -77,23 +77,28 @@ def test_mode_eval_parity(ctx, orc, mode, G, P, seed):
     assert np.allclose(cg.cpu().numpy()[:3], r.c, rtol=1e-4)
 
 
-@pytest.mark.parametrize("mode,G,seed", [(ANCHORED, 4, 3), (LEADER, 4, 3), (ANCHORED, 2, 1), (LEADER, 2, 1)])
-def test_mode_segment_parity(ctx, orc, mode, G, seed):
+@pytest.mark.parametrize("mode,G,seed,v", [(ANCHORED, 4, 3, 1), (LEADER, 4, 3, 1), (ANCHORED, 2, 1, 1), (LEADER, 2, 1, 1),
+                                          (ANCHORED, 3, 3, 2), (LEADER, 3, 1, 2)])
+def test_mode_segment_parity(ctx, orc, mode, G, seed, v):
     """The whole pipeline with the mode: same GMM start and PSO trajectory
     (bit-identical lambda*, xi*); labels >= 99.9 % where the final IFCM is well
     conditioned."""
     from paper_2002_01981_b200 import IfcmConfig, PsoConfig
     vol, _ = _case(C=4, shape=(12, 30, 33), seed=8)
-    cfg = IfcmConfig(C=4)
+    cfg = IfcmConfig(C=4, v=v)
     pso = PsoConfig(P=6, max_gen=G, patience=0, seed=seed, fitness=mode)
     labels, U, rep = ctx.segment(torch.as_tensor(vol, device="cuda:0"), cfg, pso, want_U=True)
-    r = orc.segment_u8(vol, C=4, P=6, max_gen=G, seed=seed, fitness_mode=mode)
+    r = orc.segment_u8(vol, C=4, P=6, max_gen=G, seed=seed, fitness_mode=mode, v=v)
     assert rep["lambda"] == r.lam and rep["xi"] == r.xi
     if min(r.lam, r.xi) > 0.95:
         pytest.skip(f"ill-conditioned final IFCM at lambda*={r.lam:.3f}, xi*={r.xi:.3f}")
     agree = (labels.cpu().numpy() == r.labels).mean()
     assert agree >= 0.999, agree
-    assert np.allclose(rep["centers"], r.c, rtol=1e-3)
+    # centres after up to 100 final-IFCM iterations from different roundings;
+    # the 124-neighbour map (v = 2) drifts further than v = 1's (the per-step
+    # parity from the same state is 1e-4: test_step_parity_v2)
+    rtol = 1e-3 if v == 1 else 1e-2
+    assert np.allclose(rep["centers"], r.c, rtol=rtol), (rep["centers"], r.c, r.lam, r.xi)
 
 
 def test_mode_workspace_is_smaller(ctx):
