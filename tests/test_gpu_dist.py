@@ -22,7 +22,7 @@ CFG = dict(C=4)
 PSO = dict(P=5, max_gen=4, patience=0, seed=31)
 
 
-def _worker(rank, world, port, nz, shard, q):
+def _worker(rank, world, port, nz, shard, q, eb=0):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -31,7 +31,8 @@ def _worker(rank, world, port, nz, shard, q):
     from paper_2002_01981_b200.dist import ShardedSegmenter
     ctx = Context(0)
     vol = _case(nz)
-    seg = ShardedSegmenter(ctx, IfcmConfig(**CFG), PsoConfig(**PSO), vol.shape, dist, shard_final=shard)
+    seg = ShardedSegmenter(ctx, IfcmConfig(**CFG), PsoConfig(**PSO, eval_batch=eb), vol.shape, dist,
+                           shard_final=shard)
     rep = seg.segment(torch.as_tensor(vol, device="cuda:0"))
     q.put((rank, seg.labels.cpu().numpy(), rep["lambda"], rep["xi"], rep["final_iters"], rep["centers"]))
     dist.barrier()
@@ -48,8 +49,9 @@ def _port():
 
 # nz = 12: one z-chunk, the final IFCM runs replicated; nz = 40: five chunks,
 # the final IFCM z-slab sharded 3 + 2 (uneven record counts) or replicated
-@pytest.mark.parametrize("nz,shard", [(12, None), (40, True), (40, False)])
-def test_sharded_equals_single(nz, shard):
+# eb: each rank evaluates its particles in batches of eb over Pl + eb + 1 slots
+@pytest.mark.parametrize("nz,shard,eb", [(12, None, 0), (40, True, 0), (40, False, 0), (40, True, 1)])
+def test_sharded_equals_single(nz, shard, eb):
     from paper_2002_01981_b200 import Context, IfcmConfig, PsoConfig
     from paper_2002_01981_b200.dist import ShardedSegmenter
     ctx = Context(0)
@@ -68,7 +70,7 @@ def test_sharded_equals_single(nz, shard):
     cm = mp.get_context("spawn")
     q = cm.Queue()
     port = _port()
-    procs = [cm.Process(target=_worker, args=(r, 2, port, nz, shard, q)) for r in range(2)]
+    procs = [cm.Process(target=_worker, args=(r, 2, port, nz, shard, q, eb)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=180) for _ in range(2)]
