@@ -367,10 +367,13 @@ def run_ours(args, rank, world, local_rank):
     hbm, hbm_kind = _peaks()
     achieved = (k_bytes / k_n) / ((k_ms / k_n) * 1e-3) / 1e9 if k_n else None
     traffic = None
+    ncu_instr = None
     if not c5 and not c2:  # the committed ncu capture is of the C3 P = 32 launch
         try:
             with open(PROFILE_SUMMARY) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                summ = json.load(f)
+            traffic = summ.get("dram_bytes_per_launch")
+            ncu_instr = summ.get("instructions_per_vp")
         except Exception:
             pass
     # The kernel's binding resource is the FP32 pipe, not HBM:
@@ -446,6 +449,8 @@ def run_ours(args, rank, world, local_rank):
             "launches": k_n,
             "share_of_step": (k_ms / ms) if ms else None,
             "alu": alu_view,
+            # smsp__inst_executed / (N_vox P) of the same launch, from the committed ncu capture
+            "ncu_instr_per_vp": ncu_instr,
             "single_state_launches": {
                 "what": "final IFCM (P = 1) launches of the same kernel",
                 "launches": s_n, "avg_launch_ms": (s_ms / s_n) if s_n else None,
