@@ -514,9 +514,10 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
     // TMA destinations: 128-byte aligned stages (as the 3D ring)
     __shared__ __align__(128) unsigned char sbuf[2 * (kUStagePad + kXStagePad)];
     __shared__ __align__(8) uint64_t bar[2];
-    float4 *sUb[2] = {reinterpret_cast<float4 *>(sbuf), reinterpret_cast<float4 *>(sbuf + kUStagePad)};
-    float *sXb[2] = {reinterpret_cast<float *>(sbuf + 2 * kUStagePad),
-                     reinterpret_cast<float *>(sbuf + 2 * kUStagePad + kXStagePad)};
+    // (stage pointers are formed from the __shared__ array at each use, so the
+    // compiler keeps them in the shared window: LDS, not generic loads)
+    auto sUb = [&](int b) { return reinterpret_cast<float4 *>(sbuf + b * kUStagePad); };
+    auto sXb = [&](int b) { return reinterpret_cast<float *>(sbuf + 2 * kUStagePad + b * kXStagePad); };
     const int p = blockIdx.z;
     if (a.stop && *a.stop) return;
     if (a.stats && a.stats[4 * p + 3] != 0.0) return;
@@ -536,8 +537,8 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
     auto issue = [&](int k) {
         const int b = k & 1, y0k = (ty0 + k) * kTY;
         mbar_expect_tx(&bar[b], kUStageBytes + kXStageBytes);
-        tma_load_4d(sUb[b], &tmU, &bar[b], 4 * (x0 - 1), y0k - 1, 0, slot);
-        tma_load_3d(sXb[b], &tmX, &bar[b], x0 - kXOff, y0k - 1, 0);
+        tma_load_4d(sUb(b), &tmU, &bar[b], 4 * (x0 - 1), y0k - 1, 0, slot);
+        tma_load_3d(sXb(b), &tmX, &bar[b], x0 - kXOff, y0k - 1, 0);
     };
     if (tid == 0) {
         issue(0);
@@ -560,8 +561,8 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
 #pragma unroll 1  // one copy of the tile body (an unrolled loop overflows the instruction cache)
     for (int k = 0; k < ntile; ++k) {
         const int b = k & 1;
-        const float4 *sU = sUb[b];
-        const float *sX = sXb[b];
+        const float4 *sU = sUb(b);
+        const float *sX = sXb(b);
         const int y0 = (ty0 + k) * kTY;
         float invQ[kRY];
         unsigned vmask = 0u;
