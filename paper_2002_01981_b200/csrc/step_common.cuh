@@ -13,6 +13,9 @@
 #ifndef PIFCM_KGATE
 #define PIFCM_KGATE 1
 #endif
+#ifndef PIFCM_KGATE_UNIFORM
+#define PIFCM_KGATE_UNIFORM 1
+#endif
 
 namespace pifcm {
 __device__ __forceinline__ float rcp_approx(float v) {
@@ -262,7 +265,12 @@ __device__ __forceinline__ Memb memb_compute(float xv, const float2 (&c2)[2], co
     // band and K need not be formed (NaN factors fall through to K)
     float amin = fminf(fabsf(Ar[0].x), fabsf(Ar[0].y));
     if (NP > 1) amin = fminf(amin, fminf(fabsf(Ar[NP - 1].x), fabsf(Ar[NP - 1].y)));
+#if PIFCM_KGATE_UNIFORM
+    // warp-uniform decision (no reconvergence point): K is exact where formed
+    const bool kneed = __any_sync(__activemask(), !(amin * kKMax >= 0.75f * (M2 ? 1.0f : inv_m1)));
+#else
     const bool kneed = !(amin * kKMax >= 0.75f * (M2 ? 1.0f : inv_m1));
+#endif
 #else
     const bool kneed = true;
 #endif
