@@ -124,15 +124,16 @@ def _volume(name="C3"):
 def cpu_baseline_measure(vol, budget_s=20.0, P=P):
     """The oracle as it stands (fp64 C, OpenMP on all host cores) on a bounded
     sample of the same workload: whole IFCM steps of single particles over the
-    full volume, repeated until ~budget_s of CPU work."""
-    import numpy as np
-
+    full volume, repeated until ~budget_s of CPU work; plus one step on one
+    thread (SURVEY 8(d)'s "sequential" point, in the spirit of Table 7's CPU
+    column)."""
     import oracle
     x = oracle.normalize_u8(vol)
     c0 = oracle.gmm_init(oracle.histogram_u8(vol), C)
     U, c, _ = oracle.fcm_run(x, c0, max_iter=1)
     pos, _ = oracle.pso_init(P, 12345)
     n_vox = vol.size
+    cores = oracle.num_threads()
     steps = 0
     t0 = time.perf_counter()
     while True:
@@ -142,11 +143,20 @@ def cpu_baseline_measure(vol, budget_s=20.0, P=P):
         el = time.perf_counter() - t0
         if el >= budget_s or steps >= 64:
             break
-    del np
+    seq = None
+    try:
+        oracle.set_num_threads(1)
+        t1 = time.perf_counter()
+        oracle.ifcm_step(x, U, c, pos[0, 0], pos[0, 1], m=2.0)
+        e1 = time.perf_counter() - t1
+        seq = {"value": n_vox / e1, "cores": 1, "sample": f"1 oracle IFCM step on one thread, {e1:.1f} s"}
+    finally:
+        oracle.set_num_threads(cores)
     return {"value": n_vox * steps / el, "unit": "voxel-iterations/s (x particles)",
-            "cores": oracle.num_threads(), "kind": "oracle",
+            "cores": cores, "kind": "oracle",
             "sample": f"{steps} oracle IFCM steps (one particle each, lambda/xi from the bench "
-                      f"swarm) over the full {'x'.join(map(str, vol.shape[::-1]))} volume, {el:.1f} s"}
+                      f"swarm) over the full {'x'.join(map(str, vol.shape[::-1]))} volume, {el:.1f} s",
+            "sequential": seq}
 
 
 def run_reference(args, rank, world):
@@ -427,6 +437,8 @@ def run_ours(args, rank, world, local_rank):
                    f" GB per GPU; every generation streams {Pw * nx * ny * nz * 32 / 1e9:.1f} GB)"),
             "eval_batch": eval_batch,
             "pso_wall_ms": last["t_pso"] * 1e3, "segment_wall_ms": last["t_total"] * 1e3,
+            # the segmentation's phases (CUDA events inside the library)
+            "phases_ms": {k: last[k] * 1e3 for k in ("t_norm", "t_init", "t_pso", "t_final") if k in last},
             "fcm_iters": last["fcm_iters"], "final_iters": last["final_iters"],
             "lambda_star": last["lambda"], "xi_star": last["xi"],
         },
@@ -478,7 +490,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--workload", default="C3", choices=["C3", "C2", "C4", "C5"],
                     help="C3 (default, the BASELINE metric's config), C2 (854x854 2D, the paper's Table 7 "
                          "image), C4 (16 C3-shaped volumes per step) or C5 (512^3, z-slab sharded)")
