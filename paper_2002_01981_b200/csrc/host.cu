@@ -442,6 +442,16 @@ int pifcm_iterate_ex(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cf
     double *S = stats ? stats : st_scr;
     CK(ctx, cudaMemsetAsync(S, 0, sizeof(double) * 4 * P, st));
     CK(ctx, cudaMemsetAsync(status, 0, sizeof(int), st));
+    // a small 2D image (C1): all iterations in one launch, one CTA per state
+    // holding the image in shared memory (small2d.cu); not for the canonical
+    // decomposition, whose records must match the pipeline's final IFCM
+    if (!canonical && cfg->v == 1 && grid->nz == 1 && (long long)grid->nx * grid->ny <= 4096 &&
+        small2d_smem(grid->nx, grid->ny) <= 200 * 1024) {
+        LAUNCH(ctx, 1, launch_iterate_small2d(x, grid->nx, grid->ny, grid->pitch, reinterpret_cast<const float4 *>(U_in),
+                                              reinterpret_cast<float4 *>(U_out), centers, lam_xi, P, iters,
+                                              cfg->eps, cfg->m, cfg->q_mode, cfg->C, S, status, st));
+        return PIFCM_OK;
+    }
     bool ok = true;
     const bool zero = host_zero_lamxi(lam_xi, P, st, &ok);
     if (!ok) return fail(ctx, PIFCM_ECUDA, "reading lam_xi failed");

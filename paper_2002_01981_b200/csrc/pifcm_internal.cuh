@@ -193,6 +193,10 @@ cudaError_t launch_value_hist(const void *vol, int dtype, long long n, int64_t *
 cudaError_t launch_fcm_hist(const FcmHistArgs &a, int C, bool m2, cudaStream_t st);
 cudaError_t launch_fcm_memberships(const float *x, int nx, int ny, int nz, int pitch, const float *c, int C,
                                    float m, float4 *U, cudaStream_t st);
+size_t small2d_smem(int nx, int ny);
+cudaError_t launch_iterate_small2d(const float *x, int nx, int ny, int pitch, const float4 *U_in, float4 *U_out,
+                                   float *centers, const double *lam_xi, int P, int iters, float eps, float m,
+                                   int q_mode, int C, double *stats, int *status, cudaStream_t st);
 cudaError_t launch_gmm(const int64_t *hist, int C, int max_iter, float *c0, cudaStream_t st);
 cudaError_t launch_incs(const uint8_t *labels, const uint8_t *truth, long long n, int C, const float *centers,
                         int64_t *count, cudaStream_t st);

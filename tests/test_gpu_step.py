@@ -259,3 +259,43 @@ def test_same_state_parity_ill_conditioned(ctx, orc):
         assert err < U_TOL, (it, err)
         assert np.all(np.abs(cen[0, :3].cpu().numpy() - cs) <= C_TOL * np.abs(cs) + 1e-7)
         Ut, Uo = Uo, Ut
+
+
+@pytest.mark.parametrize("shape,C,m,q_mode", [((1, 32, 32), 3, 2.0, 0), ((1, 50, 40), 4, 1.7, 1), ((1, 7, 61), 2, 2.0, 0)])
+def test_small2d_multi_iteration(ctx, orc, shape, C, m, q_mode):
+    """pifcm_iterate on a small 2D image runs every iteration in one launch
+    (small2d.cu): one iteration from the same state within 1e-4 for three
+    states at once; six iterations against the oracle's run (1e-3, as C1);
+    the eps stop at the oracle's iteration count."""
+    from paper_2002_01981_b200 import IfcmConfig, to_aos, to_pitched_x
+    nz, ny, nx = shape
+    dev = torch.device("cuda:0")
+    states = [random_state(nx, ny, nz, C, seed=500 + s, crisp_frac=0.05) for s in range(3)]
+    x = states[0][0]
+    lams = [(0.3, 0.6), (0.8, 0.9), (0.0, 0.0)]
+    U = torch.stack([to_aos(s[1], dev) for s in states])
+    cen = torch.zeros((3, 4), device=dev)
+    for i, s in enumerate(states):
+        cen[i, :C] = torch.as_tensor(s[2])
+    lx = torch.tensor(lams, dtype=torch.float64, device=dev)
+    xt = to_pitched_x(x, dev)
+    Un = torch.empty_like(U)
+    stats = torch.zeros((3, 4), dtype=torch.float64, device=dev)
+    c1 = cen.clone()
+    ctx.iterate(xt, U, Un, c1, lx, IfcmConfig(C=C, m=m, q_mode=q_mode, eps=0.0), iters=1, stats=stats, nx=nx)
+    for i, s in enumerate(states):
+        Uo, co, Jo, _ = orc.ifcm_step(x, s[1], s[2], lams[i][0], lams[i][1], m=m, q_mode=q_mode)
+        assert np.abs(Un[i, :, :C].cpu().numpy() - Uo).max() < 1e-4, i
+        assert np.allclose(c1[i, :C].cpu().numpy(), co, rtol=1e-4)
+        assert abs(stats[i, 0].item() - Jo) <= 1e-4 * Jo
+    c6 = cen.clone()
+    ctx.iterate(xt, U, Un, c6, lx, IfcmConfig(C=C, m=m, q_mode=q_mode, eps=0.0), iters=6, stats=stats, nx=nx)
+    assert (stats[:, 2].cpu().numpy() == 6).all()
+    for i, s in enumerate(states):
+        Ur, cr, it, _ = orc.ifcm_run(x, s[1], s[2], lams[i][0], lams[i][1], eps=0.0, max_iter=6, m=m, q_mode=q_mode)
+        assert np.abs(Un[i, :, :C].cpu().numpy() - Ur).max() < 1e-3, i
+    ce = cen.clone()
+    ctx.iterate(xt, U, Un, ce, lx, IfcmConfig(C=C, m=m, q_mode=q_mode, eps=1e-3), iters=100, stats=stats, nx=nx)
+    for i, s in enumerate(states):
+        _, _, it, _ = orc.ifcm_run(x, s[1], s[2], lams[i][0], lams[i][1], eps=1e-3, max_iter=100, m=m, q_mode=q_mode)
+        assert abs(int(stats[i, 2].item()) - it) <= 1, (i, stats[i, 2].item(), it)
