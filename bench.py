@@ -165,6 +165,12 @@ def run_reference(args, rank, world):
         return
     import oracle
     oracle.build_oracle()
+    # torchrun sets OMP_NUM_THREADS=1 for every rank; rank 0 runs the oracle
+    # alone (the other ranks have exited), so it gets the host's cores
+    try:
+        oracle.set_num_threads(len(os.sched_getaffinity(0)))
+    except Exception:
+        pass
     c5 = args.workload == "C5"
     vol = _volume(args.workload)
     workload = (WORKLOAD_C5.format(P=64) if c5 else
