@@ -188,6 +188,9 @@ int pifcm_iterate_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *c
  *   ws       dev scratch of pifcm_iterate_workspace_size() bytes (NULL if 0).
  * With cfg->eps > 0 a state stops once its max|du| < eps (its U_out then
  * holds the converged U); otherwise exactly `iters` iterations run.
+ * A 2D image of at most 4096 voxels (e.g. the 32 x 32 config C1) runs all
+ * iterations in one launch, one CTA per state holding the image in shared
+ * memory; any other grid runs one launch per iteration.
  * Errors: PIFCM_EINVAL (dims, C, m, P < 1, iters < 1, lam/xi range is not
  * checked on device data), PIFCM_EALIGN (pitch), PIFCM_ENOMEM (ws too small),
  * PIFCM_ECUDA. */
