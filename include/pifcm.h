@@ -246,6 +246,16 @@ int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cf
                      const pifcm_pso_cfg *pso, const float *x, void *ws, size_t ws_bytes,
                      pifcm_stream stream);
 
+/* Per-generation record of the swarm (a test / debugging aid, SURVEY 5
+ * tracing): while set, every pifcm_pso_update of this ctx (and so
+ * pifcm_pso_step / _run / pifcm_segment) writes, for its generation t <
+ * max_gen, the fitness vector it consumed f[t][P] (Alg. 1 step 4), the
+ * positions it was evaluated at pos[t][P][2] and the gbest particle after the
+ * update gbest[t] (step 8) into these caller-owned device buffers.  The
+ * generation counter restarts at pifcm_pso_init.  All three NULL switch it
+ * off; a partial set, or max_gen < 1, is PIFCM_EINVAL.  No synchronisation. */
+int pifcm_pso_trace(pifcm_ctx *ctx, double *f, double *pos, int32_t *gbest, int32_t max_gen);
+
 /* One generation on one process: pifcm_pso_eval + pifcm_pso_update.  Async. */
 int pifcm_pso_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
                    const pifcm_pso_cfg *pso, const float *x, void *ws, size_t ws_bytes,

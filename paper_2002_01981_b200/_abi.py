@@ -89,6 +89,7 @@ SIGNATURES = {
     "pifcm_pso_eval": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_fitness_ptr": (ct.c_int, [_G, _C, _P, _vp, ct.POINTER(_vp)]),
     "pifcm_pso_update": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
+    "pifcm_pso_trace": (ct.c_int, [_vp, _vp, _vp, _vp, ct.c_int32]),
     "pifcm_pso_step": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_result_get": (ct.c_int, [_vp, _G, _C, _P, _vp, ct.POINTER(PsoResult),
                                         ct.POINTER(ct.c_int32), _vp]),

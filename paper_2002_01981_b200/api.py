@@ -222,6 +222,13 @@ class Context:
         self._ck(self.lib.pifcm_pso_update(self._h, ct.byref(grid), ct.byref(cfg.c()),
                                            ct.byref(pso.c()), _ptr(x), _ptr(ws), ws.numel(), _stream(stream)))
 
+    def pso_trace(self, f: torch.Tensor | None, pos: torch.Tensor | None = None,
+                  gbest: torch.Tensor | None = None):
+        """pifcm_pso_trace: f [G,P] f64, pos [G,P,2] f64, gbest [G] int32 (device),
+        filled per generation by every later PSO update; None switches it off."""
+        G = 0 if f is None else f.shape[0]
+        self._ck(self.lib.pifcm_pso_trace(self._h, _ptr(f), _ptr(pos), _ptr(gbest), G))
+
     def pso_step(self, grid, cfg, pso, x, ws, stream=None):
         self._ck(self.lib.pifcm_pso_step(self._h, ct.byref(grid), ct.byref(cfg.c()), ct.byref(pso.c()),
                                          _ptr(x), _ptr(ws), ws.numel(), _stream(stream)))

@@ -190,6 +190,7 @@ __global__ void k_pso_init(SwarmDev s, int P, int Pl, int p0, double v0, uint32_
         s.hdr[kHGbest] = -1;
         s.hdr[kHGbestSlot] = -1;
         s.hdr[kHInit] = 1;
+        for (int i = 0; i < 16; ++i) s.dhdr[i] = 0.0;  // the whole record is read back (pifcm_pso_result_get)
         s.dhdr[kDPrevGf] = INFINITY;
         s.dhdr[kDGbestJ] = INFINITY;
         s.dhdr[kDGbestL] = 0.0;
@@ -231,6 +232,11 @@ __global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs 
         s.evalpos[2 * p] = s.pos[2 * p];
         s.evalpos[2 * p + 1] = s.pos[2 * p + 1];
         const double f = s.fit[p];
+        if (a.tr_f && t < a.tr_max) {
+            a.tr_f[(long long)t * a.P + p] = f;
+            a.tr_pos[2 * ((long long)t * a.P + p)] = s.pos[2 * p];
+            a.tr_pos[2 * ((long long)t * a.P + p) + 1] = s.pos[2 * p + 1];
+        }
         if (f < s.pbf[p]) {
             s.pbf[p] = f;
             s.pbx[2 * p] = s.pos[2 * p];
@@ -256,6 +262,7 @@ __global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs 
         const double gf_old = s.dhdr[kDGbestJ];
         const int improved = (s.pbf[g] < gf_old) ? 1 : 0;
         s.hdr[kHGbest] = g;
+        if (a.tr_gbest && t < a.tr_max) a.tr_gbest[t] = g;
         if (a.mode == PIFCM_FIT_CHAINED) {
             for (int q = 0; q < a.Pl; ++q) s.cur[q] = s.nxt[q];
             if (improved) {

@@ -28,6 +28,10 @@ struct pifcm_ctx {
     size_t tused = 0;               // events in use
     double t_ms[2] = {0.0, 0.0}, t_bytes[2] = {0.0, 0.0};
     long long t_launches[2] = {0, 0};
+    // pifcm_pso_trace
+    double *tr_f = nullptr, *tr_pos = nullptr;
+    int *tr_gbest = nullptr;
+    int tr_max = 0;
 };
 
 namespace {
@@ -561,6 +565,15 @@ int pifcm_pso_eval(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg 
     return PIFCM_OK;
 }
 
+int pifcm_pso_trace(pifcm_ctx *ctx, double *f, double *pos, int32_t *gbest, int32_t max_gen) {
+    if (!ctx) return PIFCM_EINVAL;
+    const bool off = !f && !pos && !gbest;
+    if (!off && (!f || !pos || !gbest || max_gen < 1))
+        return fail(ctx, PIFCM_EINVAL, "pifcm_pso_trace: f, pos, gbest all non-NULL with max_gen >= 1, or all NULL");
+    ctx->tr_f = f; ctx->tr_pos = pos; ctx->tr_gbest = gbest; ctx->tr_max = off ? 0 : max_gen;
+    return PIFCM_OK;
+}
+
 int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
                      const float *x, void *ws, size_t ws_bytes, pifcm_stream stream) {
     Layout L;
@@ -574,6 +587,7 @@ int pifcm_pso_update(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cf
     a.nslots = L.nslots; a.tol = pso->tol; a.vmax = pso->vmax; a.mode = L.mode;
     a.batched = L.eb < L.Pl ? 1 : 0;
     a.key0 = (uint32_t)(pso->seed & 0xFFFFFFFFu); a.key1 = (uint32_t)(pso->seed >> 32);
+    a.tr_f = ctx->tr_f; a.tr_pos = ctx->tr_pos; a.tr_gbest = ctx->tr_gbest; a.tr_max = ctx->tr_max;
     LAUNCH(ctx, 1, launch_pso_update(a, st));
     if (L.mode == PIFCM_FIT_CHAINED) return PIFCM_OK;
     // ANCHORED: on an improvement, the snapshot = one step from the start at the

@@ -120,6 +120,11 @@ struct PsoUpdateArgs {
     int batched;  // CHAINED with batched evaluation: next slots assigned per batch (k_assign_batch)
     double tol, vmax;
     uint32_t key0, key1;
+    // optional per-generation record (pifcm_pso_trace): f[t][P], evaluation
+    // positions [t][P][2], gbest index [t] for t < tr_max; NULL = off
+    double *tr_f, *tr_pos;
+    int *tr_gbest;
+    int tr_max;
 };
 
 // z-slab exchange over peer memory (p2p.cu)

@@ -234,3 +234,23 @@ def test_segment_small(orc):
     _, _, J00, _ = orc.ifcm_step(x, U, c, 0.0, 0.0)
     assert r.J <= J00
     assert (np.diff(np.sort(r.c)) > 0).all()
+
+
+def test_segment_equals_its_parts(orc):
+    """orc_segment_u8 = gmm_init -> fcm_run -> pso_run -> ifcm_run -> argmax
+    (Alg. 1 steps 2-11): the end-to-end GPU test at C3 runs the
+    oracle through these parts to get the swarm trace, so they must compose to
+    the whole pipeline exactly."""
+    from inputs import add_noise_u8, cube_phantom
+    img, _ = cube_phantom(20, 18, 6, (0.1, 0.35, 0.65, 0.9))
+    vol = add_noise_u8(img, 9.0, 11)
+    r = orc.segment_u8(vol, C=4, P=5, max_gen=4, seed=99)
+    x = orc.normalize_u8(vol)
+    c0 = orc.gmm_init(orc.histogram_u8(vol), 4)
+    U1, c1, _ = orc.fcm_run(x, c0)
+    p = orc.pso_run(x, U1, c1, P=5, max_gen=4, seed=99)
+    Uf, cf, it, _ = orc.ifcm_run(x, p.U, p.c, p.lam, p.xi)
+    assert (p.lam, p.xi) == (r.lam, r.xi)
+    assert it == r.final_iters
+    assert np.array_equal(orc.argmax(Uf).reshape(vol.shape), r.labels)
+    assert np.array_equal(cf, r.c)
