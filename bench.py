@@ -398,6 +398,10 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = vp_e2e / (float(te.item()) * 1e-3)
 
+    dump = os.environ.get("PIFCM_BENCH_DUMP")  # test hook: the last e2e step's labels and (lambda*, xi*)
+    if dump and rank == 0:
+        np.savez(dump, labels=lab_h.numpy(), lam_xi=np.array([r["lambda"], r["xi"]]),
+                 final_iters=np.array(r["final_iters"]))
     if rank != 0:
         if dist is not None:
             dist.barrier()

@@ -70,7 +70,7 @@ typedef enum {
     PIFCM_EALIGN = -2,   /* pitch / pointer alignment violated (16-byte rows required) */
     PIFCM_ENOMEM = -3,   /* workspace smaller than pifcm_workspace_size() */
     PIFCM_ECUDA = -4,    /* a CUDA runtime error (launch or asynchronous) */
-    PIFCM_ENCCL = -5,    /* reserved: collectives are done by the caller (torch.distributed) */
+    PIFCM_ENCCL = -5,    /* the context's communicator failed (NCCL load / init / collective, or a host collective) */
     PIFCM_ENUMERIC = -6, /* non-finite cost J */
     PIFCM_ESTATE = -7    /* call order violated (e.g. pso_step before pso_init) */
 } pifcm_status;
@@ -162,6 +162,49 @@ void pifcm_ctx_destroy(pifcm_ctx *ctx);
 const char *pifcm_last_error(const pifcm_ctx *ctx);
 /* Library version string. */
 const char *pifcm_version(void);
+
+/* ----------------------------------------------------------- multi-process */
+/* The particle-sharded pipeline (SURVEY 8(b) pifcm_dist, 8(e)).  The PSO's
+ * particles are independent within a generation (Alg. 1 step 4), so
+ * rank r of `world` evaluates the contiguous range pifcm_dist_range(P, world,
+ * r) (20 over 8 -> 3,3,3,3,2,2,2,2); the only exchanges are the all-gather of
+ * the fitness vector every generation (step 4 -> 5) and the broadcast of the
+ * gbest state from its owner before the final IFCM (steps 10-11,
+ * PAPER:104-105).  Every rank runs the identical fp64 PSO update and the
+ * final IFCM in the canonical decomposition, so labels, centres and
+ * (lambda*, xi*) are bit-identical to the single-process pifcm_segment on
+ * every rank. */
+typedef struct {
+    int32_t rank, world;             /* this process, number of processes        */
+    const uint8_t *nccl_unique_id;   /* 128 bytes from pifcm_nccl_unique_id (one
+                                        rank creates it, the caller shares it);
+                                        ignored when host collectives are given */
+    int32_t shard;                   /* 0 = particles (the only C-level sharding;
+                                        the z-slab final IFCM is pifcm_slab_*)   */
+} pifcm_dist;
+/* Host-memory collectives supplied by the caller (gloo, MPI, ...; e.g. ranks
+ * sharing one GPU, which NCCL refuses).  Both return 0 on success; they are
+ * called synchronously, in the same order, on every rank. */
+typedef struct {
+    void *user;
+    /* dst[world][bytes] <- every rank's src[bytes], in rank order */
+    int (*allgather)(void *user, const void *src, void *dst, size_t bytes);
+    /* buf[bytes] on every rank <- buf of rank `root` */
+    int (*broadcast)(void *user, void *buf, size_t bytes, int32_t root);
+} pifcm_host_coll;
+/* 128-byte NCCL unique id (ncclGetUniqueId of the libnccl.so.2 the library
+ * loads with dlopen).  PIFCM_ENCCL when NCCL cannot be loaded. */
+int pifcm_nccl_unique_id(uint8_t id[128]);
+/* Attach a communicator to ctx (the ctx owns it; a previous one is freed):
+ * NCCL (ncclCommInitRank on ctx's device; collective over all ranks, blocks
+ * until every rank has called it) unless `coll` is non-NULL, in which case
+ * the caller's host collectives are used.  world == 1 detaches.  Errors:
+ * PIFCM_EINVAL (rank outside [0, world), shard != 0, missing id / callbacks),
+ * PIFCM_ENCCL (NCCL load or init). */
+int pifcm_ctx_dist(pifcm_ctx *ctx, const pifcm_dist *dist, const pifcm_host_coll *coll);
+/* The particle range [*p_begin, *p_end) of `rank`: what pifcm_pso_cfg.p_begin
+ * / p_end must hold (and the workspace be sized for) on that rank. */
+int pifcm_dist_range(int32_t P, int32_t world, int32_t rank, int32_t *p_begin, int32_t *p_end);
 
 /* --------------------------------------------------------------- workspace */
 /* Bytes of device workspace needed by pso_* / segment calls for this grid and
@@ -360,7 +403,12 @@ int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float 
  *            the whole volume is segmented in 3D (R10) and only plane z_slice
  *            of `labels` is written (labels then points to [ny][nx]).
  *   rep      host out, nullable.
- * Errors: as above, plus PIFCM_ENUMERIC for a non-finite fitness. */
+ * With a communicator attached (pifcm_ctx_dist, world > 1) the PSO is
+ * particle-sharded: pso->p_begin / p_end must be this rank's
+ * pifcm_dist_range (and ws sized for it); every rank returns the same labels
+ * and report, bit-identical to the single-process call (CHAINED fitness).
+ * Errors: as above, plus PIFCM_ENUMERIC for a non-finite fitness and
+ * PIFCM_ENCCL for a failed collective. */
 int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, int32_t ny,
                   int32_t nz, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
                   int32_t z_slice, void *ws, size_t ws_bytes, uint8_t *labels, float *U_out,

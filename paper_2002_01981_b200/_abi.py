@@ -54,6 +54,19 @@ class Report(ct.Structure):
                 ("t_final", ct.c_double), ("t_total", ct.c_double)]
 
 
+class Dist(ct.Structure):
+    _fields_ = [("rank", ct.c_int32), ("world", ct.c_int32), ("nccl_unique_id", ct.c_void_p),
+                ("shard", ct.c_int32)]
+
+
+HOST_ALLGATHER = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_void_p, ct.c_size_t)
+HOST_BROADCAST = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_size_t, ct.c_int32)
+
+
+class HostColl(ct.Structure):
+    _fields_ = [("user", ct.c_void_p), ("allgather", HOST_ALLGATHER), ("broadcast", HOST_BROADCAST)]
+
+
 MAX_PEERS = 16
 
 
@@ -90,6 +103,10 @@ SIGNATURES = {
     "pifcm_pso_fitness_ptr": (ct.c_int, [_G, _C, _P, _vp, ct.POINTER(_vp)]),
     "pifcm_pso_update": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_trace": (ct.c_int, [_vp, _vp, _vp, _vp, ct.c_int32]),
+    "pifcm_nccl_unique_id": (ct.c_int, [_vp]),
+    "pifcm_ctx_dist": (ct.c_int, [_vp, ct.POINTER(Dist), ct.POINTER(HostColl)]),
+    "pifcm_dist_range": (ct.c_int, [ct.c_int32, ct.c_int32, ct.c_int32, ct.POINTER(ct.c_int32),
+                                    ct.POINTER(ct.c_int32)]),
     "pifcm_pso_step": (ct.c_int, [_vp, _G, _C, _P, _vp, _vp, ct.c_size_t, _vp]),
     "pifcm_pso_result_get": (ct.c_int, [_vp, _G, _C, _P, _vp, ct.POINTER(PsoResult),
                                         ct.POINTER(ct.c_int32), _vp]),

@@ -157,6 +157,60 @@ class Context:
         if rc != 0:
             raise PifcmError(rc, self.lib.pifcm_last_error(self._h).decode())
 
+    # ------------------------------------------------------------ multi-process
+    def attach_dist(self, rank: int, world: int, pg=None, backend: str = "nccl"):
+        """pifcm_ctx_dist: give this context a communicator for the
+        particle-sharded pifcm_segment.  backend "nccl": NCCL inside the
+        library (rank 0's pifcm_nccl_unique_id is shared through the
+        torch.distributed process group `pg`); "host": the library calls back
+        into torch.distributed (gloo) with host buffers -- ranks sharing a GPU.
+        world == 1 detaches."""
+        import torch.distributed as tdist
+        d = _abi.Dist(rank, world, None, 0)
+        coll = None
+        if world > 1 and backend == "nccl":
+            uid = (ct.c_uint8 * 128)()
+            if rank == 0:
+                rc = self.lib.pifcm_nccl_unique_id(uid)
+                if rc != 0:
+                    raise PifcmError(rc, "pifcm_nccl_unique_id failed")
+            obj = [bytes(uid)]
+            tdist.broadcast_object_list(obj, src=0, group=pg)
+            uid = (ct.c_uint8 * 128).from_buffer_copy(obj[0])
+            self._uid = uid
+            d.nccl_unique_id = ct.cast(uid, ct.c_void_p)
+        elif world > 1:
+            def _ag(user, src, dst, n):
+                try:
+                    t = torch.frombuffer(bytearray(ct.string_at(src, n)), dtype=torch.uint8)
+                    out = [torch.empty(n, dtype=torch.uint8) for _ in range(world)]
+                    tdist.all_gather(out, t, group=pg)
+                    cat = torch.cat(out).numpy()  # (kept alive across the copy)
+                    ct.memmove(dst, cat.ctypes.data, n * world)
+                    return 0
+                except Exception:
+                    return 1
+
+            def _bc(user, buf, n, root):
+                try:
+                    t = torch.frombuffer(bytearray(ct.string_at(buf, n)), dtype=torch.uint8)
+                    tdist.broadcast(t, src=root, group=pg)
+                    arr = t.numpy()
+                    ct.memmove(buf, arr.ctypes.data, n)
+                    return 0
+                except Exception:
+                    return 1
+
+            coll = _abi.HostColl(None, _abi.HOST_ALLGATHER(_ag), _abi.HOST_BROADCAST(_bc))
+            self._coll = coll  # keep the callbacks alive
+        self._ck(self.lib.pifcm_ctx_dist(self._h, ct.byref(d), ct.byref(coll) if coll is not None else None))
+        self.rank, self.world = rank, world
+
+    def dist_range(self, P: int, world: int, rank: int) -> tuple[int, int]:
+        a, b = ct.c_int32(), ct.c_int32()
+        self._ck(self.lib.pifcm_dist_range(P, world, rank, ct.byref(a), ct.byref(b)))
+        return a.value, b.value
+
     def launch_count(self) -> int:
         return int(self.lib.pifcm_launch_count(self._h))
 

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "pifcm_comm.h"
 #include "pifcm_internal.cuh"
 
 using namespace pifcm;
@@ -28,6 +29,7 @@ struct pifcm_ctx {
     size_t tused = 0;               // events in use
     double t_ms[2] = {0.0, 0.0}, t_bytes[2] = {0.0, 0.0};
     long long t_launches[2] = {0, 0};
+    pifcm::Comm comm;  // pifcm_ctx_dist
     // pifcm_pso_trace
     double *tr_f = nullptr, *tr_pos = nullptr;
     int *tr_gbest = nullptr;
@@ -334,12 +336,38 @@ int pifcm_ctx_create(int device, pifcm_ctx **out) {
 
 void pifcm_ctx_destroy(pifcm_ctx *ctx) {
     if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    pifcm::comm_free(ctx->comm);
     for (int i = 0; i < 8; ++i) cudaEventDestroy(ctx->ev[i]);
     for (cudaEvent_t e : ctx->tev) cudaEventDestroy(e);
     delete ctx;
 }
 
 const char *pifcm_last_error(const pifcm_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int pifcm_nccl_unique_id(uint8_t id[128]) {
+    if (!id) return PIFCM_EINVAL;
+    std::string err;
+    return pifcm::comm_unique_id(id, err);
+}
+
+int pifcm_ctx_dist(pifcm_ctx *ctx, const pifcm_dist *dist, const pifcm_host_coll *coll) {
+    if (!ctx) return PIFCM_EINVAL;
+    if (!dist) return fail(ctx, PIFCM_EINVAL, "dist is NULL");
+    if (dist->world < 1) return fail(ctx, PIFCM_EINVAL, "world = %d < 1", dist->world);
+    std::string err;
+    const int r = pifcm::comm_init(ctx->comm, ctx->device, dist, coll, err);
+    return r ? fail(ctx, r, "pifcm_ctx_dist: %s", err.c_str()) : PIFCM_OK;
+}
+
+int pifcm_dist_range(int32_t P, int32_t world, int32_t rank, int32_t *p_begin, int32_t *p_end) {
+    if (!p_begin || !p_end || P < 1 || world < 1 || rank < 0 || rank >= world) return PIFCM_EINVAL;
+    int a, b;
+    pifcm::dist_range(P, world, rank, &a, &b);
+    *p_begin = a;
+    *p_end = b;
+    return PIFCM_OK;
+}
 
 int64_t pifcm_launch_count(const pifcm_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
@@ -864,8 +892,16 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     Layout L;
     int r = pso_common(ctx, &g, cfg, pso, ws, ws_bytes, &L);
     if (r) return r;
-    if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
-        return fail(ctx, PIFCM_EINVAL, "pifcm_segment is single-process");
+    const bool sharded = ctx->comm.world > 1;
+    if (sharded) {
+        int a, b;
+        pifcm::dist_range(pso->P, ctx->comm.world, ctx->comm.rank, &a, &b);
+        if (pso->p_begin != a || pso->p_end != b)
+            return fail(ctx, PIFCM_EINVAL, "rank %d of %d must evaluate particles [%d, %d) (pifcm_dist_range), not [%d, %d)",
+                        ctx->comm.rank, ctx->comm.world, a, b, pso->p_begin, pso->p_end);
+    } else if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P)) {
+        return fail(ctx, PIFCM_EINVAL, "a particle sub-range needs a communicator (pifcm_ctx_dist)");
+    }
     if (z_slice < -1 || z_slice >= nz) return fail(ctx, PIFCM_EINVAL, "z_slice %d out of range", z_slice);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     CK(ctx, cudaSetDevice(ctx->device));
@@ -924,13 +960,55 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     CK(ctx, cudaEventRecord(ev[2], st));
     // Alg. 1 steps 3-10: PSO (c0 now holds the FCM centres for pso_init)
     pifcm_pso_result pres;
-    if ((r = pifcm_pso_run(ctx, &g, cfg, pso, x, reinterpret_cast<float *>(slots), c0, ws, ws_bytes, &pres, stream)))
-        return r;
+    if (!sharded) {
+        if ((r = pifcm_pso_run(ctx, &g, cfg, pso, x, reinterpret_cast<float *>(slots), c0, ws, ws_bytes, &pres,
+                               stream)))
+            return r;
+    } else {
+        // particle-sharded generations: local evaluation, fitness all-gather,
+        // the identical update on every rank (Alg. 1 steps 4-9)
+        if ((r = pifcm_pso_init(ctx, &g, cfg, pso, reinterpret_cast<float *>(slots), c0, ws, ws_bytes, stream)))
+            return r;
+        for (int gen = 0; gen < pso->max_gen; ++gen) {
+            if ((r = pifcm_pso_eval(ctx, &g, cfg, pso, x, ws, ws_bytes, stream))) return r;
+            std::string err;
+            if ((r = pifcm::comm_allgather_fitness(ctx->comm, s.fit, pso->P, st, err)))
+                return fail(ctx, r, "fitness all-gather: %s", err.c_str());
+            if ((r = pifcm_pso_update(ctx, &g, cfg, pso, x, ws, ws_bytes, stream))) return r;
+            if (pso->patience > 0 && (gen + 1) % 4 == 0) {
+                int32_t stopped = 0;
+                if ((r = pifcm_pso_result_get(ctx, &g, cfg, pso, ws, &pres, &stopped, stream))) return r;
+                if (stopped) break;
+            }
+        }
+        if ((r = pifcm_pso_result_get(ctx, &g, cfg, pso, ws, &pres, nullptr, stream))) return r;
+    }
     CK(ctx, cudaEventRecord(ev[3], st));
     // Alg. 1 step 11: final IFCM from the gbest state at (lambda*, xi*)
     int gs = -1;
     CK(ctx, cudaMemcpyAsync(&gs, s.hdr + kHGbestSlot, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(ctx, cudaStreamSynchronize(st));
+    if (sharded && L.mode == PIFCM_FIT_CHAINED) {
+        // Alg. 1 step 10 across ranks: the owner's gbest state (slot + centres)
+        // into slot 0 of every rank
+        int owner = 0;
+        for (int q = 0; q < ctx->comm.world; ++q) {
+            int a, b;
+            pifcm::dist_range(pso->P, ctx->comm.world, q, &a, &b);
+            if (pres.gbest_particle >= a && pres.gbest_particle < b) owner = q;
+        }
+        if (ctx->comm.rank == owner) {
+            if (gs < 0) return fail(ctx, PIFCM_ESTATE, "gbest owner holds no gbest state");
+            if (gs != 0)
+                CK(ctx, cudaMemcpyAsync(slots, slots + (long long)gs * L.nvox, sizeof(float4) * (size_t)L.nvox,
+                                        cudaMemcpyDeviceToDevice, st));
+        }
+        std::string err;
+        if ((r = pifcm::comm_broadcast(ctx->comm, slots, sizeof(float4) * (size_t)L.nvox, owner, st, err)) ||
+            (r = pifcm::comm_broadcast(ctx->comm, s.gbest_c, sizeof(float) * 4, owner, st, err)))
+            return fail(ctx, r, "gbest broadcast: %s", err.c_str());
+        gs = 0;
+    }
     if (gs < 0) return fail(ctx, PIFCM_ESTATE, "no gbest state after PSO");
     const int other = (gs == 0) ? 1 : 0;
     CK(ctx, cudaMemcpyAsync(cent, s.gbest_c, sizeof(float) * 4, cudaMemcpyDeviceToDevice, st));

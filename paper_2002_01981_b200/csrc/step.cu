@@ -492,7 +492,9 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
     const int blk = blockIdx.x + gridDim.x * blockIdx.y;
     block_partials<kWarpsY>(num, den, Jacc, duacc, a.partials + ((long long)p * a.nblk + blk) * kNR);
-    finalize_if_last<kStepThreads>(a, p, a.nblk);
+    // the ring is idle now: its shared memory is the finaliser's scratch
+    // (no static 10 KB array, which would cost a CTA slot per SM)
+    finalize_if_last<kStepThreads>(a, p, a.nblk, reinterpret_cast<double(*)[kNR]>(smem_raw));
 }
 
 // ----------------------------------------------------------------------------

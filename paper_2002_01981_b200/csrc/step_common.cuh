@@ -112,21 +112,14 @@ __device__ __forceinline__ void block_partials(const float (&num)[kMaxC], const 
     }
 }
 
-// Finalisation by the last CTA of state p (threadFenceReduction pattern):
-// the fixed-order fp64 sum of the nblk partial records, then Eq. 3:
-// c_j = sum u^m x / sum u^m (c_j kept if the sum < 1e-12, R9) and Eq. 1
-// (PAPER:53): J = sum of the per-voxel costs.  The summation order does not
-// depend on which CTA finishes last.
+// Fixed-order fp64 sum of the nblk partial records of state p, then Eq. 3
+// (PAPER:57): c_j = sum u^m x / sum u^m (c_j kept if the sum < 1e-12, R9) and
+// Eq. 1: J = sum of the per-voxel costs.  All NT threads of the CTA
+// take part; red is NT x kNR doubles of shared memory.  The summation order
+// depends on nblk and NT only, not on which CTA runs it (k_slab_finalize uses
+// the same order for records gathered across z-slab ranks).
 template <int NT>
-__device__ __forceinline__ void finalize_if_last(const StepArgs &a, int p, int nblk) {
-    __shared__ int is_last;
-    __shared__ double red[NT][kNR];
-    if (a.counters == nullptr) return;  // z-slab mode: records are combined across ranks
-    __syncthreads();
-    if (threadIdx.x == 0) is_last = (atomicAdd(&a.counters[p], 1u) == (unsigned)(nblk - 1));
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
+__device__ __forceinline__ void finalize_state(const StepArgs &a, int p, int nblk, double (*red)[kNR]) {
     const double *src = a.partials + (long long)p * nblk * kNR;
     double v[kNR];
 #pragma unroll
@@ -163,6 +156,26 @@ __device__ __forceinline__ void finalize_if_last(const StepArgs &a, int p, int n
         if (!isfinite(J) && a.status) atomicExch(a.status, (int)PIFCM_ENUMERIC);
         a.counters[p] = 0u;  // ready for the next launch
     }
+    __syncthreads();  // red is reused by the caller
+}
+
+// Finalisation by the last CTA of state p (threadFenceReduction pattern);
+// red: NT x kNR doubles of shared memory the caller no longer needs.
+template <int NT>
+__device__ __forceinline__ void finalize_if_last(const StepArgs &a, int p, int nblk, double (*red)[kNR]) {
+    __shared__ int is_last;
+    if (a.counters == nullptr) return;  // z-slab mode: records are combined across ranks
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(&a.counters[p], 1u) == (unsigned)(nblk - 1));
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    finalize_state<NT>(a, p, nblk, red);
+}
+template <int NT>
+__device__ __forceinline__ void finalize_if_last(const StepArgs &a, int p, int nblk) {
+    __shared__ double red[NT][kNR];
+    finalize_if_last<NT>(a, p, nblk, red);
 }
 
 // ----------------------------------------------------------------------------

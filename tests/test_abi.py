@@ -91,3 +91,18 @@ def test_eq11_host_matches_oracle(orc):
     import pytest
     with pytest.raises(PifcmError):
         eq11([[1.0]], [[1.0]], 1.5)
+
+
+def test_dist_range_matches_shard_range():
+    """pifcm_dist_range (C) is the split the Python drivers use (dist.shard_range)."""
+    import ctypes as ct
+    from paper_2002_01981_b200 import _abi
+    from paper_2002_01981_b200.dist import shard_range
+    lib = _abi.load()
+    a, b = ct.c_int32(), ct.c_int32()
+    for P in (1, 5, 20, 32, 33, 64):
+        for world in (1, 2, 3, 8):
+            for r in range(world):
+                assert lib.pifcm_dist_range(P, world, r, ct.byref(a), ct.byref(b)) == 0
+                assert (a.value, b.value) == shard_range(P, world, r)
+    assert lib.pifcm_dist_range(4, 2, 2, ct.byref(a), ct.byref(b)) != 0

@@ -81,3 +81,53 @@ def test_sharded_equals_single(nz, shard, eb):
         assert (labels == ref).all()
         assert (lam, xi) == (rep["lambda"], rep["xi"])
         assert fi == rep["final_iters"] and cen == rep["centers"]
+
+
+def _abi_worker(rank, world, port, P, q):
+    """pifcm_segment itself sharded through the C ABI's communicator (the
+    library calls back into gloo for the fitness all-gather and the gbest
+    broadcast; NCCL would be the same calls on separate GPUs)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from dataclasses import replace
+    from paper_2002_01981_b200 import Context, IfcmConfig, PsoConfig
+    ctx = Context(0)
+    ctx.attach_dist(rank, world, backend="host")
+    vol = _case(40)
+    pso = PsoConfig(**dict(PSO, P=P))
+    a, b = ctx.dist_range(P, world, rank)
+    pso = replace(pso, p_begin=a, p_end=b)
+    lab, _, rep = ctx.segment(torch.as_tensor(vol, device="cuda:0"), IfcmConfig(**CFG), pso)
+    q.put((rank, lab.cpu().numpy(), rep["lambda"], rep["xi"], rep["final_iters"], rep["centers"],
+           rep["gbest_particle"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P,world", [(5, 2), (7, 3)])
+def test_abi_sharded_segment_equals_single(P, world):
+    """SURVEY 8(b)'s pifcm_dist: every rank's pifcm_segment returns the
+    single-process labels, (lambda*, xi*), final iterations and centres bit
+    for bit, for uneven particle splits (5 over 2, 7 over 3)."""
+    from paper_2002_01981_b200 import Context, IfcmConfig, PsoConfig
+    ctx = Context(0)
+    vol = _case(40)
+    lab, _, rep = ctx.segment(torch.as_tensor(vol, device="cuda:0"), IfcmConfig(**CFG),
+                              PsoConfig(**dict(PSO, P=P)))
+    ref = lab.cpu().numpy()
+    cm = mp.get_context("spawn")
+    q = cm.Queue()
+    port = _port()
+    procs = [cm.Process(target=_abi_worker, args=(r, world, port, P, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, labels, lam, xi, fi, cen, gb in res:
+        assert (labels == ref).all(), rank
+        assert (lam, xi) == (rep["lambda"], rep["xi"])
+        assert fi == rep["final_iters"] and cen == rep["centers"] and gb == rep["gbest_particle"]

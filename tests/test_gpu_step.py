@@ -78,6 +78,36 @@ def test_step_parity(ctx, orc, shape, C, m, q_mode):
         assert np.abs(U[p].sum(1) - 1).max() < 1e-5
 
 
+@pytest.mark.parametrize("shape,C,m,q_mode", [
+    ((9, 17, 33), 4, 2.0, 0),
+    ((19, 37, 70), 4, 2.0, 1),
+    ((17, 16, 32), 3, 1.5, 0),
+    ((1, 70, 130), 4, 2.0, 0),      # 2D kernel
+])
+def test_step_parity_offgrid_x(ctx, orc, shape, C, m, q_mode):
+    """Intensities off the u8 grid (fp32 values of an f32 volume's
+    normalisation, random in [0, 1)): the same 1e-4 / 1e-4 bounds, one step
+    and three chained steps (3e-4, the per-step bound compounded)."""
+    nz, ny, nx = shape
+    states = [random_state(nx, ny, nz, C, seed=500 + s, u8_levels=False, crisp_frac=0.1) for s in range(3)]
+    x = states[0][0]
+    assert not np.allclose(x * 255, np.round(x * 255))
+    Us = [s[1] for s in states]
+    cs = [s[2] for s in states]
+    lamxi = [(0.3, 0.6), (1.0, 1.0), (0.05, 0.95)]
+    U, c, st = gpu_step(ctx, x, Us, cs, lamxi, C, m=m, q_mode=q_mode)
+    for p in range(3):
+        Uo, co, Jo, _ = orc.ifcm_step(x, Us[p], cs[p], *lamxi[p], m=m, q_mode=q_mode)
+        assert np.abs(U[p] - Uo).max() < U_TOL, p
+        assert np.all(np.abs(c[p] - co) <= C_TOL * np.abs(co) + 1e-7), (c[p], co)
+        assert abs(st[p, 0] - Jo) <= 1e-4 * abs(Jo) + 1e-9
+    U3, c3, _ = gpu_step(ctx, x, Us[:1], cs[:1], lamxi[:1], C, m=m, q_mode=q_mode, iters=3)
+    Uo, co = Us[0].astype(np.float64), cs[0].astype(np.float64)
+    for _ in range(3):
+        Uo, co, _, _ = orc.ifcm_step(x, Uo, co, *lamxi[0], m=m, q_mode=q_mode)
+    assert np.abs(U3[0] - Uo).max() < 3e-4
+
+
 CASES_V2 = [
     # (nz, ny, nx), C, m, q_mode, h -- two Chebyshev shells (NEXT-2, Eq. 10)
     ((1, 9, 9), 2, 2.0, 0, 1.0),

@@ -14,6 +14,8 @@ from paper_2002_01981_b200 import Context, IfcmConfig, PsoConfig
 from paper_2002_01981_b200.api import _grid
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "segment"
+# "time": device time per launch of the P = 32 fused step and of the
+# single-state canonical launches of the final IFCM (CUDA events)
 ctx = Context(0)
 vol, _ = config_volume("C3")
 nz, ny, nx = vol.shape
@@ -42,3 +44,21 @@ if mode == "time":
     ms, n, b = ctx.timing_read()
     print(f"fused step: {ms / n:.3f} ms/launch, {b / n / 1e9:.3f} GB alg/launch, "
           f"{(b / n) / (ms / n * 1e-3) / 1e9:.1f} GB/s, {32 * nz * ny * nx / (ms / n * 1e-3) / 1e9:.1f} G vp/s")
+
+if mode == "time":
+    # single-state canonical launches (the final IFCM's decomposition)
+    nvox = nz * ny * nx
+    Ua = U0.view(1, nvox, 4).clone()
+    Ub = torch.empty_like(Ua)
+    cen = c0.clone().view(1, 4)
+    lx = torch.tensor([[1.0, 1.0]], dtype=torch.float64, device="cuda:0")
+    for _ in range(5):
+        ctx.iterate(x, Ua, Ub, cen, lx, cfg, iters=1, nx=nx, canonical=True)
+        Ua, Ub = Ub, Ua
+    ctx.timing_enable(False)
+    ctx.timing_enable(True)
+    for _ in range(40):
+        ctx.iterate(x, Ua, Ub, cen, lx, cfg, iters=1, nx=nx, canonical=True)
+        Ua, Ub = Ub, Ua
+    ms, n, b = ctx.timing_read(batched=False)
+    print(f"single state: {ms / n * 1e3:.1f} us/launch, {(b / n) / (ms / n * 1e-3) / 1e9:.1f} GB/s")
