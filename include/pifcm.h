@@ -108,7 +108,7 @@ typedef struct {
 typedef struct {
     int32_t C;        /* clusters, 2..4 on the device path                      */
     float m;          /* fuzzifier, m > 1 (Eq. 2); m == 2 takes a fast path     */
-    int32_t v;        /* shells (Eq. 10); only v == 1 on the device path (R2)   */
+    int32_t v;        /* shells (Eq. 9-10, R2): 1 (26 neighbours), 2 (124), 3 (342) */
     float h;          /* Eq. 10 decay (> 0); irrelevant at v == 1               */
     int32_t q_mode;   /* pifcm_qmode (R1)                                       */
     float eps;        /* stop when max|u_new - u_old| < eps (R14); <= 0: never   */

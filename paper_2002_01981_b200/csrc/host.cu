@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "pifcm_comm.h"
 #include "pifcm_internal.cuh"
 
@@ -87,7 +89,7 @@ int check_cfg(pifcm_ctx *ctx, const pifcm_ifcm_cfg *c) {
     if (!c) return fail(ctx, PIFCM_EINVAL, "cfg is NULL");
     if (c->C < 2 || c->C > kMaxC) return fail(ctx, PIFCM_EINVAL, "C = %d outside [2, 4]", c->C);
     if (!(c->m > 1.0f) || !(c->m < 1e6f)) return fail(ctx, PIFCM_EINVAL, "m = %g must be > 1", (double)c->m);
-    if (c->v != 1 && c->v != 2) return fail(ctx, PIFCM_EINVAL, "v = %d: the device path has v = 1 and v = 2", c->v);
+    if (c->v < 1 || c->v > kMaxV) return fail(ctx, PIFCM_EINVAL, "v = %d: the device path has v = 1 .. %d", c->v, kMaxV);
     if (!(c->h > 0.0f)) return fail(ctx, PIFCM_EINVAL, "h must be > 0");
     if (c->q_mode != PIFCM_Q_LITERAL && c->q_mode != PIFCM_Q_SQEUCLID)
         return fail(ctx, PIFCM_EINVAL, "q_mode %d unknown", c->q_mode);
@@ -237,10 +239,10 @@ void set_shells(StepArgs &a, const pifcm_ifcm_cfg *cfg) {
     a.v = cfg->v;
     double s = 0.0;
     for (int r = 1; r <= cfg->v; ++r) s += exp(-(double)r / (double)cfg->h);
-    a.w1d = exp(-1.0 / (double)cfg->h) / s;
-    a.w2d = cfg->v >= 2 ? exp(-2.0 / (double)cfg->h) / s : 0.0;
-    a.w1 = (float)a.w1d;
-    a.w2 = (float)a.w2d;
+    for (int r = 1; r <= kMaxV; ++r) {  // Eq. 10
+        a.wshd[r - 1] = r <= cfg->v ? exp(-(double)r / (double)cfg->h) / s : 0.0;
+        a.wsh[r - 1] = (float)a.wshd[r - 1];
+    }
 }
 
 // A step launch, bracketed by CUDA events on its stream when timing is on
@@ -916,6 +918,17 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     SwarmDev s = swarm_of(ws, L);
     int *status = s.hdr + kHStatus;
     float *cent = s.centers;  // [Pl][4]; entry 0 reused by the FCM start and the final IFCM
+    // NVTX ranges per phase (SURVEY 5 tracing; no cost without a profiler)
+    struct Nvtx {
+        bool open = false;
+        void phase(const char *name) {
+            if (open) nvtxRangePop();
+            nvtxRangePushA(name);
+            open = true;
+        }
+        ~Nvtx() { if (open) nvtxRangePop(); }
+    } nvtx;
+    nvtx.phase("pifcm: normalize (Alg. 2 step 1)");
     CK(ctx, cudaEventRecord(ev[0], st));
     // Alg. 2 step 1: normalise (+ histogram for the GMM start)
 
@@ -924,6 +937,7 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     LAUNCH(ctx, 1, launch_normalize(vol, dtype, nx, ny, nz, g.pitch, mm, x, st));
     LAUNCH(ctx, 2, launch_hist(vol, dtype, L.nvox, mm, hist, st));
     CK(ctx, cudaEventRecord(ev[1], st));
+    nvtx.phase("pifcm: GMM + FCM start (Alg. 1 step 2)");
     // Alg. 1 step 2: GMM centres, then FCM (lambda = xi = 0) until eps
     LAUNCH(ctx, 1, launch_gmm(hist, cfg->C, 100, c0, st));
     float cinit[4];
@@ -958,6 +972,7 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     }
     CK(ctx, cudaMemcpyAsync(c0, cent, sizeof(float) * 4, cudaMemcpyDeviceToDevice, st));
     CK(ctx, cudaEventRecord(ev[2], st));
+    nvtx.phase("pifcm: PSO (Alg. 1 steps 3-10)");
     // Alg. 1 steps 3-10: PSO (c0 now holds the FCM centres for pso_init)
     pifcm_pso_result pres;
     if (!sharded) {
@@ -984,6 +999,7 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
         if ((r = pifcm_pso_result_get(ctx, &g, cfg, pso, ws, &pres, nullptr, stream))) return r;
     }
     CK(ctx, cudaEventRecord(ev[3], st));
+    nvtx.phase("pifcm: final IFCM (Alg. 1 step 11)");
     // Alg. 1 step 11: final IFCM from the gbest state at (lambda*, xi*)
     int gs = -1;
     CK(ctx, cudaMemcpyAsync(&gs, s.hdr + kHGbestSlot, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1019,6 +1035,7 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
                        at<unsigned>(ws, L.cnt), st, &fin_slot, &fin_iters)))
         return r;
     CK(ctx, cudaEventRecord(ev[4], st));
+    nvtx.phase("pifcm: defuzzify");
     // defuzzify (+ optional U copy)
     const float4 *Ufin = slots + (long long)fin_slot * L.nvox;
     if (z_slice < 0) {

@@ -11,6 +11,7 @@ namespace pifcm {
 // ---------------------------------------------------------------- constants
 constexpr int kMaxC = 4;          // AoS-C4 rows: one float4 per voxel
 constexpr int kNR = 2 * kMaxC + 2; // partial record: num[4], den[4], J, max|du|
+constexpr int kMaxV = 3;          // shells on the device path (Eq. 9-10; v = 1 the hot kernel, 2..3 step_shells.cu)
 constexpr float kAFloor = 1e-9f;  // R4: floor of 1 - lam H - xi F (Eq. 4)
 constexpr double kDenEps = 1e-12; // R9: keep c_j if sum u^m < 1e-12 (Eq. 3)
 // Ill-conditioned voxels: u_j moves by u_j (1 - u_j) / ((m-1) a_j) per unit
@@ -39,7 +40,6 @@ constexpr int kRY = PIFCM_RY;           // consecutive y rows per thread (regist
 constexpr int kTY = kWarpsY * kRY;  // 16
 constexpr int kSX = kTX + 2;        // haloed smem row length
 constexpr int kSY = kTY + 2;        // haloed smem rows
-constexpr int kStages = 4;          // plane ring: z-1, z, z+1 resident, z+2 landing
 #ifndef PIFCM_TZ
 #define PIFCM_TZ 32
 #endif
@@ -88,8 +88,8 @@ struct StepArgs {
     int *status;         // nullable: PIFCM_ENUMERIC on a non-finite J
     float4 *hf;          // non-null: emit H (float4) and F (float4) per voxel [nvox][2] instead of a step
     int v;               // neighbourhood shells (Eq. 9-10): 1 = the 26-neighbourhood, 2 = two shells
-    float w1, w2;        // Eq. 10 shell weights W_1, W_2 (v = 2)
-    double w1d, w2d;     // the same in fp64 (ill-conditioned re-evaluation)
+    float wsh[kMaxV];    // Eq. 10 shell weights W_1 .. W_v (v >= 2)
+    double wshd[kMaxV];  // the same in fp64 (ill-conditioned re-evaluation)
 };
 
 // Swarm state in the workspace (all device pointers).
@@ -173,7 +173,7 @@ struct FcmHistArgs {
 // ---------------------------------------------------------------- launchers
 // All return cudaGetLastError() of the launch.
 cudaError_t launch_step(const StepArgs &a, int C, bool stencil, int P, cudaStream_t st);
-cudaError_t launch_step_v2(const StepArgs &a, int C, int P, cudaStream_t st);  // step_v2.cu
+cudaError_t launch_step_shells(const StepArgs &a, int C, int P, cudaStream_t st);  // step_shells.cu (v = 2, 3)
 int step_nblk(int nx, int ny, int nz, bool stencil, int P);
 int slab_tz(int nx, int ny, int nz_total);
 int step_nblk_max(int nx, int ny, int nz);

@@ -13,8 +13,9 @@
 //
 // Data layout: x fp32 [nz][ny][pitch]; U fp32 AoS-C4 [state][nz][ny][nx][4].
 // CTA = 32 x 16 voxels per plane (4 warps, 4 y-rows per thread), marching
-// kTZ planes in z through a 4-stage shared-memory ring filled by cp.async
-// (zero-filled outside the volume, so out-of-bounds neighbours contribute 0
+// a z-chunk through a kRing-stage (5) shared-memory ring of haloed planes
+// filled by TMA (cp.async.bulk.tensor, one mbarrier per stage; boxes are
+// zero-filled outside the volume, so out-of-bounds neighbours contribute 0
 // to every numerator).  Because every U row sums to 1, the Eq. 5
 // denominator is recovered as G_i = sum_j Hn_ij = sum_k g_ik sum_j u_kj, which
 // automatically excludes out-of-bounds neighbours; the Eq. 7 denominator is a
@@ -28,7 +29,7 @@
 
 namespace pifcm {
 
-// Shared-memory ring: kStages planes of the haloed U tile (float4) and of the
+// Shared-memory ring: kRing planes of the haloed U tile (float4) and of the
 // intensity tile (float, rows padded to kSXP for 16-byte TMA boxes).
 // TMA requires a 16-byte-aligned start of the innermost box dimension, so the
 // intensity box starts at x0 - 4 (not x0 - 1) and is 40 floats wide; the
@@ -166,8 +167,9 @@ __device__ __forceinline__ void plane_SR(const float4 *Us, int ty, int tx, float
 //   of its voxels: g (Eq. 6) for two voxels per FADD2, one FFMA2 per cluster
 //   pair for the numerator.  Eq. 7: the separable in-plane sums S, R of the
 //   newest plane (plane_SR), carried across the z march.
-//   Planes arrive by TMA into a 4-stage ring (full barriers); each warp
-//   releases a stage on its empty barrier, so warps are not lock-stepped.
+//   Planes arrive by TMA into a kRing-stage ring (one full mbarrier per
+//   stage); each warp counts its release of a stage in shared memory and the
+//   last warp to release it refills it, so warps are not lock-stepped.
 template <int C, bool M2, bool DU, bool HF>
 __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     k_step_stencil(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX,
@@ -927,7 +929,7 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
     }
     if (stencil && a.nz == 1 && a.nz_g == 1 && !a.hf && a.v == 1)  // plain 2D image: k_step_2d's blocks
         a.nblk = step_nblk(a.nx, a.ny, 1, true, P);
-    if (stencil && a.v == 2) return launch_step_v2(a, C, P, st);
+    if (stencil && a.v >= 2) return launch_step_shells(a, C, P, st);
     const bool m2 = (a.m == 2.0f) || a.hf != nullptr;  // the H, F pass does not depend on m
     switch (C) {
         case 2: return m2 ? launch_t<2, true>(a, stencil, P, st) : launch_t<2, false>(a, stencil, P, st);

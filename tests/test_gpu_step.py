@@ -119,18 +119,28 @@ CASES_V2 = [
 ]
 
 
-@pytest.mark.parametrize("shape,C,m,q_mode,h", CASES_V2)
-def test_step_parity_v2(ctx, orc, shape, C, m, q_mode, h):
-    """v = 2: every membership within 1e-4, centres 1e-4 relative, J 1e-4."""
+CASES_V3 = [
+    # (nz, ny, nx), C, m, q_mode, h -- three Chebyshev shells (342 neighbours)
+    ((1, 11, 12), 2, 2.0, 0, 1.0),      # 2D
+    ((9, 21, 37), 4, 2.0, 0, 1.0),      # ragged tiles, boundary shells everywhere
+    ((14, 40, 70), 3, 2.0, 1, 0.7),     # several tiles, interior voxels
+    ((3, 3, 3), 4, 1.5, 0, 2.0),        # every voxel sees the whole volume
+]
+
+
+@pytest.mark.parametrize("v,shape,C,m,q_mode,h", [(2,) + c for c in CASES_V2] + [(3,) + c for c in CASES_V3])
+def test_step_parity_v2(ctx, orc, v, shape, C, m, q_mode, h):
+    """v = 2, 3 (Eq. 9-10): every membership within 1e-4, centres
+    1e-4 relative, J 1e-4."""
     nz, ny, nx = shape
     states = [random_state(nx, ny, nz, C, seed=300 + s, crisp_frac=0.1) for s in range(3)]
     x = states[0][0]
     Us = [s[1] for s in states]
     cs = [s[2] for s in states]
     lamxi = [(0.3, 0.6), (1.0, 1.0), (0.05, 0.95)]
-    U, c, st = gpu_step(ctx, x, Us, cs, lamxi, C, m=m, q_mode=q_mode, v=2, h=h)
+    U, c, st = gpu_step(ctx, x, Us, cs, lamxi, C, m=m, q_mode=q_mode, v=v, h=h)
     for p in range(3):
-        Uo, co, Jo, duo = orc.ifcm_step(x, Us[p], cs[p], *lamxi[p], m=m, q_mode=q_mode, v=2, h=h)
+        Uo, co, Jo, duo = orc.ifcm_step(x, Us[p], cs[p], *lamxi[p], m=m, q_mode=q_mode, v=v, h=h)
         err = np.abs(U[p] - Uo).max()
         assert err < U_TOL, (p, err)
         assert np.all(np.abs(c[p] - co) <= C_TOL * np.abs(co) + 1e-7), (c[p], co)

@@ -1,4 +1,4 @@
-"""Device time of the fused step for v = 1 and v = 2 (NEXT-2) on C3, P = 32
+"""Device time of the fused step for v = 1, 2 and 3 (NEXT-2) on C3, P = 32
 (one PSO generation per launch; CUDA events on the launch stream via the
 library's timing; never a bench value).
 
@@ -20,7 +20,7 @@ vol, _ = config_volume("C3")
 nz, ny, nx = vol.shape
 vt = torch.as_tensor(vol, device="cuda:0")
 out = {}
-for v in (1, 2):
+for v in (1, 2, 3):
     cfg = IfcmConfig(C=4, v=v, h=1.0)
     pso = PsoConfig(P=32, max_gen=30, patience=0, seed=12345)
     ws = ctx.workspace(nx, ny, nz, cfg, pso)
@@ -32,12 +32,12 @@ for v in (1, 2):
     for _ in range(2):
         ctx.pso_step(g, cfg, pso, x, ws)
     ctx.timing_enable(True)
-    for _ in range(6):
+    for _ in range(6 if v < 3 else 2):
         ctx.pso_step(g, cfg, pso, x, ws)
     ms, n, b = ctx.timing_read()
     ctx.timing_enable(False)
     out[f"v{v}"] = {"ms_per_launch": ms / n, "G_vp_per_s": 32 * nz * ny * nx / (ms / n * 1e-3) / 1e9,
-                    "neighbours": 26 if v == 1 else 124}
+                    "neighbours": (2 * v + 1) ** 3 - 1}
     del ws
     torch.cuda.empty_cache()
 print(json.dumps(out, indent=1))
