@@ -384,7 +384,10 @@ void orc_histogram_f32(const float *vol, long N, int64_t *hist) {
  * (bin b at level y_b = b/255), evenly spaced initialisation, <= max_iter EM
  * iterations, component means (sorted ascending) -> initial centres.
  * Degenerate fits fall back to evenly spaced centres c_j = j/(C-1).
- * Pin: partial (two-mode histogram -> the modes); otherwise parity unpinned. */
+ * Pins: the two-mode fixed point (-> the modes), a hand-worked one-iteration
+ * case, and every EM iteration against scikit-learn's GaussianMixture from the
+ * same start (tests/test_oracle_pso.py, tests/test_oracle_pins_init.py); the
+ * R15 reading itself (what the paper's undefined step is) stays a reading. */
 void orc_gmm_init(const int64_t *hist, int C, int max_iter, double *c0) {
     double y[256], n[256], Ntot = 0.0;
     int distinct = 0;
