@@ -38,9 +38,12 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None,
+          only=()) -> str:
     """Compile every csrc/*.cu for sm_100a and link libpifcm.so.  `defines` /
-    `out` build tuning variants (e.g. PIFCM_RING=6) under another name."""
+    `out` build tuning variants (e.g. PIFCM_RING=6) under another name; with
+    `only` (source basenames) just those sources take the defines and the
+    other objects come from the default build."""
     lib = out or LIB
     if not force and not defines and out is None and not needs_build():
         return LIB
@@ -52,6 +55,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     # source, any header or this script (headers are not tracked per source)
     hdr_t = max([os.path.getmtime(f) for f in headers()] + [os.path.getmtime(__file__)])
     for src in sources():
+        if only and os.path.basename(src) not in only:
+            objs.append(os.path.join(HERE, "build", os.path.basename(src) + ".o"))
+            continue
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
         if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
@@ -77,5 +83,6 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
 if __name__ == "__main__":
     defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
     outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    only = [s for a in sys.argv[1:] if a.startswith("--only=") for s in a[7:].split(",")]
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
-                out=outs[0] if outs else None))
+                out=outs[0] if outs else None, only=only))
