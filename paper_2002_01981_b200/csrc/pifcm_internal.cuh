@@ -86,7 +86,6 @@ struct StepArgs {
     double *stats_out;   // nullable [P][4] {J, du, iters, converged} (same array as stats)
     float eps;
     int *status;         // nullable: PIFCM_ENUMERIC on a non-finite J
-    const float *gsum;   // [nz][ny][pitch]: Eq. 5 denominator G_i = sum_k g_ik of the target planes (k_gsum)
     float4 *hf;          // non-null: emit H (float4) and F (float4) per voxel [nvox][2] instead of a step
     int v;               // neighbourhood shells (Eq. 9-10): 1 = the 26-neighbourhood, 2 = two shells
     float wsh[kMaxV];    // Eq. 10 shell weights W_1 .. W_v (v >= 2)

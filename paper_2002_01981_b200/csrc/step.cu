@@ -51,9 +51,6 @@ constexpr int kRing = PIFCM_RING;  // planes in flight: z-1, z, z+1 in use, the 
 #ifndef PIFCM_FOLD
 #define PIFCM_FOLD 1  // 3D step: Eq. 5 / Eq. 7 denominators folded into the Eq. 4 weights (+0.6 %)
 #endif
-#ifndef PIFCM_COMPL
-#define PIFCM_COMPL 0  // 3D step: Eq. 5 numerator of the last cluster from G - sum of the others
-#endif
 constexpr int kStencilSmem = kRing * (kUStagePad + kXStagePad) + 128;
 
 // Warp-cooperative fp64 re-evaluation of the Eq. 4 factors of one voxel (the
@@ -261,15 +258,6 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     float2 den2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
     float Jacc = 0.f, duacc = 0.f;
 
-#if PIFCM_COMPL
-    // Eq. 5 denominators G_i of the thread's rows (a.gsum, pitched like x)
-    const float *Grow = a.gsum + (long long)(y0 + ty * kRY) * a.pitch + gx;
-    const long long gplane = (long long)a.ny * a.pitch;
-    float gnext[kRY];
-#pragma unroll
-    for (int r = 0; r < kRY; ++r)
-        gnext[r] = ((vmask >> r) & 1u) ? __ldg(Grow + (long long)zb * gplane + r * a.pitch) : 0.f;
-#endif
     // Eq. 7 carried sums: Pc = R(z-1) + S(z), Rc = R(z)
     float2 Pc[kRY][NP], Rc[kRY][NP];
     wait_plane(zb - 1);
@@ -297,16 +285,6 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
         float xr[kRY];
 #pragma unroll
         for (int r = 0; r < kRY; ++r) xr[r] = Xc[(ty * kRY + 1 + r) * kSXP + tx + kXOff];
-#if PIFCM_COMPL
-        // G_i of plane z (prefetched one plane ahead); fetch plane z+1's
-        float gcur[kRY];
-#pragma unroll
-        for (int r = 0; r < kRY; ++r) {
-            gcur[r] = gnext[r];
-            gnext[r] = (z + 1 < ze && ((vmask >> r) & 1u)) ? __ldg(Grow + (long long)(z + 1) * gplane + r * a.pitch)
-                                                         : 0.f;
-        }
-#endif
 
         // ---- Eq. 5 numerators (and, on the z+1 plane, the Eq. 7 plane sums)
         float2 hn[kRY][NP];
@@ -314,39 +292,6 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
         for (int r = 0; r < kRY; ++r)
 #pragma unroll
             for (int q = 0; q < NP; ++q) hn[r][q] = make_float2(0.f, 0.f);
-#if PIFCM_COMPL
-        // Eq. 5 numerators of clusters 0 and 1 per voxel (one FFMA2 with |g|
-        // broadcast); for C = 4 cluster 2 packed across the voxel pairs
-        // (r, r+1) that share the neighbour (one FFMA2 with u_k2 broadcast and
-        // the |g| pair); the last cluster is G - the others (rows of U sum to 1)
-        float2 h2p[kRY / 2];
-#pragma unroll
-        for (int r = 0; r < kRY / 2; ++r) h2p[r] = make_float2(0.f, 0.f);
-        auto h_row = [&](const int dx, const int dz, const int t, const float4 uk4, const float xk) {
-            const float2 u01 = make_float2(uk4.x, uk4.y);
-#pragma unroll
-            for (int r = 0; r < kRY; r += 2) {
-                const int dy0 = t - 1 - r, dy1 = t - 2 - r;
-                const bool v0 = dy0 >= -1 && dy0 <= 1 && !(dx == 0 && dy0 == 0 && dz == 0);
-                const bool v1 = dy1 >= -1 && dy1 <= 1 && !(dx == 0 && dy1 == 0 && dz == 0);
-                if (v0 && v1) {
-                    const float2 d = __fadd2_rn(make_float2(xr[r], xr[r + 1]), make_float2(-xk, -xk));  // Eq. 6
-                    const float2 ad = make_float2(fabsf(d.x), fabsf(d.y));
-                    hn[r][0] = __ffma2_rn(u01, make_float2(ad.x, ad.x), hn[r][0]);
-                    hn[r + 1][0] = __ffma2_rn(u01, make_float2(ad.y, ad.y), hn[r + 1][0]);
-                    if (C == 4) h2p[r / 2] = __ffma2_rn(make_float2(uk4.z, uk4.z), ad, h2p[r / 2]);
-                } else if (v0 || v1) {
-                    const int rr = v0 ? r : r + 1;
-                    const float g = fabsf(xr[rr] - xk);  // Eq. 6
-                    hn[rr][0] = __ffma2_rn(u01, make_float2(g, g), hn[rr][0]);
-                    if (C == 4) {
-                        if (v0) h2p[r / 2].x = fmaf(uk4.z, g, h2p[r / 2].x);
-                        else h2p[r / 2].y = fmaf(uk4.z, g, h2p[r / 2].y);
-                    }
-                }
-            }
-        };
-#else
         // one loaded neighbour row (column dx, plane dz, haloed row t): g_ik
         // (Eq. 6) for the voxels it touches, two per FADD2, and the Eq. 5
         // numerators, one FFMA2 per cluster pair
@@ -379,7 +324,6 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
                 if (NP > 1) hn[r][NP - 1] = __ffma2_rn(u23, g2, hn[r][NP - 1]);
             }
         };
-#endif
 #pragma unroll
         for (int dz = -1; dz <= 0; ++dz) {
             const float4 *Us = dz < 0 ? Um : Uc;
@@ -450,19 +394,9 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
         unsigned band_bits = 0u;
 #pragma unroll
         for (int r = 0; r < kRY; ++r) {
-#if PIFCM_COMPL
-            const float G = gcur[r];  // Eq. 5 denominator sum_k g_ik (k_gsum)
-            if (C == 4) {
-                const float h2 = (r & 1) ? h2p[r / 2].y : h2p[r / 2].x;
-                hn[r][NP - 1] = make_float2(h2, G - ((hn[r][0].x + hn[r][0].y) + h2));
-            } else if (C == 3) {
-                hn[r][NP - 1] = make_float2(G - (hn[r][0].x + hn[r][0].y), 0.f);
-            }
-#else
             float G = hn[r][0].x + hn[r][0].y;
             if (C > 2) G += hn[r][NP - 1].x;
             if (C > 3) G += hn[r][NP - 1].y;  // = sum_k g_ik (rows of U sum to 1)
-#endif
             const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
             float2 A[2], Ar[2];
             if (HF) {  // particle-invariant H, F of this state (ANCHORED / LEADER fitness)
@@ -818,53 +752,6 @@ __global__ void __launch_bounds__(kPwThreads) k_step_pointwise(const StepArgs a)
 }
 
 // ----------------------------------------------------------------------------
-// Eq. 5 denominator G_i = sum_k g_ik = sum_k |x_i - x_k| (Eq. 5-6)
-// over the in-bounds 26-neighbourhood (Eq. 9, R2) of every target voxel: a
-// function of the intensities alone, formed once per volume instead of once
-// per state (the stencil step then needs the Eq. 5 numerators of C - 1
-// clusters only, the last one being G minus the others because rows of U sum
-// to 1).  Target planes [z_lo, z_lo + nz_t) of an array of nz planes whose
-// plane 0 is global plane goff of a volume of nz_g planes.
-__global__ void __launch_bounds__(256) k_gsum(const float *__restrict__ x, int nx, int ny, int nz, int pitch,
-                                              int z_lo, int goff, int nz_g, float *__restrict__ G) {
-    // one z-plane per blockIdx.y, 32-bit in-plane indices
-    const int Z = z_lo + blockIdx.y;
-    const int n = nx * ny;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int Y = i / nx, X = i - Y * nx;
-        const float xi = x[((long long)Z * ny + Y) * pitch + X];
-        float s = 0.f;
-#pragma unroll
-        for (int dz = -1; dz <= 1; ++dz) {
-            const int zz = Z + dz;
-            if (zz < 0 || zz >= nz || zz + goff < 0 || zz + goff >= nz_g) continue;
-#pragma unroll
-            for (int dy = -1; dy <= 1; ++dy) {
-                const int yy = Y + dy;
-                if (yy < 0 || yy >= ny) continue;
-                const float *row = x + ((long long)zz * ny + yy) * pitch;
-#pragma unroll
-                for (int dx = -1; dx <= 1; ++dx) {
-                    const int xx = X + dx;
-                    if (xx < 0 || xx >= nx || (dx == 0 && dy == 0 && dz == 0)) continue;
-                    s += fabsf(xi - __ldg(row + xx));  // Eq. 6
-                }
-            }
-        }
-        G[((long long)Z * ny + Y) * pitch + X] = s;
-    }
-}
-
-cudaError_t launch_gsum(const float *x, int nx, int ny, int nz, int pitch, int z_lo, int nz_t, int goff, int nz_g,
-                        float *G, cudaStream_t st) {
-    if (nz_t < 1) return cudaSuccess;
-    const int n = nx * ny;
-    const int bx = (n + 255) / 256 < 64 ? (n + 255) / 256 : 64;
-    k_gsum<<<dim3(bx, nz_t), 256, 0, st>>>(x, nx, ny, nz, pitch, z_lo, goff, nz_g, G);
-    return cudaGetLastError();
-}
-
-// ----------------------------------------------------------------------------
 static int pw_blocks(long long nvox) {
     long long b = (nvox + kPwThreads * kPwSpan - 1) / (kPwThreads * kPwSpan);
     if (b > 148 * 16) b = 148 * 16;
@@ -905,6 +792,9 @@ int step_zchunks(int nx, int ny, int nz, int P) {
 // them centres and J -- are the same for any number of slabs.  Chosen like
 // step_zchunks for one state on one GPU (wave fill x halo overhead), subject
 // to at least 8 chunks (up to 8 slabs get work).
+#ifndef PIFCM_HALO_COST
+#define PIFCM_HALO_COST 2.0  // planes of work a chunk's halo and prologue cost (canonical chooser)
+#endif
 int slab_tz(int nx, int ny, int nz) {
     const long long tiles = (long long)((nx + kTX - 1) / kTX) * ((ny + kTY - 1) / kTY);
     const long long slots = 148LL * kStepMinBlocks;
@@ -918,7 +808,7 @@ int slab_tz(int nx, int ny, int nz) {
         if (zz < zmin) continue;
         const long long ctas = tiles * zz;
         const long long waves = (ctas + slots - 1) / slots;
-        const double eff = (double)ctas / (double)(waves * slots) * (double)tz / (double)(tz + 2);
+        const double eff = (double)ctas / (double)(waves * slots) * (double)tz / ((double)tz + PIFCM_HALO_COST);
         if (eff > best_eff + 1e-9) {
             best_eff = eff;
             best = tz;
@@ -1044,31 +934,6 @@ cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStre
     if (stencil && a.nz == 1 && a.nz_g == 1 && !a.hf && a.v == 1)  // plain 2D image: k_step_2d's blocks
         a.nblk = step_nblk(a.nx, a.ny, 1, true, P);
     if (stencil && a.v >= 2) return launch_step_shells(a, C, P, st);
-#if PIFCM_COMPL
-    if (stencil && !(a.nz == 1 && a.nz_g == 1 && !a.hf) && a.gsum == nullptr) {
-        // EXPERIMENT: G cached per x (to be replaced by the workspace)
-        static float *gbuf = nullptr;
-        static size_t gcap = 0;
-        static const float *gx = nullptr;
-        static int gkey[8] = {0};
-        const size_t need = sizeof(float) * (size_t)a.pitch * a.ny * a.nz;
-        const int key[8] = {a.nx, a.ny, a.nz, a.pitch, a.z_lo, a.nz_t, a.goff, a.nz_g};
-        bool same = gx == a.x && need <= gcap && P > 1;
-        for (int i = 0; i < 8; ++i) same = same && key[i] == gkey[i];
-        if (!same) {
-            if (need > gcap) {
-                if (gbuf) cudaFree(gbuf);
-                if (cudaMalloc(&gbuf, need) != cudaSuccess) return cudaErrorMemoryAllocation;
-                gcap = need;
-            }
-            cudaError_t e = launch_gsum(a.x, a.nx, a.ny, a.nz, a.pitch, a.z_lo, a.nz_t, a.goff, a.nz_g, gbuf, st);
-            if (e != cudaSuccess) return e;
-            gx = a.x;
-            for (int i = 0; i < 8; ++i) gkey[i] = key[i];
-        }
-        a.gsum = gbuf;
-    }
-#endif
     const bool m2 = (a.m == 2.0f) || a.hf != nullptr;  // the H, F pass does not depend on m
     switch (C) {
         case 2: return m2 ? launch_t<2, true>(a, stencil, P, st) : launch_t<2, false>(a, stencil, P, st);
