@@ -571,7 +571,8 @@ void orc_pso_move(int P, double vmax, const double *p1, const double *p2, const 
  *   step 7: v = v + p1 (x_pbest - x) + p2 (x_lbest - x), p1, p2 in [0,1) from
  *           Philox counter (gen, p, 0, 0); R12: |v| clamped to vmax
  *   step 8: x = clamp(x + v, 0, 1)
- * gbest (lowest index on ties) is returned in *gbest; *improved is 1 when the
+ * gbest (lowest index on ties, except that the incumbent keeps it on an exact
+ * tie, R13) is returned in *gbest; *improved is 1 when the
  * global best fitness strictly decreased this generation.                    */
 void orc_pso_update(int P, int ring_k, uint32_t gen, uint64_t seed, double vmax,
                     const double *f, double *pos, double *vel, double *pbest_f,
@@ -588,6 +589,9 @@ void orc_pso_update(int P, int ring_k, uint32_t gen, uint64_t seed, double vmax,
     int g = 0;
     for (int p = 1; p < P; ++p)
         if (pbest_f[p] < pbest_f[g]) g = p;
+    /* R13: the incumbent gbest keeps the title on an exact tie (its state is
+     * the pinned snapshot; a tied lower index did not improve on it) */
+    if (g_old >= 0 && !(pbest_f[g] < pbest_f[g_old])) g = g_old;
     *gbest = g;
     *improved = (pbest_f[g] < gf_old) ? 1 : 0;
     int *lb = (int *)malloc(sizeof(int) * (size_t)P);

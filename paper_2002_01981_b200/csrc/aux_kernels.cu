@@ -259,6 +259,10 @@ __global__ void __launch_bounds__(kPsoThreads) k_pso_update(const PsoUpdateArgs 
         int g = 0;
         for (int p = 1; p < a.P; ++p)
             if (s.pbf[p] < s.pbf[g]) g = p;
+        // R13: on an exact tie the incumbent keeps the gbest (its state is the
+        // pinned snapshot, so gbest_particle always names the snapshot's owner)
+        const int g_old = s.hdr[kHGbest];
+        if (g_old >= 0 && !(s.pbf[g] < s.pbf[g_old])) g = g_old;
         const double gf_old = s.dhdr[kDGbestJ];
         const int improved = (s.pbf[g] < gf_old) ? 1 : 0;
         s.hdr[kHGbest] = g;

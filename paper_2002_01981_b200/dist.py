@@ -247,9 +247,10 @@ class ShardedSegmenter:
             final_iters = int(sl.stats[0, 2].item())
         else:
             stats.zero_()
-            zero = out.lam == 0.0 and out.xi == 0.0
+            # canonical=True: pifcm_iterate_ex takes the pointwise FCM step at
+            # lambda = xi = 0 itself, exactly as pifcm_segment's final IFCM
             ctx.iterate(x, self.Ua, self.Ub, self.cen, lx, cfg, iters=cfg.max_iter, stats=stats, nx=nx,
-                        canonical=not zero)
+                        canonical=True)
             labels = ctx.argmax(self.Ub[0], nx, ny, nz, cfg.C)
             final_iters = int(stats[0, 2].item())
         ev[4].record()

@@ -70,6 +70,27 @@ def test_pso_update_bit_exact(ctx, orc):
     assert summ.generations == G
 
 
+def test_pso_gbest_tie_keeps_incumbent(ctx, orc):
+    """R13 on the device: an exact fp64 tie with the incumbent gbest leaves
+    the gbest (and so the owner of the pinned snapshot) unchanged; a strictly
+    better pbest takes it (tests/test_oracle_pins_init.py's worked example)."""
+    P, seed = 4, 5
+    x, U0, c0, cfg, pso, xt, Ut, ws, g = _setup_swarm(ctx, orc, P, seed)
+    fit = ctx.pso_fitness(g, cfg, pso, ws)
+    pos, vel = orc.pso_init(P, seed)
+    pbf = np.full(P, np.inf)
+    pbx = pos.copy()
+    gb = -1
+    for t, (f, want) in enumerate((([5.0, 4.0, 2.0, 3.0], 2), ([2.0, 9.0, 9.0, 9.0], 2),
+                                   ([1.0, 9.0, 9.0, 9.0], 0))):
+        fit.copy_(torch.as_tensor(f, dtype=torch.float64, device=fit.device))
+        ctx.pso_update(g, cfg, pso, ws)
+        gb, _ = orc.pso_update(np.array(f), pos, vel, pbf, pbx, gb, t, seed)
+        summ, _ = ctx.pso_result(g, cfg, pso, ws)
+        assert summ.gbest_particle == gb == want
+        assert summ.J == pbf[gb]
+
+
 def test_pso_eval_parity(ctx, orc):
     """Generations 0 and 1 of the CHAINED fitness (one IFCM step per particle
     from its own state) within 1e-5 / 1e-4 of the oracle's."""

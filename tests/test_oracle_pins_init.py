@@ -167,3 +167,26 @@ def test_ring_lbest_k2_wraps(orc):
         orc.pso_update(f, p_, vel, pbf, pos.copy(), -1, gen, seed, ring_k=k, vmax=10.0)
         p1, p2 = orc.philox_pair(seed, gen, 0, 0, 0)
         np.testing.assert_array_equal(vel[0], p2 * (pos[lb0] - pos[0]))
+
+
+def test_gbest_incumbent_keeps_exact_tie(orc):
+    """R13: the gbest is the lowest index among the minimal pbests, but the
+    incumbent keeps it on an exact tie -- its evaluation's state is the
+    pinned snapshot (Alg. 1 step 10) and a tied particle did not
+    improve on it.  Worked example, P = 4:
+        generation 0: f = [5, 4, 2, 3]  -> gbest 2 (strict minimum), improved
+        generation 1: f = [2, 9, 9, 9]  -> particle 0 ties the incumbent's 2:
+                                           gbest stays 2, not improved
+        generation 2: f = [1, 9, 9, 9]  -> particle 0 is strictly better:
+                                           gbest 0, improved"""
+    P, seed = 4, 5
+    pos = np.array([[0.1, 0.1], [0.3, 0.3], [0.5, 0.5], [0.7, 0.7]])
+    vel = np.zeros((P, 2))
+    pbf = np.full(P, np.inf)
+    pbx = pos.copy()
+    g, imp = orc.pso_update(np.array([5.0, 4.0, 2.0, 3.0]), pos, vel, pbf, pbx, -1, 0, seed)
+    assert (g, imp) == (2, 1)
+    g, imp = orc.pso_update(np.array([2.0, 9.0, 9.0, 9.0]), pos, vel, pbf, pbx, g, 1, seed)
+    assert (g, imp) == (2, 0) and pbf[0] == pbf[2] == 2.0
+    g, imp = orc.pso_update(np.array([1.0, 9.0, 9.0, 9.0]), pos, vel, pbf, pbx, g, 2, seed)
+    assert (g, imp) == (0, 1)
