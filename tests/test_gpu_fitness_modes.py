@@ -91,7 +91,12 @@ def test_mode_segment_parity(ctx, orc, mode, G, seed, v):
     r = orc.segment_u8(vol, C=4, P=6, max_gen=G, seed=seed, fitness_mode=mode, v=v)
     assert rep["lambda"] == r.lam and rep["xi"] == r.xi
     if min(r.lam, r.xi) > 0.95:
-        pytest.skip(f"ill-conditioned final IFCM at lambda*={r.lam:.3f}, xi*={r.xi:.3f}")
+        # ill-conditioned final IFCM: same-state parity from the GPU's final
+        # state instead of comparing two chaotic trajectories (tests/illcond.py)
+        from tests.illcond import final_state_step_parity
+        final_state_step_parity(ctx, orc, torch.as_tensor(vol, device="cuda:0"), U, rep["centers"],
+                                rep["lambda"], rep["xi"], cfg)
+        return
     agree = (labels.cpu().numpy() == r.labels).mean()
     assert agree >= 0.999, agree
     # centres after up to 100 final-IFCM iterations from different roundings;
