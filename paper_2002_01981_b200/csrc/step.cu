@@ -48,9 +48,6 @@ constexpr int kStepMinBlocks = PIFCM_STEP_MINBLOCKS;  // CTAs per SM the registe
 #define PIFCM_RING 5
 #endif
 constexpr int kRing = PIFCM_RING;  // planes in flight: z-1, z, z+1 in use, the rest prefetching
-#ifndef PIFCM_FOLD
-#define PIFCM_FOLD 1  // 3D step: Eq. 5 / Eq. 7 denominators folded into the Eq. 4 weights (+0.6 %)
-#endif
 constexpr int kStencilSmem = kRing * (kUStagePad + kXStagePad) + 128;
 
 // Warp-cooperative fp64 re-evaluation of the Eq. 4 factors of one voxel (the
@@ -231,7 +228,6 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     c2[0] = make_float2(a.centers[4 * p + 0], a.centers[4 * p + 1]);
     c2[1] = make_float2(a.centers[4 * p + 2], a.centers[4 * p + 3]);
     const float lam = (float)a.lam_xi[2 * p], xi = (float)a.lam_xi[2 * p + 1];
-    const float2 nlam2 = make_float2(-lam, -lam), nxi2 = make_float2(-xi, -xi);
     const float w2 = a.q_mode == 0 ? 4.0f : 2.0f, w3 = a.q_mode == 0 ? 9.0f : 3.0f;  // Eq. 7 q2 (R1)
     const float2 w22 = make_float2(w2, w2), w32 = make_float2(w3, w3);
     const int gx = x0 + tx;
@@ -392,14 +388,118 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
         }
         float4 *Uo = Urow + (long long)z * plane;  // this row's output (advanced by one image row per r)
         unsigned band_bits = 0u;
+        if (!HF) {
+            // the four rows' Eq. 4 / Eq. 2 without branches, then one warp
+            // vote each for the rare paths (a zero distance, R5; a factor
+            // small enough that the sensitivity K must be formed), then the
+            // per-row partial sums and stores
+            float u[kRY][4], Ji[kRY], S[kRY], Kr[kRY], d2v[kRY][4];
+            float2 Arr[kRY][2];
+            bool need_any = false;
 #pragma unroll
-        for (int r = 0; r < kRY; ++r) {
-            float G = hn[r][0].x + hn[r][0].y;
-            if (C > 2) G += hn[r][NP - 1].x;
-            if (C > 3) G += hn[r][NP - 1].y;  // = sum_k g_ik (rows of U sum to 1)
-            const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
-            float2 A[2], Ar[2];
-            if (HF) {  // particle-invariant H, F of this state (ANCHORED / LEADER fitness)
+            for (int r = 0; r < kRY; ++r) {
+                float G = hn[r][0].x + hn[r][0].y;
+                if (C > 2) G += hn[r][NP - 1].x;
+                if (C > 3) G += hn[r][NP - 1].y;  // = sum_k g_ik (rows of U sum to 1)
+                const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
+                const float sl = -lam * invG, sx = -xi * invQ[r];  // Eq. 5 / 7 denominators folded
+                const float2 x2 = make_float2(xr[r], xr[r]);
+                float w[4] = {0.f, 0.f, 0.f, 0.f};
+                float Sr = 0.f;
+#pragma unroll
+                for (int q = 0; q < NP; ++q) {
+                    Arr[r][q] = __ffma2_rn(hn[r][q], make_float2(sl, sl),
+                                           __ffma2_rn(Fn[r][q], make_float2(sx, sx), make_float2(1.f, 1.f)));  // Eq. 4
+                    const float2 Aq = make_float2(fmaxf(Arr[r][q].x, kAFloor), fmaxf(Arr[r][q].y, kAFloor));  // R4
+                    const float2 d = __fadd2_rn(x2, make_float2(-c2[q].x, -c2[q].y));
+                    const float2 e = __fmul2_rn(__fmul2_rn(d, d), Aq);  // Eq. 4
+                    d2v[r][2 * q] = e.x;
+                    d2v[r][2 * q + 1] = e.y;
+                }
+#pragma unroll
+                for (int j = 0; j < C; ++j) {
+                    w[j] = M2 ? rcp_approx(d2v[r][j]) : exp2f(-log2f(d2v[r][j]) * a.inv_m1);  // d2 = 0 -> +inf
+                    Sr += w[j];
+                }
+                const float invS = rcp_approx(Sr);
+#pragma unroll
+                for (int q = 0; q < NP; ++q) {
+                    const float2 uu = __fmul2_rn(make_float2(w[2 * q], w[2 * q + 1]), make_float2(invS, invS));  // Eq. 2
+                    u[r][2 * q] = uu.x;
+                    u[r][2 * q + 1] = uu.y;
+                }
+                if (NP == 1) { u[r][2] = 0.f; u[r][3] = 0.f; }
+                Ji[r] = M2 ? invS : exp2f((1.0f - a.m) * log2f(Sr));  // Eq. 1 per voxel: S^{1-m}
+                S[r] = Sr;
+                Kr[r] = 0.f;
+                float amin = fminf(fabsf(Arr[r][0].x), fabsf(Arr[r][0].y));
+                if (NP > 1) amin = fminf(amin, fminf(fabsf(Arr[r][NP - 1].x), fabsf(Arr[r][NP - 1].y)));
+                // K <= (1 - 1/C) / min_j |a_j| (x 1/(m-1)): below kKMax the
+                // voxel is not in the band (NaN factors fall through to K)
+                need_any |= !(amin * kKMax >= 0.75f * (M2 ? 1.0f : a.inv_m1));
+            }
+            if (__any_sync(0xffffffffu, need_any)) {
+#pragma unroll
+                for (int r = 0; r < kRY; ++r) {
+                    float Kp[2] = {0.f, 0.f};
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        const float2 uu = make_float2(u[r][2 * q], u[r][2 * q + 1]);
+                        const float2 ia = make_float2(rcp_approx(fabsf(Arr[r][q].x)), rcp_approx(fabsf(Arr[r][q].y)));
+                        const float2 t = __fmul2_rn(__fmul2_rn(uu, __fadd2_rn(make_float2(1.f, 1.f), make_float2(-uu.x, -uu.y))), ia);
+                        Kp[q] = t.x + ((2 * q + 1 < C) ? t.y : 0.f);
+                    }
+                    Kr[r] = M2 ? Kp[0] + Kp[1] : (Kp[0] + Kp[1]) * a.inv_m1;
+                }
+            }
+            bool crisp_any = false;
+#pragma unroll
+            for (int r = 0; r < kRY; ++r) crisp_any |= !(S[r] < INFINITY);
+            if (__any_sync(0xffffffffu, crisp_any)) {  // R5: a zero distance -> crisp row at the lowest such j
+#pragma unroll
+                for (int r = 0; r < kRY; ++r) {
+                    if (S[r] < INFINITY) continue;
+                    int jz = C - 1;
+#pragma unroll
+                    for (int j = C - 1; j >= 0; --j)
+                        if (d2v[r][j] == 0.0f) jz = j;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) u[r][j] = (j == jz) ? 1.0f : 0.0f;
+                    Ji[r] = 0.0f;
+                    Kr[r] = 0.0f;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kRY; ++r) {
+                const bool valid = (vmask >> r) & 1u;
+                const bool band = valid && !(Kr[r] <= kKMax);  // ill-conditioned: fp64 pass below
+                band_bits |= band ? (1u << r) : 0u;
+                const bool ok = valid && !band;
+                const float4 un = make_float4(u[r][0], u[r][1], u[r][2], u[r][3]);
+                if (ok) {
+                    Memb mb;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) mb.u[j] = u[r][j];
+                    mb.Ji = Ji[r];
+                    mb.K = Kr[r];
+                    memb_accumulate<C, M2>(mb, xr[r], a.m, num2, den2, Jacc);
+                    if (DU) {
+                        const float4 uo = Uc[(ty * kRY + 1 + r) * kSX + tx + 1];
+                        duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
+                                                   fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
+                    }
+                    *Uo = un;
+                }
+                Uo += a.nx;
+            }
+        }
+        if (HF) {  // particle-invariant H, F of this state (ANCHORED / LEADER fitness)
+#pragma unroll
+            for (int r = 0; r < kRY; ++r) {
+                float G = hn[r][0].x + hn[r][0].y;
+                if (C > 2) G += hn[r][NP - 1].x;
+                if (C > 3) G += hn[r][NP - 1].y;  // = sum_k g_ik (rows of U sum to 1)
+                const float invG = G > 0.f ? rcp_approx(G) : 0.f;  // R3
                 float2 Hh[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
                 float2 Ff[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
@@ -412,43 +512,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
                     o[0] = make_float4(Hh[0].x, Hh[0].y, Hh[1].x, Hh[1].y);
                     o[1] = make_float4(Ff[0].x, Ff[0].y, Ff[1].x, Ff[1].y);
                 }
-                continue;
             }
-#if PIFCM_FOLD
-            // Eq. 4 with the Eq. 5 / Eq. 7 denominators folded into the
-            // weights: a = 1 + Hn (-lam / G) + Fn (-xi / Qs)
-            const float sl = -lam * invG, sx = -xi * invQ[r];
-#endif
-#pragma unroll
-            for (int q = 0; q < NP; ++q) {
-#if PIFCM_FOLD
-                Ar[q] = __ffma2_rn(hn[r][q], make_float2(sl, sl),
-                                   __ffma2_rn(Fn[r][q], make_float2(sx, sx), make_float2(1.f, 1.f)));
-#else
-                const float2 H = __fmul2_rn(hn[r][q], make_float2(invG, invG));          // Eq. 5
-                const float2 F = __fmul2_rn(Fn[r][q], make_float2(invQ[r], invQ[r]));    // Eq. 7
-                Ar[q] = __ffma2_rn(H, nlam2, __ffma2_rn(F, nxi2, make_float2(1.f, 1.f))); // Eq. 4
-#endif
-                A[q].x = fmaxf(Ar[q].x, kAFloor);                                          // R4
-                A[q].y = fmaxf(Ar[q].y, kAFloor);
-            }
-            if (NP == 1) { A[1] = make_float2(1.f, 1.f); Ar[1] = A[1]; }
-            const Memb mb = memb_compute<C, M2>(xr[r], c2, A, a.m, a.inv_m1, Ar);
-            const bool valid = (vmask >> r) & 1u;
-            const bool band = valid && !(mb.K <= kKMax);  // ill-conditioned: fp64 pass below
-            band_bits |= band ? (1u << r) : 0u;
-            const bool ok = valid && !band;
-            const float4 un = make_float4(mb.u[0], mb.u[1], mb.u[2], mb.u[3]);
-            if (ok) {
-                memb_accumulate<C, M2>(mb, xr[r], a.m, num2, den2, Jacc);
-                if (DU) {
-                    const float4 uo = Uc[(ty * kRY + 1 + r) * kSX + tx + 1];
-                    duacc = fmaxf(duacc, fmaxf(fmaxf(fabsf(un.x - uo.x), fabsf(un.y - uo.y)),
-                                               fmaxf(fabsf(un.z - uo.z), fabsf(un.w - uo.w))));
-                }
-                *Uo = un;
-            }
-            Uo += a.nx;
         }
 
         // Ill-conditioned voxels of this warp, one at a time, all lanes together.
