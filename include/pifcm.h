@@ -91,8 +91,10 @@ typedef struct pifcm_ctx pifcm_ctx;
  * (PAPER:93).  nz == 1 is the 2D case (8-neighbourhood).
  * z-slab mode (nz_total > 0, only for the pifcm_slab_* calls): this process
  * holds the planes [z0, z0 + nz) of a volume of nz_total planes; its x and U
- * arrays then have nz + 2 planes, plane 0 being global z0 - 1 and plane
- * nz + 1 global z0 + nz (halo planes).  With tz = pifcm_slab_chunk(nx, ny,
+ * arrays then have nz + 2v planes for the neighbourhood radius v of the
+ * pifcm_ifcm_cfg (Eq. 9-10), plane 0 being global z0 - v and plane
+ * nz + 2v - 1 global z0 + nz + v - 1 (v halo planes per side; v = 1: nz + 2
+ * planes, halos at 0 and nz + 1).  With tz = pifcm_slab_chunk(nx, ny,
  * nz_total), z0 must be a multiple of tz and every slab but the last must
  * have a multiple of tz planes (the slab reductions use global chunks of tz
  * planes, which makes them independent of the number of slabs).
@@ -419,10 +421,11 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
  * "through each voxel in the slice of a particular z axis image"): segment
  * slice z of a u8 volume with its 3D neighbourhood.  The volume is normalised
  * (Alg. 2 step 1); the R15 histogram of slice z on the volume's levels feeds
- * the GMM; FCM runs on the slice; the rows of planes z - 1, z + 1 (where they
- * exist) are the Eq. 2 memberships at the FCM centres and stay fixed; the
- * CHAINED PSO and the final IFCM update slice z only (Eq. 3 / Eq. 1 over the
- * slice).  v = 1, CHAINED, single process (eval_batch allowed).  Sync.
+ * the GMM; FCM runs on the slice; the rows of planes z - v .. z - 1 and
+ * z + 1 .. z + v (where they exist; v = the cfg's neighbourhood radius) are
+ * the Eq. 2 memberships at the FCM centres and stay fixed; the CHAINED PSO
+ * and the final IFCM update slice z only (Eq. 3 / Eq. 1 over the slice).
+ * v = 1 .. 3, CHAINED, single process (eval_batch allowed).  Sync.
  *   vol     dev u8 [nz][ny][nx];  0 <= z < nz
  *   labels  dev u8 [ny][nx] out;  U_out dev fp32 [ny][nx][4] out, nullable
  *   ws      >= pifcm_segment_slice_workspace_size bytes (dev, 256-B aligned) */
@@ -441,8 +444,8 @@ int pifcm_segment_host(pifcm_ctx *ctx, const uint8_t *vol_host, int32_t nx, int3
 
 /* ------------------------------------------------------------------- z-slab */
 /* The IFCM step of a volume too large for one GPU, partitioned into z-slabs
- * across processes: per iteration the caller exchanges one halo
- * plane per neighbour and per state (pifcm_slab_halo + its own collective),
+ * across processes: per iteration the caller exchanges v halo
+ * planes per neighbour and per state (pifcm_slab_halo_v + its own collective),
  * runs pifcm_slab_step, all-gathers the per-chunk partial records of all
  * ranks in rank order and calls pifcm_slab_finalize, which applies Eq. 3 /
  * Eq. 1 identically on every rank.  Because the records are
@@ -460,8 +463,9 @@ int pifcm_slab_chunk(int32_t nx, int32_t ny, int32_t nz_total, int32_t *tz);
 int pifcm_slab_records(const pifcm_grid *grid, int32_t *nrec);
 
 /* One Jacobi IFCM step over the slab's local planes for P
- * states.  x dev fp32 [nz+2][ny][pitch]; U_in, U_out dev fp32
- * [P][nz+2][ny][nx][4] (halo planes of U_in filled); centers dev fp32 [P][4]
+ * states, any v of cfg (v >= 2: the shell step, Eq. 9-10).  x dev fp32
+ * [nz+2v][ny][pitch]; U_in, U_out dev fp32 [P][nz+2v][ny][nx][4] (halo planes
+ * of U_in filled); centers dev fp32 [P][4]
  * (read only); lam_xi dev fp64 [P][2]; stats dev fp64 [P][4] nullable (states
  * with stats[p][3] != 0 are skipped); records dev fp64 [P][nrec][10] out:
  * per chunk and tile {sum u^m x (4), sum u^m (4), J, max|du|}.  Async. */
@@ -480,12 +484,20 @@ int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int
                         const int32_t *counts, const double *records, float *centers, double *stats,
                         double *fitness, float eps, pifcm_stream stream);
 
-/* Halo planes of P slab states U [P][nz+2][ny][nx][4]:
- *   op 0: pack the first local plane (array plane 1) into buf [P][ny][nx][4]
- *   op 1: pack the last local plane (array plane nz) into buf
- *   op 2: unpack buf into the lower halo (array plane 0); zeros when z0 == 0
- *   op 3: unpack buf into the upper halo (plane nz+1); zeros at the volume end
- * (buf may be NULL for a zero fill).  Async. */
+/* The v halo planes per side of P slab states U [P][nz+2v][ny][nx][4]
+ * (v = the cfg's neighbourhood radius, 1 .. 3):
+ *   op 0: pack the first v local planes (array planes v .. 2v-1) into
+ *         buf [P][v][ny][nx][4]
+ *   op 1: pack the last v local planes (array planes nz .. nz+v-1) into buf
+ *   op 2: unpack buf into the lower halo (array planes 0 .. v-1); zeros when
+ *         z0 == 0
+ *   op 3: unpack buf into the upper halo (planes nz+v .. nz+2v-1); zeros at
+ *         the volume end
+ * (buf may be NULL for a zero fill).  A slab thinner than v planes is only
+ * valid at a volume end (PIFCM_EINVAL otherwise).  Async.
+ * pifcm_slab_halo = pifcm_slab_halo_v with v = 1. */
+int pifcm_slab_halo_v(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t v, int32_t P, int32_t op, float *U,
+                      float *buf, pifcm_stream stream);
 int pifcm_slab_halo(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t P, int32_t op, float *U,
                     float *buf, pifcm_stream stream);
 
@@ -557,7 +569,7 @@ int pifcm_hist_u8(pifcm_ctx *ctx, const uint8_t *vol, int64_t n, const uint32_t 
 /* ------------------------------------------------- PSO over z-slab ranks
  * Alg. 1 steps 3-10 for a volume split into z-slabs (SURVEY
  * 8(e), the 512^3 C5 workload): every rank holds ALL particles' states for
- * its slab (a slot pool like pifcm_pso_*, each slot [nz+2][ny][nx][4] with
+ * its slab (a slot pool like pifcm_pso_*, each slot [nz+2v][ny][nx][4] with
  * the halo planes) and the identical swarm.  Per generation the caller runs
  *   pifcm_slab_pso_halo (pack, op 0/1) -> send/recv -> pifcm_slab_pso_halo
  *   (unpack, op 2/3) -> pifcm_slab_pso_eval (records of every particle) ->
@@ -570,17 +582,17 @@ int pifcm_hist_u8(pifcm_ctx *ctx, const uint8_t *vol, int64_t n, const uint32_t 
  * particles).  The workspace holds the slots, the swarm and scratch. */
 int pifcm_slab_workspace_size(const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
                               size_t *bytes);
-/* U0 dev fp32 [nz+2][ny][nx][4] (the slab's start state, halos included),
+/* U0 dev fp32 [nz+2v][ny][nx][4] (the slab's start state, halos included),
  * c0 dev fp32 [4].  Positions / velocities from Philox (R12).  Async. */
 int pifcm_slab_pso_init(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
                         const float *U0, const float *c0, void *ws, size_t ws_bytes, pifcm_stream stream);
-/* Halo planes of every particle's current state, ops as pifcm_slab_halo with
- * buf [P][ny][nx][4].  Async. */
+/* Halo planes of every particle's current state, ops as pifcm_slab_halo_v
+ * with the cfg's v and buf [P][v][ny][nx][4].  Async. */
 int pifcm_slab_pso_halo(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
                         void *ws, size_t ws_bytes, int32_t op, float *buf, pifcm_stream stream);
 /* One IFCM step of every particle at its own (lambda, xi) on the slab's
  * planes (Alg. 1 step 4, CHAINED R11); records dev fp64 [P][nrec][10] out
- * (nrec = pifcm_slab_records).  x dev fp32 [nz+2][ny][pitch].  Async. */
+ * (nrec = pifcm_slab_records).  x dev fp32 [nz+2v][ny][pitch].  Async. */
 int pifcm_slab_pso_eval(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso,
                         const float *x, void *ws, size_t ws_bytes, double *records, pifcm_stream stream);
 /* Eq. 3 / Eq. 1 of every particle from the gathered records [world][P][nrec][10]
@@ -592,7 +604,7 @@ int pifcm_slab_pso_finalize(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_
 int pifcm_slab_pso_update(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
                           const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, pifcm_stream stream);
 /* As pifcm_pso_result_get / pifcm_pso_gbest_state (U_out: the slab part of
- * the gbest state, [nz+2][ny][nx][4]; every rank holds it).  Sync. */
+ * the gbest state, [nz+2v][ny][nx][4]; every rank holds it).  Sync. */
 int pifcm_slab_pso_result_get(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
                               const pifcm_pso_cfg *pso, void *ws, pifcm_pso_result *out, int32_t *stopped,
                               pifcm_stream stream);

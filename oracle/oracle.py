@@ -96,7 +96,7 @@ def _declare(L):
     L.orc_segment_u8.restype = i
     L.orc_ifcm_step_planes.argtypes = [_dp, i, i, i, i, i, i, d, d, d, i, i, d, _dp, _dp, _dp, _dp, _dp, _dp]
     L.orc_histogram_u8_range.argtypes = [_u8p, l, i, i, _i64p]
-    L.orc_segment_slice_u8.argtypes = [_u8p, i, i, i, i, i, d, i, d, i, i, i, i, i, d, d, d, u64,
+    L.orc_segment_slice_u8.argtypes = [_u8p, i, i, i, i, i, d, i, i, d, d, i, i, i, i, i, d, d, d, u64,
                                        _u8p, _dp, _dp, _dp, _dp, _ip, _ip, _dp, _ip]
     L.orc_segment_slice_u8.restype = i
     L.orc_incs.argtypes = [_u8p, _u8p, l, i, _dp]
@@ -409,9 +409,10 @@ class SliceResult:
 
 
 def segment_slice_u8(vol, z, C, P, max_gen, seed, m=2.0, q_mode=0, eps=1e-5, max_iter=100, ring_k=1,
-                     patience=0, tol=1e-4, v0=0.1, vmax=0.5):
+                     patience=0, tol=1e-4, v0=0.1, vmax=0.5, v=1, h=1.0):
     """The literal slice mode (R25, orc_segment_slice_u8): segment slice z of a
-    u8 volume [nz, ny, nx] with its 3D neighbourhood."""
+    u8 volume [nz, ny, nx] with its 3D neighbourhood of radius v (Eq. 9-10;
+    the neighbour planes z - v .. z + v fixed at the FCM rows)."""
     vol = np.ascontiguousarray(vol, dtype=np.uint8)
     nz, ny, nx = vol.shape
     n = nx * ny
@@ -424,7 +425,8 @@ def segment_slice_u8(vol, z, C, P, max_gen, seed, m=2.0, q_mode=0, eps=1e-5, max
     fi = ct.c_int()
     ci = np.empty(C)
     fc = ct.c_int()
-    r = _L().orc_segment_slice_u8(_p(vol, _u8p), nx, ny, nz, int(z), C, m, q_mode, eps, max_iter, P, ring_k,
+    r = _L().orc_segment_slice_u8(_p(vol, _u8p), nx, ny, nz, int(z), C, m, q_mode, int(v), float(h), eps,
+                                  max_iter, P, ring_k,
                                   max_gen, patience, tol, v0, vmax, seed, _p(lab, _u8p), _p(U), _p(c), _p(lx),
                                   ct.byref(J), ct.byref(gens), ct.byref(fi), _p(ci), ct.byref(fc))
     if r != 0:

@@ -889,7 +889,8 @@ static int segment_core(const double *xin, const int64_t *histin, int nx, int ny
  * orc_segment_u8; the plane-restricted step equals the whole step on the
  * target rows (tests/test_oracle_pso.py); end to end parity unpinned. */
 int orc_segment_slice_u8(const uint8_t *vol, int nx, int ny, int nz, int z, int C, double m, int q_mode,
-                         double eps, int max_iter, int P, int ring_k, int max_gen, int patience, double tol,
+                         int v, double h, double eps, int max_iter, int P, int ring_k, int max_gen, int patience,
+                         double tol,
                          double v0, double vmax, uint64_t seed, uint8_t *labels, double *U_out, double *c_out,
                          double *lam_xi_out, double *J_out, int *gens_out, int *final_iters_out,
                          double *c_init_out, int *fcm_iters_out) {
@@ -907,8 +908,10 @@ int orc_segment_slice_u8(const uint8_t *vol, int nx, int ny, int nz, int z, int 
     double c0[8], c1[8], cb[8], lx[2], Jb = 0.0;
     orc_gmm_init(hist, C, 100, c0);
     if (c_init_out) memcpy(c_init_out, c0, sizeof(double) * C);
-    /* the neighbourhood planes of slice z: sub-volume [zs0, zs1), target t */
-    const int zs0 = z > 0 ? z - 1 : 0, zs1 = z + 2 < nz ? z + 2 : nz, nzs = zs1 - zs0, t = z - zs0;
+    /* the neighbourhood planes of slice z (Eq. 9 radius v in z): sub-volume
+     * [zs0, zs1), target t */
+    const int zs0 = z - v > 0 ? z - v : 0, zs1 = z + v + 1 < nz ? z + v + 1 : nz, nzs = zs1 - zs0,
+              t = z - zs0;
     const double *xs = x + (long)zs0 * pl;
     double *Us = (double *)malloc(sizeof(double) * (size_t)nzs * pl * C);
     double *Ub = (double *)malloc(sizeof(double) * (size_t)nzs * pl * C);
@@ -919,10 +922,10 @@ int orc_segment_slice_u8(const uint8_t *vol, int nx, int ny, int nz, int z, int 
         double cn[8], Jh, duh;
         orc_fcm_step(xs + (long)k * pl, pl, C, m, c1, NULL, Us + (long)k * pl * C, cn, &Jh, &duh);
     }
-    const int gens = pso_core(xs, nx, ny, nzs, t, t + 1, C, m, q_mode, 1, 1.0, Us, c1, P, ring_k, max_gen,
+    const int gens = pso_core(xs, nx, ny, nzs, t, t + 1, C, m, q_mode, v, h, Us, c1, P, ring_k, max_gen,
                               patience, tol, v0, vmax, seed, lx, &Jb, Ub, cb, NULL, NULL, NULL, 0);
     double Jf = 0.0;
-    const int fi = ifcm_run_planes(xs, nx, ny, nzs, t, t + 1, C, m, lx[0], lx[1], q_mode, 1, 1.0, eps,
+    const int fi = ifcm_run_planes(xs, nx, ny, nzs, t, t + 1, C, m, lx[0], lx[1], q_mode, v, h, eps,
                                    max_iter, Ub, cb, &Jf);
     orc_argmax(Ub + (long)t * pl * C, pl, C, labels);
     if (U_out) memcpy(U_out, Ub + (long)t * pl * C, sizeof(double) * (size_t)pl * C);

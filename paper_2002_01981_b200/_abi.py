@@ -158,6 +158,7 @@ SIGNATURES = {
     "pifcm_slab_finalize": (ct.c_int, [_vp, ct.c_int32, ct.c_int32, ct.c_int32, ct.c_int32, _vp, _vp, _vp,
                                        _vp, _vp, ct.c_float, _vp]),
     "pifcm_slab_halo": (ct.c_int, [_vp, _G, ct.c_int32, ct.c_int32, _vp, _vp, _vp]),
+    "pifcm_slab_halo_v": (ct.c_int, [_vp, _G, ct.c_int32, ct.c_int32, ct.c_int32, _vp, _vp, _vp]),
 }
 
 _lib = None

@@ -473,8 +473,10 @@ class Context:
         self._ck(self.lib.pifcm_slab_finalize(self._h, C, P, world, nrec, _ptr(counts), _ptr(records),
                                               _ptr(centers), _ptr(stats), _ptr(fitness), eps, _stream(stream)))
 
-    def slab_halo(self, grid, P, op, U, buf=None, stream=None):
-        self._ck(self.lib.pifcm_slab_halo(self._h, ct.byref(grid), P, op, _ptr(U), _ptr(buf), _stream(stream)))
+    def slab_halo(self, grid, P, op, U, buf=None, stream=None, v=1):
+        """pifcm_slab_halo_v: the v halo planes per side of P slab states."""
+        self._ck(self.lib.pifcm_slab_halo_v(self._h, ct.byref(grid), v, P, op, _ptr(U), _ptr(buf),
+                                            _stream(stream)))
 
     # ------------------------------------------------------- peer memory
     def peer_alloc(self, nbytes: int) -> int:
@@ -574,7 +576,7 @@ class Context:
 
     def slab_pso_fitness(self, grid, cfg, pso, ws) -> torch.Tensor:
         """Fitness vector of the slab swarm (a view into ws)."""
-        pg = _grid(grid.nx, grid.ny, grid.nz + 2, grid.pitch)
+        pg = _grid(grid.nx, grid.ny, grid.nz + 2 * cfg.v, grid.pitch)  # the slab arrays: v halo planes per side
         return self.pso_fitness(pg, cfg, pso, ws)
 
 

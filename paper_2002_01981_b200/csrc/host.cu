@@ -1093,7 +1093,14 @@ int pifcm_segment_host(pifcm_ctx *ctx, const uint8_t *vol_host, int32_t nx, int3
 }
 
 // ============================================================== ABI: z-slab
-static int check_slab(pifcm_ctx *ctx, const pifcm_grid *g) {
+// The slice mode's single-plane slab (R25): its halo planes are the fixed
+// neighbour rows, refilled by pifcm_segment_slice itself.
+static bool slab_is_slice(const pifcm_grid *g) { return g && g->nz == 1; }
+
+// H = halo planes per side of the slab arrays (= cfg->v, the neighbourhood
+// radius in z); slice: the single-plane slab of the slice mode, whose halo
+// planes are the fixed neighbour rows, not a neighbour rank's planes.
+static int check_slab(pifcm_ctx *ctx, const pifcm_grid *g, int H = 1, bool slice = false) {
     if (!g) return fail(ctx, PIFCM_EINVAL, "grid is NULL");
     if (g->nx < 1 || g->ny < 1 || g->nz < 1) return fail(ctx, PIFCM_EINVAL, "grid dims must be >= 1");
     if (g->pitch < g->nx || g->pitch % 4 != 0) return fail(ctx, PIFCM_EALIGN, "pitch must be >= nx and % 4 == 0");
@@ -1106,7 +1113,11 @@ static int check_slab(pifcm_ctx *ctx, const pifcm_grid *g) {
         return fail(ctx, PIFCM_EINVAL, "slab z0 = %d is not a multiple of %d", g->z0, tz);
     if (g->nz > 1 && g->z0 + g->nz != g->nz_total && g->nz % tz != 0)
         return fail(ctx, PIFCM_EINVAL, "a slab other than the last must hold a multiple of %d planes", tz);
-    if ((long long)g->nx * g->ny * (g->nz + 2) >= (1LL << 31)) return fail(ctx, PIFCM_EINVAL, "slab too large");
+    if ((long long)g->nx * g->ny * (g->nz + 2 * H) >= (1LL << 31)) return fail(ctx, PIFCM_EINVAL, "slab too large");
+    // a slab's neighbours take their H halo planes from its own planes only
+    // (a thinner slab is allowed where the other side is outside the volume)
+    if (!slice && g->nz < H && g->z0 > 0 && g->z0 + g->nz < g->nz_total)
+        return fail(ctx, PIFCM_EINVAL, "an interior slab needs >= %d planes for v = %d", H, H);
     return PIFCM_OK;
 }
 
@@ -1130,17 +1141,19 @@ int pifcm_slab_step(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg
                     const double *stats, double *records, pifcm_stream stream) {
     if (!ctx) return PIFCM_EINVAL;
     int r;
-    if ((r = check_slab(ctx, grid)) || (r = check_cfg(ctx, cfg))) return r;
-    if (cfg->v != 1) return fail(ctx, PIFCM_EINVAL, "z-slab ranks carry one halo plane: v = 1 only");
+    if (!cfg) return fail(ctx, PIFCM_EINVAL, "cfg is NULL");
+    if ((r = check_cfg(ctx, cfg)) || (r = check_slab(ctx, grid, cfg->v, slab_is_slice(grid)))) return r;
+    const int H = cfg->v;  // halo planes per side (Eq. 9 radius in z)
     if (P < 1 || P > 65535) return fail(ctx, PIFCM_EINVAL, "P = %d outside [1, 65535]", P);
     if (!x || !U_in || !U_out || !centers || !lam_xi || !records)
         return fail(ctx, PIFCM_EINVAL, "x, U_in, U_out, centers, lam_xi and records must be non-NULL");
     if (U_in == U_out) return fail(ctx, PIFCM_EINVAL, "U_in and U_out must not alias");
     StepArgs a{};
     a.x = x;
-    a.nx = grid->nx; a.ny = grid->ny; a.nz = grid->nz + 2; a.pitch = grid->pitch;
-    a.nvox = (long long)grid->nx * grid->ny * (grid->nz + 2);
-    a.z_lo = 1; a.nz_t = grid->nz; a.goff = grid->z0 - 1; a.nz_g = grid->nz_total;
+    a.nx = grid->nx; a.ny = grid->ny; a.nz = grid->nz + 2 * H; a.pitch = grid->pitch;
+    a.nvox = (long long)grid->nx * grid->ny * (grid->nz + 2 * H);
+    a.z_lo = H; a.nz_t = grid->nz; a.goff = grid->z0 - H; a.nz_g = grid->nz_total;
+    set_shells(a, cfg);
     a.U_in = reinterpret_cast<const float4 *>(U_in); a.U_out = reinterpret_cast<float4 *>(U_out);
     a.centers = const_cast<float *>(centers); a.lam_xi = lam_xi; a.partials = records;
     a.stats = stats;
@@ -1164,27 +1177,34 @@ int pifcm_slab_finalize(pifcm_ctx *ctx, int32_t C, int32_t P, int32_t world, int
     return PIFCM_OK;
 }
 
-int pifcm_slab_halo(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t P, int32_t op, float *U, float *buf,
-                    pifcm_stream stream) {
+int pifcm_slab_halo_v(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t v, int32_t P, int32_t op, float *U,
+                      float *buf, pifcm_stream stream) {
     if (!ctx) return PIFCM_EINVAL;
     int r;
-    if ((r = check_slab(ctx, grid))) return r;
+    if (v < 1 || v > kMaxV) return fail(ctx, PIFCM_EINVAL, "v = %d outside [1, %d]", v, kMaxV);
+    if ((r = check_slab(ctx, grid, v))) return r;
     if (P < 1 || op < 0 || op > 3 || !U) return fail(ctx, PIFCM_EINVAL, "invalid halo arguments");
+    const int H = v;
     const long long plane = (long long)grid->nx * grid->ny;
-    const long long state = plane * (grid->nz + 2);
+    const long long state = plane * (grid->nz + 2 * H);
     float4 *U4 = reinterpret_cast<float4 *>(U), *B4 = reinterpret_cast<float4 *>(buf);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    if (op <= 1) {
+    if (op <= 1) {  // the first / last H local planes -> buf [P][H planes]
         if (!buf) return fail(ctx, PIFCM_EINVAL, "pack needs a buffer");
-        const long long src_plane = op == 0 ? 1 : grid->nz;
-        LAUNCH(ctx, 1, launch_halo_copy(U4 + src_plane * plane, state, B4, plane, plane, P, false, st));
-    } else {
-        const long long dst_plane = op == 2 ? 0 : grid->nz + 1;
+        const long long src_plane = op == 0 ? H : grid->nz;
+        LAUNCH(ctx, 1, launch_halo_copy(U4 + src_plane * plane, state, B4, H * plane, H * plane, P, false, st));
+    } else {  // buf -> the lower / upper H halo planes (zeros outside the volume)
+        const long long dst_plane = op == 2 ? 0 : grid->nz + H;
         const bool outside = op == 2 ? grid->z0 == 0 : grid->z0 + grid->nz == grid->nz_total;
         if (!outside && !buf) return fail(ctx, PIFCM_EINVAL, "unpack of an interior halo needs a buffer");
-        LAUNCH(ctx, 1, launch_halo_copy(B4, plane, U4 + dst_plane * plane, state, plane, P, outside, st));
+        LAUNCH(ctx, 1, launch_halo_copy(B4, H * plane, U4 + dst_plane * plane, state, H * plane, P, outside, st));
     }
     return PIFCM_OK;
+}
+
+int pifcm_slab_halo(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t P, int32_t op, float *U, float *buf,
+                    pifcm_stream stream) {
+    return pifcm_slab_halo_v(ctx, grid, 1, P, op, U, buf, stream);
 }
 
 
@@ -1221,17 +1241,21 @@ int pifcm_hist_u8(pifcm_ctx *ctx, const uint8_t *vol, int64_t n, const uint32_t 
 // ============================================================== ABI: PSO over z-slabs
 // The swarm of a slab rank lives in a pifcm workspace laid out for the slab's
 // arrays (nz + 2 planes with the halos); every rank holds all particles.
-static pifcm_grid plain_of(const pifcm_grid *s) { return pifcm_grid{s->nx, s->ny, s->nz + 2, s->pitch, 0, 0}; }
+static pifcm_grid plain_of(const pifcm_grid *s, int H) {
+    return pifcm_grid{s->nx, s->ny, s->nz + 2 * H, s->pitch, 0, 0};
+}
 
 static int slab_pso_common(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_cfg *cfg,
                            const pifcm_pso_cfg *pso, void *ws, size_t ws_bytes, Layout *L, pifcm_grid *pg) {
     int r;
-    if ((r = check_slab(ctx, slab)) || (r = check_cfg(ctx, cfg)) || (r = check_pso(ctx, pso))) return r;
-    if (cfg->v != 1) return fail(ctx, PIFCM_EINVAL, "z-slab ranks carry one halo plane: v = 1 only");
+    if (!cfg) return fail(ctx, PIFCM_EINVAL, "cfg is NULL");
+    if ((r = check_cfg(ctx, cfg)) || (r = check_slab(ctx, slab, cfg->v, slab_is_slice(slab))) ||
+        (r = check_pso(ctx, pso)))
+        return r;
     if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
         return fail(ctx, PIFCM_EINVAL, "slab ranks hold every particle (p_begin = p_end = 0)");
     if (pso->fitness_mode != PIFCM_FIT_CHAINED) return fail(ctx, PIFCM_EINVAL, "slab PSO: CHAINED fitness only");
-    *pg = plain_of(slab);
+    *pg = plain_of(slab, cfg->v);
     *L = layout(pg, cfg, pso);
     if (ctx) CK(ctx, cudaSetDevice(ctx->device));
     return ws ? check_ws(ctx, ws, ws_bytes, L->total) : PIFCM_OK;
@@ -1266,20 +1290,21 @@ int pifcm_slab_pso_halo(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm
     int r = slab_pso_common(ctx, slab, cfg, pso, ws, ws_bytes, &L, &pg);
     if (r) return r;
     if (op < 0 || op > 3) return fail(ctx, PIFCM_EINVAL, "halo op %d outside [0, 3]", op);
-    const long long plane = (long long)slab->nx * slab->ny;
+    const int H = cfg->v;
+    const long long plane = (long long)slab->nx * slab->ny, hp = H * plane;
     SwarmDev s = swarm_of(ws, L);
     float4 *slots = at<float4>(ws, L.slots), *B4 = reinterpret_cast<float4 *>(buf);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     if (op <= 1) {
         if (!buf) return fail(ctx, PIFCM_EINVAL, "pack needs a buffer");
-        const long long src_plane = op == 0 ? 1 : slab->nz;
-        LAUNCH(ctx, 1, launch_halo_copy(slots + src_plane * plane, L.nvox, B4, plane, plane, L.Pl, false, st, s.cur,
+        const long long src_plane = op == 0 ? H : slab->nz;
+        LAUNCH(ctx, 1, launch_halo_copy(slots + src_plane * plane, L.nvox, B4, hp, hp, L.Pl, false, st, s.cur,
                                         nullptr));
     } else {
-        const long long dst_plane = op == 2 ? 0 : slab->nz + 1;
+        const long long dst_plane = op == 2 ? 0 : slab->nz + H;
         const bool outside = op == 2 ? slab->z0 == 0 : slab->z0 + slab->nz == slab->nz_total;
         if (!outside && !buf) return fail(ctx, PIFCM_EINVAL, "unpack of an interior halo needs a buffer");
-        LAUNCH(ctx, 1, launch_halo_copy(B4, plane, slots + dst_plane * plane, L.nvox, plane, L.Pl, outside, st,
+        LAUNCH(ctx, 1, launch_halo_copy(B4, hp, slots + dst_plane * plane, L.nvox, hp, L.Pl, outside, st,
                                         nullptr, s.cur));
     }
     return PIFCM_OK;
@@ -1297,9 +1322,11 @@ int pifcm_slab_pso_eval(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm
     float4 *slots = at<float4>(ws, L.slots);
     StepArgs a{};
     a.x = x;
-    a.nx = slab->nx; a.ny = slab->ny; a.nz = slab->nz + 2; a.pitch = slab->pitch;
+    const int H = cfg->v;
+    a.nx = slab->nx; a.ny = slab->ny; a.nz = slab->nz + 2 * H; a.pitch = slab->pitch;
     a.nvox = L.nvox;
-    a.z_lo = 1; a.nz_t = slab->nz; a.goff = slab->z0 - 1; a.nz_g = slab->nz_total;
+    a.z_lo = H; a.nz_t = slab->nz; a.goff = slab->z0 - H; a.nz_g = slab->nz_total;
+    set_shells(a, cfg);
     a.U_in = slots; a.U_out = slots;
     a.stop = s.hdr + kHStop;
     a.m = cfg->m; a.inv_m1 = 1.0f / (cfg->m - 1.0f); a.q_mode = cfg->q_mode;
@@ -1411,7 +1438,9 @@ int pifcm_slab_p2p_run(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_
                        uint32_t *epoch, int32_t *cur, int32_t *iters_done, pifcm_stream stream) {
     if (!ctx) return PIFCM_EINVAL;
     int r;
-    if ((r = check_slab(ctx, slab)) || (r = check_cfg(ctx, cfg))) return r;
+    if (!cfg) return fail(ctx, PIFCM_EINVAL, "cfg is NULL");
+    if ((r = check_cfg(ctx, cfg)) || (r = check_slab(ctx, slab, cfg->v))) return r;
+    const int H = cfg->v;
     if (!peers || !x || !centers || !lam_xi || !stats || !rec_local || !epoch || !cur || !iters_done)
         return fail(ctx, PIFCM_EINVAL, "NULL argument");
     const int world = peers->world, rank = peers->rank;
@@ -1431,16 +1460,17 @@ int pifcm_slab_p2p_run(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_
         P2PPut a{};
         a.src = reinterpret_cast<const float4 *>(peers->U[buf][rank]);
         a.plane = plane;
-        a.state = plane * (slab->nz + 2);
+        a.H = H;
+        a.state = plane * (slab->nz + 2 * H);
         a.nz = slab->nz;
         a.P = P;
-        if (rank > 0) {
-            a.lo_dst = reinterpret_cast<float4 *>(peers->U[buf][rank - 1]) + (long long)(peers->nz[rank - 1] + 1) * plane;
-            a.lo_state = plane * (peers->nz[rank - 1] + 2);
+        if (rank > 0) {  // our first H planes -> rank-1's upper halo
+            a.lo_dst = reinterpret_cast<float4 *>(peers->U[buf][rank - 1]) + (long long)(peers->nz[rank - 1] + H) * plane;
+            a.lo_state = plane * (peers->nz[rank - 1] + 2 * H);
         }
-        if (rank < world - 1) {
+        if (rank < world - 1) {  // our last H planes -> rank+1's lower halo
             a.hi_dst = reinterpret_cast<float4 *>(peers->U[buf][rank + 1]);
-            a.hi_state = plane * (peers->nz[rank + 1] + 2);
+            a.hi_state = plane * (peers->nz[rank + 1] + 2 * H);
         }
         a.rec_src = records ? rec_local : nullptr;
         a.nrec = nrec; a.nrec_max = nrec_max; a.world = world; a.rank = rank;
@@ -1488,11 +1518,12 @@ int pifcm_slab_p2p_run(pifcm_ctx *ctx, const pifcm_grid *slab, const pifcm_ifcm_
 
 // ============================================================== ABI: slice mode
 // The literal slice mode (R25; Alg. 1 with its input z):
-// slice z is segmented with its 3D neighbourhood; the neighbour planes z - 1,
-// z + 1 carry the FCM start's memberships at its centres c1, fixed.  The slice
-// is a single-plane slab (pifcm_slab_* calls, nz = 1, z0 = z): its state slots
-// hold the two halo planes, refilled with the fixed rows before every
-// evaluation; the final IFCM iterates the slab step + finalisation.
+// slice z is segmented with its 3D neighbourhood; the neighbour planes
+// z - v .. z - 1, z + 1 .. z + v (Eq. 9 radius v in z) carry the FCM start's
+// memberships at its centres c1, fixed.  The slice is a single-plane slab
+// (pifcm_slab_* calls, nz = 1, z0 = z): its state slots hold the 2v halo
+// planes, refilled with the fixed rows before every evaluation; the final
+// IFCM iterates the slab step + finalisation.
 namespace {
 struct SliceLayout {
     Layout L;           // the slab PSO workspace (offset 0)
@@ -1502,18 +1533,19 @@ struct SliceLayout {
 };
 SliceLayout slice_layout(const pifcm_grid *sg, const pifcm_ifcm_cfg *cfg, const pifcm_pso_cfg *pso) {
     SliceLayout S{};
-    const pifcm_grid pg{sg->nx, sg->ny, 3, sg->pitch, 0, 0};
+    const int H = cfg->v;  // neighbour planes per side (Eq. 9 radius in z)
+    const pifcm_grid pg{sg->nx, sg->ny, 1 + 2 * H, sg->pitch, 0, 0};
     S.L = layout(&pg, cfg, pso);
     S.plane = (long long)sg->nx * sg->ny;
     const int tz = slab_tz(sg->nx, sg->ny, sg->nz_total);
     S.nrec = ((sg->nx + kTX - 1) / kTX) * ((sg->ny + kTY - 1) / kTY) * ((1 + tz - 1) / tz);
     size_t o = S.L.total;
     auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes, 256); return r; };
-    S.xs = take(sizeof(float) * 3 * (size_t)sg->ny * sg->pitch);
-    S.hlo = take(sizeof(float4) * (size_t)S.plane);
-    S.hhi = take(sizeof(float4) * (size_t)S.plane);
-    S.A = take(sizeof(float4) * 3 * (size_t)S.plane);
-    S.B = take(sizeof(float4) * 3 * (size_t)S.plane);
+    S.xs = take(sizeof(float) * (1 + 2 * H) * (size_t)sg->ny * sg->pitch);
+    S.hlo = take(sizeof(float4) * H * (size_t)S.plane);
+    S.hhi = take(sizeof(float4) * H * (size_t)S.plane);
+    S.A = take(sizeof(float4) * (1 + 2 * H) * (size_t)S.plane);
+    S.B = take(sizeof(float4) * (1 + 2 * H) * (size_t)S.plane);
     S.rec = take(sizeof(double) * kNR * (size_t)S.nrec * (pso->P > 1 ? pso->P : 1));
     S.mm = take(sizeof(unsigned) * 2);
     S.hist = take(sizeof(int64_t) * 256);
@@ -1537,7 +1569,6 @@ int slice_check(pifcm_ctx *ctx, int32_t nx, int32_t ny, int32_t nz, int32_t z, c
     *sg = pifcm_grid{nx, ny, 1, (nx + 3) / 4 * 4, z, nz};
     int r;
     if ((r = check_slab(ctx, sg)) || (r = check_cfg(ctx, cfg)) || (r = check_pso(ctx, pso))) return r;
-    if (cfg->v != 1) return fail(ctx, PIFCM_EINVAL, "slice mode: v = 1 (one neighbour plane per side)");
     if (pso->fitness_mode != PIFCM_FIT_CHAINED) return fail(ctx, PIFCM_EINVAL, "slice mode: CHAINED fitness");
     if (!(pso->p_begin == 0 && pso->p_end == 0) && (pso->p_begin != 0 || pso->p_end != pso->P))
         return fail(ctx, PIFCM_EINVAL, "slice mode is single-process");
@@ -1575,13 +1606,14 @@ int pifcm_segment_slice(pifcm_ctx *ctx, const uint8_t *vol, int32_t nx, int32_t 
            *B = at<float4>(ws, S.B);
     unsigned *mm = at<unsigned>(ws, S.mm);
     int *status = at<int>(ws, S.status);
-    const bool lo_in = z > 0, hi_in = z + 1 < nz;
+    const int H = cfg->v;  // neighbour planes per side
+    const long long hp = H * plane;
     CK(ctx, cudaEventRecord(ev[0], st));
     CK(ctx, cudaMemsetAsync(status, 0, sizeof(int) * 4, st));
-    // Alg. 2 step 1: the volume's range; x of planes z - 1, z, z + 1 (0 outside)
+    // Alg. 2 step 1: the volume's range; x of planes z - H .. z + H (0 outside)
     LAUNCH(ctx, 2, launch_minmax(vol, PIFCM_U8, N, mm, st));
-    for (int k = 0; k < 3; ++k) {
-        const int gz = z - 1 + k;
+    for (int k = 0; k < 1 + 2 * H; ++k) {
+        const int gz = z - H + k;
         float *xk = xs + (size_t)k * ny * pitch;
         if (gz < 0 || gz >= nz)
             CK(ctx, cudaMemsetAsync(xk, 0, sizeof(float) * (size_t)ny * pitch, st));
@@ -1607,16 +1639,18 @@ int pifcm_segment_slice(pifcm_ctx *ctx, const uint8_t *vol, int32_t nx, int32_t 
     LAUNCH(ctx, 1, launch_fcm_hist(fa, cfg->C, cfg->m == 2.0f, st));
     // the start state: slice rows from the FCM's last iteration, the fixed
     // neighbour rows = Eq. 2 at c1 (zero outside the volume)
-    LAUNCH(ctx, 1, launch_fcm_memberships(xs + (size_t)ny * pitch, nx, ny, 1, pitch, cprev, cfg->C, cfg->m,
-                                          A + plane, st));
-    if (lo_in) LAUNCH(ctx, 1, launch_fcm_memberships(xs, nx, ny, 1, pitch, c1, cfg->C, cfg->m, hlo, st));
-    else CK(ctx, cudaMemsetAsync(hlo, 0, sizeof(float4) * plane, st));
-    if (hi_in)
-        LAUNCH(ctx, 1, launch_fcm_memberships(xs + 2 * (size_t)ny * pitch, nx, ny, 1, pitch, c1, cfg->C, cfg->m,
-                                              hhi, st));
-    else CK(ctx, cudaMemsetAsync(hhi, 0, sizeof(float4) * plane, st));
-    CK(ctx, cudaMemcpyAsync(A, hlo, sizeof(float4) * plane, cudaMemcpyDeviceToDevice, st));
-    CK(ctx, cudaMemcpyAsync(A + 2 * plane, hhi, sizeof(float4) * plane, cudaMemcpyDeviceToDevice, st));
+    LAUNCH(ctx, 1, launch_fcm_memberships(xs + (size_t)H * ny * pitch, nx, ny, 1, pitch, cprev, cfg->C, cfg->m,
+                                          A + hp, st));
+    for (int k = 0; k < 1 + 2 * H; ++k) {
+        if (k == H) continue;
+        const int gz = z - H + k;
+        float4 *dst = k < H ? hlo + (long long)k * plane : hhi + (long long)(k - H - 1) * plane;
+        if (gz < 0 || gz >= nz) CK(ctx, cudaMemsetAsync(dst, 0, sizeof(float4) * plane, st));
+        else LAUNCH(ctx, 1, launch_fcm_memberships(xs + (size_t)k * ny * pitch, nx, ny, 1, pitch, c1, cfg->C,
+                                                   cfg->m, dst, st));
+    }
+    CK(ctx, cudaMemcpyAsync(A, hlo, sizeof(float4) * hp, cudaMemcpyDeviceToDevice, st));
+    CK(ctx, cudaMemcpyAsync(A + hp + plane, hhi, sizeof(float4) * hp, cudaMemcpyDeviceToDevice, st));
     CK(ctx, cudaEventRecord(ev[2], st));
     // Alg. 1 steps 3-10: CHAINED PSO over the slice
     const Layout &L = S.L;
@@ -1627,8 +1661,8 @@ int pifcm_segment_slice(pifcm_ctx *ctx, const uint8_t *vol, int32_t nx, int32_t 
     float4 *slots = at<float4>(ws, L.slots);
     for (int gen = 0; gen < pso->max_gen; ++gen) {
         // the neighbour planes of every current state (new states carry stale halos)
-        LAUNCH(ctx, 1, launch_halo_copy(hlo, 0, slots, L.nvox, plane, L.Pl, false, st, nullptr, s.cur));
-        LAUNCH(ctx, 1, launch_halo_copy(hhi, 0, slots + 2 * plane, L.nvox, plane, L.Pl, false, st, nullptr, s.cur));
+        LAUNCH(ctx, 1, launch_halo_copy(hlo, 0, slots, L.nvox, hp, L.Pl, false, st, nullptr, s.cur));
+        LAUNCH(ctx, 1, launch_halo_copy(hhi, 0, slots + hp + plane, L.nvox, hp, L.Pl, false, st, nullptr, s.cur));
         if ((r = pifcm_slab_pso_eval(ctx, &sg, cfg, pso, xs, ws, L.total, rec, stream))) return r;
         if ((r = pifcm_slab_pso_finalize(ctx, &sg, cfg, pso, ws, L.total, 1, S.nrec, nullptr, rec, stream)))
             return r;
@@ -1647,8 +1681,8 @@ int pifcm_segment_slice(pifcm_ctx *ctx, const uint8_t *vol, int32_t nx, int32_t 
     if ((r = pifcm_slab_pso_gbest_state(ctx, &sg, cfg, pso, ws, reinterpret_cast<float *>(A), cent, stream)))
         return r;
     for (float4 *T : {A, B}) {
-        CK(ctx, cudaMemcpyAsync(T, hlo, sizeof(float4) * plane, cudaMemcpyDeviceToDevice, st));
-        CK(ctx, cudaMemcpyAsync(T + 2 * plane, hhi, sizeof(float4) * plane, cudaMemcpyDeviceToDevice, st));
+        CK(ctx, cudaMemcpyAsync(T, hlo, sizeof(float4) * hp, cudaMemcpyDeviceToDevice, st));
+        CK(ctx, cudaMemcpyAsync(T + hp + plane, hhi, sizeof(float4) * hp, cudaMemcpyDeviceToDevice, st));
     }
     double *lamxi = at<double>(ws, S.lamxi), *stats = at<double>(ws, S.stats);
     LAUNCH(ctx, 1, launch_set_lamxi(lamxi, s.dhdr, st));
@@ -1671,9 +1705,9 @@ int pifcm_segment_slice(pifcm_ctx *ctx, const uint8_t *vol, int32_t nx, int32_t 
     }
     const float4 *Ufin = (fin_iters % 2 == 1) ? B : A;
     CK(ctx, cudaEventRecord(ev[4], st));
-    LAUNCH(ctx, 1, launch_argmax(Ufin + plane, plane, cfg->C, labels, st));
+    LAUNCH(ctx, 1, launch_argmax(Ufin + hp, plane, cfg->C, labels, st));
     if (U_out)
-        CK(ctx, cudaMemcpyAsync(U_out, Ufin + plane, sizeof(float4) * (size_t)plane, cudaMemcpyDeviceToDevice, st));
+        CK(ctx, cudaMemcpyAsync(U_out, Ufin + hp, sizeof(float4) * (size_t)plane, cudaMemcpyDeviceToDevice, st));
     CK(ctx, cudaEventRecord(ev[5], st));
     float cfin[4];
     int stat = 0;

@@ -28,19 +28,20 @@ __device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
 __global__ void k_p2p_put(P2PPut a) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nth = (long long)gridDim.x * blockDim.x;
-    // boundary planes -> the neighbours' halo planes (P states each)
+    // the H boundary planes -> the neighbours' H halo planes (P states each)
+    const long long hp = (long long)a.H * a.plane;
     if (a.lo_dst) {
-        const long long n = a.plane * a.P;
+        const long long n = hp * a.P;
         for (long long i = tid; i < n; i += nth) {
-            const long long p = i / a.plane, k = i - p * a.plane;
-            a.lo_dst[p * a.lo_state + k] = a.src[p * a.state + 1 * a.plane + k];             // first local plane
+            const long long p = i / hp, k = i - p * hp;
+            a.lo_dst[p * a.lo_state + k] = a.src[p * a.state + hp + k];                        // first H local planes
         }
     }
     if (a.hi_dst) {
-        const long long n = a.plane * a.P;
+        const long long n = hp * a.P;
         for (long long i = tid; i < n; i += nth) {
-            const long long p = i / a.plane, k = i - p * a.plane;
-            a.hi_dst[p * a.hi_state + k] = a.src[p * a.state + (long long)a.nz * a.plane + k];  // last local plane
+            const long long p = i / hp, k = i - p * hp;
+            a.hi_dst[p * a.hi_state + k] = a.src[p * a.state + (long long)a.nz * a.plane + k];  // last H local planes
         }
     }
     // this rank's records -> slot [rank] of every rank's gathered buffer

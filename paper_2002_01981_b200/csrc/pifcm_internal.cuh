@@ -132,10 +132,10 @@ constexpr int kMaxPeers = 16;
 struct P2PPut {
     const float4 *src;           // this rank's new states [P][nz+2][ny][nx]
     long long plane, state;      // voxels per plane, per state (incl. halos)
-    int nz, P;
-    float4 *lo_dst;              // rank-1's buffer + its upper halo plane (nullable)
+    int nz, P, H;                // local planes, states, halo planes per side (= v)
+    float4 *lo_dst;              // rank-1's buffer + its upper halo planes (nullable)
     long long lo_state;          // rank-1's voxels per state
-    float4 *hi_dst;              // rank+1's buffer + its lower halo plane (nullable)
+    float4 *hi_dst;              // rank+1's buffer + its lower halo planes (nullable)
     long long hi_state;
     const double *rec_src;       // this rank's records [P][nrec][kNR] (nullable)
     int nrec, nrec_max, world, rank;

@@ -330,9 +330,10 @@ class _SlabGeometry:
     slab drivers: global chunk size, slab grid, per-rank record counts, the
     local / padded / gathered record buffers and their all-gather."""
 
-    def __init__(self, ctx, nx, ny, nz_total, P, dist):
+    def __init__(self, ctx, nx, ny, nz_total, P, dist, H=1):
+        """H: halo planes per side of the slab arrays (the cfg's v)."""
         from .api import _grid
-        self.ctx, self.dist, self.P = ctx, dist, P
+        self.ctx, self.dist, self.P, self.H = ctx, dist, P, H
         self.world = dist.get_world_size() if dist is not None else 1
         self.rank = dist.get_rank() if dist is not None else 0
         self.nx, self.ny, self.nz_total = nx, ny, nz_total
@@ -351,7 +352,7 @@ class _SlabGeometry:
         self.rec = torch.zeros((P, self.nrec, 10), dtype=torch.float64, device=self.dev)
         self.rec_pad = torch.zeros((P, self.nrec_max, 10), dtype=torch.float64, device=self.dev)
         self.gathered = torch.zeros((self.world, P, self.nrec_max, 10), dtype=torch.float64, device=self.dev)
-        self.halo = {k: torch.zeros((P, self.plane, 4), dtype=torch.float32, device=self.dev)
+        self.halo = {k: torch.zeros((P, H * self.plane, 4), dtype=torch.float32, device=self.dev)
                      for k in ("send_lo", "send_hi", "recv_lo", "recv_hi")}
 
     def gather_records(self) -> torch.Tensor:
@@ -370,7 +371,7 @@ class _SlabGeometry:
         return self.gathered
 
     def exchange(self, pack, unpack):
-        """pack(op, buf) fills buf with boundary plane op (0 lower, 1 upper);
+        """pack(op, buf) fills buf with the H boundary planes op (0 lower, 1 upper);
         unpack(op, buf or None) writes the halo (2 lower, 3 upper; None at the
         volume ends = zero fill)."""
         h = self.halo
@@ -385,11 +386,12 @@ class _SlabGeometry:
         unpack(3, h["recv_hi"] if self.rank < self.world - 1 else None)
 
     def slab_planes(self, t: torch.Tensor) -> torch.Tensor:
-        """Planes [z0 - 1, z0 + nz + 1) of a full-volume [nz_total][...] tensor,
+        """Planes [z0 - H, z0 + nz + H) of a full-volume [nz_total][...] tensor,
         zero where they fall outside the volume."""
-        out = torch.zeros((self.nz + 2,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.dev)
-        lo, hi = max(self.z0 - 1, 0), min(self.z0 + self.nz + 1, self.nz_total)
-        out[lo - (self.z0 - 1): hi - (self.z0 - 1)] = t[lo:hi].to(self.dev)
+        H = self.H
+        out = torch.zeros((self.nz + 2 * H,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.dev)
+        lo, hi = max(self.z0 - H, 0), min(self.z0 + self.nz + H, self.nz_total)
+        out[lo - (self.z0 - H): hi - (self.z0 - H)] = t[lo:hi].to(self.dev)
         return out
 
 
@@ -403,13 +405,14 @@ class SlabIfcm:
 
     def __init__(self, ctx, cfg, nx, ny, nz_total, P, dist=None):
         self.ctx, self.cfg, self.P, self.dist = ctx, cfg, P, dist
-        self.geo = _SlabGeometry(ctx, nx, ny, nz_total, P, dist)
+        self.H = H = cfg.v  # halo planes per side (Eq. 9 radius in z)
+        self.geo = _SlabGeometry(ctx, nx, ny, nz_total, P, dist, H)
         g = self.geo
         self.world, self.rank, self.tz = g.world, g.rank, g.tz
         self.nx, self.ny, self.nz_total = nx, ny, nz_total
         self.z0, self.nz, self.grid, self.plane = g.z0, g.nz, g.grid, g.plane
         self.dev = g.dev
-        self.Ua = torch.zeros((P, (self.nz + 2) * self.plane, 4), dtype=torch.float32, device=self.dev)
+        self.Ua = torch.zeros((P, (self.nz + 2 * H) * self.plane, 4), dtype=torch.float32, device=self.dev)
         self.Ub = torch.zeros_like(self.Ua)
         self.centers = torch.zeros((P, 4), dtype=torch.float32, device=self.dev)
         self.stats = torch.zeros((P, 4), dtype=torch.float64, device=self.dev)
@@ -423,32 +426,32 @@ class SlabIfcm:
         return self.x
 
     def set_x(self, x_slab: torch.Tensor):
-        """x of the slab's arrays [nz + 2][ny][pitch] (halo planes included)."""
+        """x of the slab's arrays [nz + 2H][ny][pitch] (halo planes included)."""
         self.x = x_slab
 
     def load_state(self, U_full: torch.Tensor, centers: torch.Tensor):
         """U_full [P][nz_total*ny*nx][4]: this slab's planes (halos exchanged later)."""
-        pl = self.plane
-        self.Ua[:, pl: pl * (self.nz + 1)] = U_full[:, self.z0 * pl:(self.z0 + self.nz) * pl].to(self.dev)
+        pl, H = self.plane, self.H
+        self.Ua[:, H * pl: pl * (self.nz + H)] = U_full[:, self.z0 * pl:(self.z0 + self.nz) * pl].to(self.dev)
         self.centers.copy_(centers.view(self.P, 4))
         self.stats.zero_()
         self.swaps = 0
 
     def load_local(self, U_slab: torch.Tensor, centers: torch.Tensor):
-        """U_slab [P][(nz+2)*ny*nx][4] already in the slab layout."""
+        """U_slab [P][(nz+2H)*ny*nx][4] already in the slab layout."""
         self.Ua.copy_(U_slab.view_as(self.Ua))
         self.centers.copy_(centers.view(self.P, 4))
         self.stats.zero_()
         self.swaps = 0
 
     def local_U(self) -> torch.Tensor:
-        return self.Ua[:, self.plane: self.plane * (self.nz + 1)]
+        return self.Ua[:, self.H * self.plane: self.plane * (self.nz + self.H)]
 
     # -- one iteration
     def exchange(self, U):
-        ctx, g, P = self.ctx, self.grid, self.P
-        self.geo.exchange(lambda op, buf: ctx.slab_halo(g, P, op, U, buf),
-                          lambda op, buf: ctx.slab_halo(g, P, op, U, buf))
+        ctx, g, P, H = self.ctx, self.grid, self.P, self.H
+        self.geo.exchange(lambda op, buf: ctx.slab_halo(g, P, op, U, buf, v=H),
+                          lambda op, buf: ctx.slab_halo(g, P, op, U, buf, v=H))
 
     def step(self, lam_xi: torch.Tensor, eps: float = 0.0):
         """One iteration (no host synchronisation).  A converged state is
@@ -512,12 +515,13 @@ class SlabIfcmP2P:
     def __init__(self, ctx, cfg, nx, ny, nz_total, P, dist=None):
         from . import _abi
         self.ctx, self.cfg, self.P, self.dist = ctx, cfg, P, dist
-        self.geo = g = _SlabGeometry(ctx, nx, ny, nz_total, P, dist)
+        self.H = H = cfg.v  # halo planes per side
+        self.geo = g = _SlabGeometry(ctx, nx, ny, nz_total, P, dist, H)
         self.world, self.rank, self.nz, self.grid, self.plane = g.world, g.rank, g.nz, g.grid, g.plane
         if self.world > _abi.MAX_PEERS:
             raise RuntimeError(f"peer exchange supports at most {_abi.MAX_PEERS} ranks")
         self.dev = g.dev
-        sb = P * (self.nz + 2) * self.plane * 16
+        sb = P * (self.nz + 2 * H) * self.plane * 16
         rb = self.world * P * g.nrec_max * 10 * 8
         # every step below is agreed on by all ranks, so that either all of
         # them use peer memory or none does (a rank that cannot map a peer
@@ -564,7 +568,7 @@ class SlabIfcmP2P:
             pe.U[0][w], pe.U[1][w], pe.rec[0][w], pe.rec[1][w], pe.flags[w] = ptrs[w]
             pe.nz[w] = allh[w][1]
         self.peers = pe
-        shape = (P, (self.nz + 2) * self.plane, 4)
+        shape = (P, (self.nz + 2 * H) * self.plane, 4)
         self.U = [_as_tensor(self._own[i], shape, torch.float32, self.dev) for i in range(2)]
         self.centers = torch.zeros((P, 4), dtype=torch.float32, device=self.dev)
         self.stats = torch.zeros((P, 4), dtype=torch.float64, device=self.dev)
@@ -591,18 +595,18 @@ class SlabIfcmP2P:
     def load_state(self, U_full: torch.Tensor, centers: torch.Tensor):
         """U_full [P][nz_total*ny*nx][4]: this slab's local planes (the outer
         halo planes stay zero, the interior ones are exchanged by the run)."""
-        pl = self.plane
-        self.U[self.cur][:, pl: pl * (self.nz + 1)] = U_full[:, self.geo.z0 * pl:(self.geo.z0 + self.nz) * pl]
+        pl, H = self.plane, self.H
+        self.U[self.cur][:, H * pl: pl * (self.nz + H)] = U_full[:, self.geo.z0 * pl:(self.geo.z0 + self.nz) * pl]
         self.centers.copy_(centers.view(self.P, 4))
 
     def load_local(self, U_slab: torch.Tensor, centers: torch.Tensor):
-        """U_slab [P][(nz+2)*ny*nx][4] in the slab layout (local planes used)."""
-        pl = self.plane
-        self.U[self.cur][:, pl: pl * (self.nz + 1)] = U_slab.view(self.P, -1, 4)[:, pl: pl * (self.nz + 1)]
+        """U_slab [P][(nz+2H)*ny*nx][4] in the slab layout (local planes used)."""
+        pl, H = self.plane, self.H
+        self.U[self.cur][:, H * pl: pl * (self.nz + H)] = U_slab.view(self.P, -1, 4)[:, H * pl: pl * (self.nz + H)]
         self.centers.copy_(centers.view(self.P, 4))
 
     def local_U(self) -> torch.Tensor:
-        return self.U[self.cur][:, self.plane: self.plane * (self.nz + 1)]
+        return self.U[self.cur][:, self.H * self.plane: self.plane * (self.nz + self.H)]
 
     @property
     def Ua(self) -> torch.Tensor:
@@ -639,13 +643,13 @@ class SlabPso:
         from dataclasses import replace
         self.ctx, self.cfg, self.dist = ctx, cfg, dist
         self.pso = replace(pso, p_begin=0, p_end=0)
-        self.geo = _SlabGeometry(ctx, nx, ny, nz_total, pso.P, dist)
+        self.geo = _SlabGeometry(ctx, nx, ny, nz_total, pso.P, dist, cfg.v)
         self.grid = self.geo.grid
         self.ws = ctx.slab_workspace(self.grid, cfg, self.pso)
         self.check_every = check_every
 
     def init(self, U0_slab: torch.Tensor, c0: torch.Tensor):
-        """U0_slab [(nz+2)*ny*nx][4] (slab layout), c0 [4]."""
+        """U0_slab [(nz+2v)*ny*nx][4] (slab layout), c0 [4]."""
         self.ctx.slab_pso_init(self.grid, self.cfg, self.pso, U0_slab, c0, self.ws)
 
     def generation(self, x_slab: torch.Tensor):
@@ -717,8 +721,9 @@ class SlabSegmenter:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
         # Alg. 2 step 1: global min-max (all-reduce) and the R15 histogram
-        v = g.slab_planes(vol)                      # [nz+2][ny][nx], zero outside the volume
-        own = v[1: g.nz + 1]
+        H = g.H
+        v = g.slab_planes(vol)                      # [nz+2H][ny][nx], zero outside the volume
+        own = v[H: g.nz + H]
         mm = torch.zeros(2, dtype=torch.int32, device=self.dev)
         ctx.minmax_u8(own, mm)
         if g.world > 1:
@@ -727,10 +732,14 @@ class SlabSegmenter:
             self._allreduce(hi, d.ReduceOp.MAX)
             mm = torch.cat([lo, hi])
         x = ctx.normalize_u8_range(v, mm)
-        if g.z0 == 0:
-            x[0].zero_()
-        if g.z0 + g.nz == g.nz_total:
-            x[g.nz + 1].zero_()
+        # halo planes outside the volume stay zero (normalising the zero
+        # padding would give them the value of intensity 0)
+        lo_out = max(0, H - g.z0)
+        hi_out = max(0, g.z0 + g.nz + H - g.nz_total)
+        if lo_out:
+            x[:lo_out].zero_()
+        if hi_out:
+            x[g.nz + 2 * H - hi_out:].zero_()
         hist = ctx.hist_u8(own, mm)
         if g.world > 1:
             self._allreduce(hist, d.ReduceOp.SUM)
@@ -748,9 +757,9 @@ class SlabSegmenter:
         c_prev, c_fcm, fst = ctx.fcm_hist(counts, mm, c0, cfg)
         pl = self.nx * self.ny
         U0 = sl.Ua[0]
-        U0[:pl].zero_()
-        U0[pl * (g.nz + 1):].zero_()
-        ctx.fcm_memberships(x[1: g.nz + 1], c_prev, cfg.C, cfg.m, self.nx, U=U0[pl: pl * (g.nz + 1)])
+        U0[:H * pl].zero_()
+        U0[pl * (g.nz + H):].zero_()
+        ctx.fcm_memberships(x[H: g.nz + H], c_prev, cfg.C, cfg.m, self.nx, U=U0[H * pl: pl * (g.nz + H)])
         fcm_iters = int(fst[2].item())
         ev[2].record()
         # Alg. 1 steps 3-10: PSO over slabs from (U_fcm, c_fcm)

@@ -25,11 +25,11 @@ def _state():
     return x, np.stack([U0, U1]), np.stack([c0, c1])
 
 
-def _run(cls, ctx, dist, iters, eps):
+def _run(cls, ctx, dist, iters, eps, v=1):
     from paper_2002_01981_b200 import IfcmConfig, to_aos, to_pitched_x
     dev = torch.device("cuda:0")
     x, U, c = _state()
-    s = cls(ctx, IfcmConfig(C=C), NX, NY, NZ, P, dist)
+    s = cls(ctx, IfcmConfig(C=C, v=v), NX, NY, NZ, P, dist)
     s.load_x(to_pitched_x(x, dev))
     cen = torch.zeros((P, 4), device=dev)
     cen[:, :C] = torch.as_tensor(c)
@@ -46,27 +46,27 @@ def _run(cls, ctx, dist, iters, eps):
     return out, out2
 
 
-def _worker(rank, world, port, cls_name, iters, eps, q):
+def _worker(rank, world, port, cls_name, iters, eps, q, v=1):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2002_01981_b200 import Context
     from paper_2002_01981_b200 import dist as D
-    out, out2 = _run(getattr(D, cls_name), Context(0), dist, iters, eps)
+    out, out2 = _run(getattr(D, cls_name), Context(0), dist, iters, eps, v)
     q.put((rank, out, out2))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def _two_ranks(cls_name, iters, eps):
+def _two_ranks(cls_name, iters, eps, v=1):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     cm = mp.get_context("spawn")
     q = cm.Queue()
-    procs = [cm.Process(target=_worker, args=(r, 2, port, cls_name, iters, eps, q)) for r in range(2)]
+    procs = [cm.Process(target=_worker, args=(r, 2, port, cls_name, iters, eps, q, v)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
@@ -79,16 +79,17 @@ def _two_ranks(cls_name, iters, eps):
     return U, res[0][1][1], res[0][1][2], res[0][1][3], U2, res[0][2][1], res
 
 
-@pytest.mark.parametrize("iters,eps", [(3, 0.0), (40, 1e-3)])
-def test_p2p_equals_collectives_and_single_rank(iters, eps):
+@pytest.mark.parametrize("iters,eps,v", [(3, 0.0, 1), (40, 1e-3, 1), (3, 0.0, 2)])
+def test_p2p_equals_collectives_and_single_rank(iters, eps, v):
+    """v = 2: the put kernel moves two boundary planes per side."""
     from paper_2002_01981_b200 import Context
     from paper_2002_01981_b200.dist import SlabIfcm, SlabIfcmP2P
     ctx = Context(0)
-    (U1, c1, st1, d1, _), (U1b, c1b) = _run(SlabIfcmP2P, ctx, None, iters, eps)
-    (Ur, cr, str_, dr, _), (Urb, crb) = _run(SlabIfcm, ctx, None, iters, eps)
+    (U1, c1, st1, d1, _), (U1b, c1b) = _run(SlabIfcmP2P, ctx, None, iters, eps, v)
+    (Ur, cr, str_, dr, _), (Urb, crb) = _run(SlabIfcm, ctx, None, iters, eps, v)
     assert (U1 == Ur).all() and (c1 == cr).all() and (st1 == str_).all()
     assert (U1b == Urb).all() and (c1b == crb).all()
-    U2, c2, st2, d2, U2b, c2b, res = _two_ranks("SlabIfcmP2P", iters, eps)
+    U2, c2, st2, d2, U2b, c2b, res = _two_ranks("SlabIfcmP2P", iters, eps, v)
     assert (U2 == U1).all(), np.abs(U2 - U1).max()
     assert (c2 == c1).all() and (st2 == st1).all() and d2 == d1
     for r in res:  # every rank holds the same centres and stats

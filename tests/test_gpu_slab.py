@@ -35,8 +35,9 @@ def _state():
     return x, np.stack([U0, U1]), np.stack([c0, c1])
 
 
-def _virtual_slabs(ctx, world, iters, lx):
-    """All slabs in one process: halos copied between slab objects directly."""
+def _virtual_slabs(ctx, world, iters, lx, v=1):
+    """All slabs in one process: halos (v planes per side) copied between slab
+    objects directly."""
     from paper_2002_01981_b200 import IfcmConfig, to_aos, to_pitched_x
     from paper_2002_01981_b200.dist import SlabIfcm
     x, U, c = _state()
@@ -45,7 +46,8 @@ def _virtual_slabs(ctx, world, iters, lx):
     Ut = to_aos(U, dev)
     ct = torch.zeros((P, 4), device=dev)
     ct[:, :C] = torch.as_tensor(c)
-    cfg = IfcmConfig(C=C)
+    cfg = IfcmConfig(C=C, v=v)
+    H = v
     slabs = []
     for r in range(world):
         s = SlabIfcm(ctx, cfg, NX, NY, NZ, P, dist=_OneRank(world, r))
@@ -56,16 +58,16 @@ def _virtual_slabs(ctx, world, iters, lx):
     pl = NX * NY
     for _ in range(iters):
         for i, s in enumerate(slabs):
-            if i > 0:
+            if i > 0:  # the lower neighbour's last H local planes
                 nb = slabs[i - 1]
-                s.geo.halo["recv_lo"].copy_(nb.Ua[:, nb.nz * pl:(nb.nz + 1) * pl])
-            if i < world - 1:
+                s.geo.halo["recv_lo"].copy_(nb.Ua[:, nb.nz * pl:(nb.nz + H) * pl])
+            if i < world - 1:  # the upper neighbour's first H local planes
                 nb = slabs[i + 1]
-                s.geo.halo["recv_hi"].copy_(nb.Ua[:, pl:2 * pl])
+                s.geo.halo["recv_hi"].copy_(nb.Ua[:, H * pl:2 * H * pl])
         for s in slabs:
             h = s.geo.halo
-            s.ctx.slab_halo(s.grid, P, 2, s.Ua, h["recv_lo"] if s.rank > 0 else None)
-            s.ctx.slab_halo(s.grid, P, 3, s.Ua, h["recv_hi"] if s.rank < world - 1 else None)
+            s.ctx.slab_halo(s.grid, P, 2, s.Ua, h["recv_lo"] if s.rank > 0 else None, v=H)
+            s.ctx.slab_halo(s.grid, P, 3, s.Ua, h["recv_hi"] if s.rank < world - 1 else None, v=H)
             s.ctx.slab_step(s.grid, cfg, s.x, s.Ua, s.Ub, s.centers, lxt, s.geo.rec)
             s.geo.rec_pad.zero_()
             s.geo.rec_pad[:, : s.geo.nrec] = s.geo.rec
@@ -78,12 +80,14 @@ def _virtual_slabs(ctx, world, iters, lx):
     return U_full, slabs[0].centers.clone(), slabs[0].stats.clone(), [s.centers for s in slabs]
 
 
-def test_slab_equals_whole_volume_and_is_g_invariant():
+@pytest.mark.parametrize("v", [1, 2])
+def test_slab_equals_whole_volume_and_is_g_invariant(v):
+    """v = 2: two Chebyshev shells (Eq. 9-10), two halo planes per side."""
     from paper_2002_01981_b200 import Context, IfcmConfig, to_aos, to_pitched_x
     ctx = Context(0)
     lx = [[0.6, 0.8], [1.0, 1.0]]
-    U1, c1, st1, _ = _virtual_slabs(ctx, 1, 3, lx)
-    U3, c3, st3, cs = _virtual_slabs(ctx, 3, 3, lx)
+    U1, c1, st1, _ = _virtual_slabs(ctx, 1, 3, lx, v=v)
+    U3, c3, st3, cs = _virtual_slabs(ctx, 3, 3, lx, v=v)
     assert (U1 == U3).all()                       # memberships: per voxel, identical
     assert (c1 == c3).all() and (st1 == st3).all()  # reductions: G-invariant
     for c in cs:
@@ -96,23 +100,25 @@ def test_slab_equals_whole_volume_and_is_g_invariant():
     cen = torch.zeros((P, 4), device=dev)
     cen[:, :C] = torch.as_tensor(c)
     lxt = torch.tensor(lx, dtype=torch.float64, device=dev)
-    ctx.iterate(to_pitched_x(x, dev), Uin, Uo, cen, lxt, IfcmConfig(C=C), iters=3, nx=NX)
+    ctx.iterate(to_pitched_x(x, dev), Uin, Uo, cen, lxt, IfcmConfig(C=C, v=v), iters=3, nx=NX)
     assert torch.equal(Uo, U3)
     assert torch.allclose(cen, c3, rtol=1e-6, atol=0)
 
 
-def test_slab_parity_with_oracle(orc):
+@pytest.mark.parametrize("v", [1, 2])
+def test_slab_parity_with_oracle(orc, v):
     """One slab step from the same state vs the fp64 oracle (1e-4 / 1e-4)."""
     x, U, c = _state()
-    U3, c3, st3, _ = _virtual_slabs(__import__("paper_2002_01981_b200").Context(0), 3, 1, [[0.4, 0.7], [0.9, 0.2]])
+    U3, c3, st3, _ = _virtual_slabs(__import__("paper_2002_01981_b200").Context(0), 3, 1, [[0.4, 0.7], [0.9, 0.2]],
+                                    v=v)
     for p, (l, s) in enumerate([(0.4, 0.7), (0.9, 0.2)]):
-        Uo, co, Jo, _ = orc.ifcm_step(x, U[p], c[p], l, s)
+        Uo, co, Jo, _ = orc.ifcm_step(x, U[p], c[p], l, s, v=v, h=1.0)
         assert np.abs(U3[p, :, :C].cpu().numpy() - Uo).max() < 1e-4
         assert np.all(np.abs(c3[p, :C].cpu().numpy() - co) <= 1e-4 * np.abs(co))
         assert abs(st3[p, 0].item() - Jo) <= 1e-4 * Jo
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, v=1):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -122,7 +128,7 @@ def _worker(rank, world, port, q):
     ctx = Context(0)
     x, U, c = _state()
     dev = torch.device("cuda:0")
-    s = SlabIfcm(ctx, IfcmConfig(C=C), NX, NY, NZ, P, dist)
+    s = SlabIfcm(ctx, IfcmConfig(C=C, v=v), NX, NY, NZ, P, dist)
     s.load_x(to_pitched_x(x, dev))
     ct = torch.zeros((P, 4), device=dev)
     ct[:, :C] = torch.as_tensor(c)
@@ -133,17 +139,18 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_slab_driver_two_ranks():
+@pytest.mark.parametrize("v", [1, 2])
+def test_slab_driver_two_ranks(v):
     from paper_2002_01981_b200 import Context
     ctx = Context(0)
-    U1, c1, st1, _ = _virtual_slabs(ctx, 1, 3, [[0.6, 0.8], [1.0, 1.0]])
+    U1, c1, st1, _ = _virtual_slabs(ctx, 1, 3, [[0.6, 0.8], [1.0, 1.0]], v=v)
     s_ = socket.socket()
     s_.bind(("127.0.0.1", 0))
     port = s_.getsockname()[1]
     s_.close()
     cm = mp.get_context("spawn")
     q = cm.Queue()
-    procs = [cm.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [cm.Process(target=_worker, args=(r, 2, port, q, v)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=180) for _ in range(2)], key=lambda t: t[0])

@@ -65,8 +65,9 @@ def test_slab_pso_eval_parity(ctx, orc):
     assert np.abs(Ul.cpu().numpy()[:, :C] - r.U).max() < 1e-4
 
 
-@pytest.mark.parametrize("C,shape,P,G,seed", [(3, (20, 24, 28), 4, 3, 99), (4, (26, 33, 35), 5, 2, 1)])
-def test_slab_segmenter_oracle(ctx, orc, C, shape, P, G, seed):
+@pytest.mark.parametrize("C,shape,P,G,seed,v", [(3, (20, 24, 28), 4, 3, 99, 1), (4, (26, 33, 35), 5, 2, 1, 1),
+                                                (4, (20, 26, 30), 4, 2, 7, 2)])
+def test_slab_segmenter_oracle(ctx, orc, C, shape, P, G, seed, v):
     """The whole slab pipeline against the oracle's Alg. 1 / Alg. 2: same GMM
     start, same PSO trajectory (bit-identical lambda*, xi*), labels identical
     on >= 99.9 % of voxels and centres within 1e-3 where the final IFCM is
@@ -74,22 +75,28 @@ def test_slab_segmenter_oracle(ctx, orc, C, shape, P, G, seed):
     from paper_2002_01981_b200 import IfcmConfig, PsoConfig
     from paper_2002_01981_b200.dist import SlabSegmenter
     vol, _ = _case(C, shape, seed=11)
-    cfg = IfcmConfig(C=C, eps=1e-5, max_iter=100)
+    cfg = IfcmConfig(C=C, eps=1e-5, max_iter=100, v=v)
     pso = PsoConfig(P=P, max_gen=G, patience=0, seed=seed)
     seg = SlabSegmenter(ctx, cfg, pso, vol.shape)
     rep = seg.segment(torch.as_tensor(vol, device="cuda:0"))
-    r = orc.segment_u8(vol, C=C, P=P, max_gen=G, seed=seed)
+    r = orc.segment_u8(vol, C=C, P=P, max_gen=G, seed=seed, v=v)
     assert np.abs(np.array(rep["c_init"]) - r.c_init).max() < 1e-6
     assert rep["lambda"] == r.lam and rep["xi"] == r.xi
     assert rep["generations"] == G
     if min(r.lam, r.xi) > 0.95:
-        pytest.skip(f"ill-conditioned final IFCM at lambda*={r.lam:.3f}, xi*={r.xi:.3f}")
+        # ill-conditioned final IFCM: same-state parity instead (tests/illcond.py)
+        from tests.illcond import final_state_step_parity
+        final_state_step_parity(ctx, orc, torch.as_tensor(vol, device="cuda:0"), seg.ifcm.local_U()[0].reshape(-1, 4),
+                                rep["centers"], rep["lambda"], rep["xi"], cfg)
+        return
     agree = (seg.labels.cpu().numpy() == r.labels).mean()
     assert agree >= 0.999, agree
-    assert np.allclose(rep["centers"], r.c, rtol=1e-3)
+    # centres after up to 100 final-IFCM iterations from different roundings;
+    # the 124-neighbour map (v = 2) drifts further (as test_mode_segment_parity)
+    assert np.allclose(rep["centers"], r.c, rtol=1e-3 if v == 1 else 1e-2)
 
 
-def _worker(rank, world, port, shape, q):
+def _worker(rank, world, port, shape, q, v=1):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -98,7 +105,8 @@ def _worker(rank, world, port, shape, q):
     from paper_2002_01981_b200.dist import SlabSegmenter
     ctx = Context(0)
     vol, _ = _case(4, shape, seed=6)
-    seg = SlabSegmenter(ctx, IfcmConfig(C=4), PsoConfig(P=5, max_gen=4, patience=0, seed=31), vol.shape, dist)
+    seg = SlabSegmenter(ctx, IfcmConfig(C=4, v=v), PsoConfig(P=5, max_gen=4, patience=0, seed=31), vol.shape,
+                        dist)
     seg.keep_trace = True
     rep = seg.segment(torch.as_tensor(vol, device="cuda:0"))
     q.put((rank, seg.labels.cpu().numpy(), rep, np.stack([t.numpy() for t in seg.trace]),
@@ -115,14 +123,16 @@ def _port():
     return p
 
 
-def test_slab_segmenter_g_invariant(ctx):
+@pytest.mark.parametrize("v", [1, 2])
+def test_slab_segmenter_g_invariant(ctx, v):
     """One rank and two ranks (2 + 1 z-chunks, uneven) give bit-identical
-    labels, lambda*, xi*, J, centres, iteration counts and fitness traces."""
+    labels, lambda*, xi*, J, centres, iteration counts and fitness traces
+    (v = 2: two halo planes per side exchanged every generation / iteration)."""
     from paper_2002_01981_b200 import IfcmConfig, PsoConfig
     from paper_2002_01981_b200.dist import SlabSegmenter
     shape = (40, 26, 30)
     vol, _ = _case(4, shape, seed=6)
-    seg = SlabSegmenter(ctx, IfcmConfig(C=4), PsoConfig(P=5, max_gen=4, patience=0, seed=31), vol.shape)
+    seg = SlabSegmenter(ctx, IfcmConfig(C=4, v=v), PsoConfig(P=5, max_gen=4, patience=0, seed=31), vol.shape)
     seg.keep_trace = True
     ref = seg.segment(torch.as_tensor(vol, device="cuda:0"))
     ref_lab = seg.labels.cpu().numpy()
@@ -130,7 +140,7 @@ def test_slab_segmenter_g_invariant(ctx):
     cm = mp.get_context("spawn")
     q = cm.Queue()
     port = _port()
-    procs = [cm.Process(target=_worker, args=(r, 2, port, shape, q)) for r in range(2)]
+    procs = [cm.Process(target=_worker, args=(r, 2, port, shape, q, v)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=240) for _ in range(2)], key=lambda t: t[0])

@@ -108,3 +108,51 @@ def test_eq11_worked_example(orc):
     want = np.array([(0.0 + 0.3 * 1.0) / 2, (0.7 + 0.3 + 0.0) / 2, (0.35 + 0.15 + 0.15) / 2])
     assert np.allclose(J, want, rtol=0, atol=1e-15)
     assert np.allclose(orc.eq11(q, t, 1.0), [0.0, 0.5, 0.25])
+
+
+@pytest.mark.parametrize("shape,t", [((7, 9, 8), 3), ((7, 9, 8), 0), ((7, 9, 8), 5)])
+def test_step_planes_v2_is_the_whole_step_on_the_target(orc, shape, t):
+    """The plane-restricted step with two shells (v = 2, Eq. 9-10) gives the
+    whole v = 2 step's rows on the target plane, bit for bit."""
+    nz, ny, nx = shape
+    x, U, c = random_state(nx, ny, nz, 4, seed=11 + t, crisp_frac=0.1)
+    Uw, _, _, _ = orc.ifcm_step(x, U, c, 0.6, 0.8, v=2, h=1.0)
+    Un, _, _, _ = orc.ifcm_step_planes(x, U, c, 0.6, 0.8, t, t + 1, v=2, h=1.0)
+    pl = nx * ny
+    assert (Un[t * pl:(t + 1) * pl] == Uw[t * pl:(t + 1) * pl]).all()
+
+
+def test_slice_mode_v2_of_a_single_plane_is_the_pipeline(orc):
+    """nz = 1 with v = 2: the slice pipeline equals the whole v = 2 pipeline."""
+    img, _ = cube_phantom(26, 22, 1, (0.1, 0.5, 0.9))
+    vol = add_noise_u8(img, 7.0, 4)
+    r = orc.segment_u8(vol, C=3, P=4, max_gen=3, seed=9, v=2)
+    s = orc.segment_slice_u8(vol, 0, C=3, P=4, max_gen=3, seed=9, v=2)
+    assert (s.labels == r.labels[0]).all() and (s.U == r.U).all()
+    assert (s.lam, s.xi, s.J, s.final_iters) == (r.lam, r.xi, r.J, r.final_iters)
+
+
+@pytest.mark.parametrize("v", [1, 2])
+def test_slice_mode_reads_planes_within_v(orc, v):
+    """The slice mode of radius v depends on planes z - v .. z + v only
+    (Eq. 9): changing the planes beyond leaves every output identical,
+    changing a plane at distance v does not."""
+    img, _ = cube_phantom(18, 16, 9, (0.1, 0.35, 0.65, 0.9))
+    vol = add_noise_u8(img, 9.0, 3)
+    z = 4
+    kw = dict(C=4, P=4, max_gen=3, seed=5, v=v)
+    s = orc.segment_slice_u8(vol, z, **kw)
+    far = vol.copy()
+    g = np.random.default_rng(1)
+    lo, hi = int(vol.min()), int(vol.max())
+    for k in range(9):
+        if abs(k - z) > v:  # new values inside the volume's range (Alg. 2 step 1 unchanged)
+            far[k] = g.integers(lo, hi + 1, size=far[k].shape, dtype=np.uint8)
+    far[0, 0, 0], far[8, 0, 0] = lo, hi
+    assert far.min() == lo and far.max() == hi
+    f = orc.segment_slice_u8(far, z, **kw)
+    assert (f.labels == s.labels).all() and (f.U == s.U).all() and f.J == s.J
+    near = vol.copy()
+    near[z + v] = 255 - near[z + v]
+    n = orc.segment_slice_u8(near, z, **kw)
+    assert not (n.U == s.U).all()
