@@ -1240,7 +1240,7 @@ int pifcm_hist_u8(pifcm_ctx *ctx, const uint8_t *vol, int64_t n, const uint32_t 
 
 // ============================================================== ABI: PSO over z-slabs
 // The swarm of a slab rank lives in a pifcm workspace laid out for the slab's
-// arrays (nz + 2 planes with the halos); every rank holds all particles.
+// arrays (nz + 2v planes with the halos); every rank holds all particles.
 static pifcm_grid plain_of(const pifcm_grid *s, int H) {
     return pifcm_grid{s->nx, s->ny, s->nz + 2 * H, s->pitch, 0, 0};
 }

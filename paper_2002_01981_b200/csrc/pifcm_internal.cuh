@@ -130,7 +130,7 @@ struct PsoUpdateArgs {
 // z-slab exchange over peer memory (p2p.cu)
 constexpr int kMaxPeers = 16;
 struct P2PPut {
-    const float4 *src;           // this rank's new states [P][nz+2][ny][nx]
+    const float4 *src;           // this rank's new states [P][nz+2H][ny][nx]
     long long plane, state;      // voxels per plane, per state (incl. halos)
     int nz, P, H;                // local planes, states, halo planes per side (= v)
     float4 *lo_dst;              // rank-1's buffer + its upper halo planes (nullable)

@@ -48,7 +48,10 @@ constexpr int kStepMinBlocks = PIFCM_STEP_MINBLOCKS;  // CTAs per SM the registe
 #define PIFCM_RING 5
 #endif
 constexpr int kRing = PIFCM_RING;  // planes in flight: z-1, z, z+1 in use, the rest prefetching
-constexpr int kStencilSmem = kRing * (kUStagePad + kXStagePad) + 128;
+#ifndef PIFCM_SMEM_SLACK
+#define PIFCM_SMEM_SLACK 128
+#endif
+constexpr int kStencilSmem = kRing * (kUStagePad + kXStagePad) + PIFCM_SMEM_SLACK;
 
 // Warp-cooperative fp64 re-evaluation of the Eq. 4 factors of one voxel (the
 // ill-conditioned band): lane k < 26 takes neighbour k of

@@ -1,5 +1,5 @@
 """z-slab sharding of the IFCM iteration: a volume split into
-slabs with one halo plane per side gives memberships bit-identical to the
+slabs with v halo planes per side (v = 1, 2) gives memberships bit-identical to the
 whole-volume step and centres / J bit-identical for any number of slabs (the
 reductions use global z-chunks fixed by the volume, pifcm_slab_chunk); across processes (gloo, two
 ranks on one GPU) through the SlabIfcm driver."""
