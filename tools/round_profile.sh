@@ -12,6 +12,8 @@ if [ -z "$NOTESTS" ]; then
       > gpurun_out/gputests_${TAG}.log 2>&1
   tail -5 gpurun_out/gputests_${TAG}.log
 fi
+timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > gpurun_out/smoke_${TAG}.log 2>&1
+tail -2 gpurun_out/smoke_${TAG}.log
 timeout 600 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 tail -c 3000 gpurun_out/bench_${TAG}.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_${TAG}.json 2>&1
@@ -28,7 +30,8 @@ timeout 600 python bench.py --workload C2 --steps 5 --warmup 3 > gpurun_out/benc
 tail -c 1500 gpurun_out/bench_c2_${TAG}.json
 timeout 900 python bench.py --workload C4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4_${TAG}.json 2> gpurun_out/bench_c4_${TAG}.err
 tail -c 800 gpurun_out/bench_c4_${TAG}.json
-[ -z "$NOSAN" ] && bash tools/sanitize.sh ${SANCASES:-3d v2 pipe modes}
+# (compute-sanitizer is closed on the GPU pool; SAN=1 runs it where allowed)
+[ -n "$SAN" ] && bash tools/sanitize.sh ${SANCASES:-3d v2 pipe modes}
 # CPU only: the oracle against itself from an fp32-rounded start at C3 (DESIGN 7)
 [ -n "$CHAOS" ] && timeout 2400 python tools/chaos_c3.py gpurun_out/chaos_c3_${TAG}.json > gpurun_out/chaos.log 2>&1
 true
