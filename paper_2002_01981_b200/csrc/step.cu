@@ -910,6 +910,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // U states: 5-D (4 floats, x, y, z, state); x: 3-D (x, y, z) with pitched rows.
+#ifndef PIFCM_U_L2_PROMOTION
+#define PIFCM_U_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 static bool make_maps(const StepArgs &a, CUtensorMap *mU, CUtensorMap *mX) {
     auto enc = encode_fn();
     if (!enc) return false;
@@ -920,7 +923,7 @@ static bool make_maps(const StepArgs &a, CUtensorMap *mU, CUtensorMap *mX) {
     const cuuint32_t bu[4] = {4 * kSX, kSY, 1, 1};
     const cuuint32_t e5[5] = {1, 1, 1, 1, 1};
     if (enc(mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float4 *>(a.U_in), du, su, bu, e5,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, PIFCM_U_L2_PROMOTION,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     const cuuint64_t dx[3] = {(cuuint64_t)a.nx, (cuuint64_t)a.ny, (cuuint64_t)a.nz};
