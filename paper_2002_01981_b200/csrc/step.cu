@@ -48,6 +48,9 @@ constexpr int kStepMinBlocks = PIFCM_STEP_MINBLOCKS;  // CTAs per SM the registe
 #define PIFCM_RING 5
 #endif
 constexpr int kRing = PIFCM_RING;  // planes in flight: z-1, z, z+1 in use, the rest prefetching
+#ifndef PIFCM_STATE_Y
+#define PIFCM_STATE_Y 1  // 3D step grid (tile, state, chunk) instead of (tile, chunk, state)
+#endif
 #ifndef PIFCM_SMEM_SLACK
 #define PIFCM_SMEM_SLACK 128
 #endif
@@ -182,14 +185,17 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     __shared__ __align__(8) uint64_t full[kRing];
     __shared__ int released[kRing];
 
-    const int p = blockIdx.z;
+    // grid (tile, state, chunk): the states of one (tile, chunk) run side by
+    // side, so the intensity planes they share are read from L2, not HBM
+    const int p = PIFCM_STATE_Y ? blockIdx.y : blockIdx.z;
+    const int chunk = PIFCM_STATE_Y ? blockIdx.z : blockIdx.y;
     if (a.stop && *a.stop) return;
     if (a.stats && a.stats[4 * p + 3] != 0.0) return;
 
     const int tile = blockIdx.x;
     const int x0 = (tile % a.tiles_x) * kTX;
     const int y0 = (tile / a.tiles_x) * kTY;
-    const int zb = a.z_lo + blockIdx.y * a.tz;
+    const int zb = a.z_lo + chunk * a.tz;
     const int ze = min(zb + a.tz, a.z_lo + a.nz_t);
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
@@ -560,7 +566,7 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
     if (HF) return;  // no reductions: H, F only
     float num[kMaxC] = {num2[0].x, num2[0].y, num2[1].x, num2[1].y};
     float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
-    const int blk = blockIdx.x + gridDim.x * blockIdx.y;
+    const int blk = blockIdx.x + gridDim.x * chunk;  // record index: (tile, chunk), whatever the grid order
     block_partials<kWarpsY>(num, den, Jacc, duacc, a.partials + ((long long)p * a.nblk + blk) * kNR);
     // the ring is idle now: its shared memory is the finaliser's scratch
     // (no static 10 KB array, which would cost a CTA slot per SM)
@@ -948,7 +954,7 @@ static cudaError_t launch_stencil(const StepArgs &a, int P, cudaStream_t st) {
     }
     CUtensorMap mU, mX;
     if (!make_maps(a, &mU, &mX)) return cudaErrorInvalidValue;
-    dim3 grid(a.tiles_x * a.tiles_y, a.zchunks, P);
+    dim3 grid(a.tiles_x * a.tiles_y, PIFCM_STATE_Y ? P : a.zchunks, PIFCM_STATE_Y ? a.zchunks : P);
     k_step_stencil<C, M2, DU, HF><<<grid, kStepThreads, kStencilSmem, st>>>(mU, mX, a);
     return cudaGetLastError();
 }
