@@ -175,13 +175,15 @@ __global__ void __launch_bounds__(kStepThreads, Shells<V>::MINBLOCKS)
     __shared__ __align__(8) uint64_t full[RING];
     __shared__ int released[RING];
 
-    const int p = blockIdx.z;
+    // grid (tile, state, chunk) as the v = 1 kernel: the states of a
+    // tile-chunk share its intensity planes in L2
+    const int p = blockIdx.y, chunk = blockIdx.z;
     if (a.stop && *a.stop) return;
     if (a.stats && a.stats[4 * p + 3] != 0.0) return;
     const int tile = blockIdx.x;
     const int x0 = (tile % a.tiles_x) * kTX;
     const int y0 = (tile / a.tiles_x) * kTY;
-    const int zb = a.z_lo + blockIdx.y * a.tz;
+    const int zb = a.z_lo + chunk * a.tz;
     const int ze = min(zb + a.tz, a.z_lo + a.nz_t);
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(kStepThreads, Shells<V>::MINBLOCKS)
     if (HF) return;  // no reductions: H, F only
     float num[kMaxC] = {num2[0].x, num2[0].y, num2[1].x, num2[1].y};
     float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
-    const int blk = blockIdx.x + gridDim.x * blockIdx.y;
+    const int blk = blockIdx.x + gridDim.x * chunk;
     block_partials<kWarpsY>(num, den, Jacc, duacc, a.partials + ((long long)p * a.nblk + blk) * kNR);
     finalize_if_last<kStepThreads>(a, p, a.nblk, reinterpret_cast<double(*)[kNR]>(smem_raw));
 }
@@ -442,7 +444,7 @@ static cudaError_t launch_shells_t(const StepArgs &a, int P, cudaStream_t st) {
     }
     CUtensorMap mU, mX;
     if (!make_maps2<V>(a, &mU, &mX)) return cudaErrorInvalidValue;
-    dim3 grid(a.tiles_x * a.tiles_y, a.zchunks, P);
+    dim3 grid(a.tiles_x * a.tiles_y, P, a.zchunks);
     k_step_shells<C, M2, DU, QL, V, HF><<<grid, kStepThreads, Shells<V>::SMEM, st>>>(mU, mX, a);
     return cudaGetLastError();
 }

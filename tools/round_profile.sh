@@ -32,6 +32,7 @@ timeout 900 python bench.py --workload C4 --steps 1 --warmup 3 --no-cpu-baseline
 tail -c 800 gpurun_out/bench_c4_${TAG}.json
 # (compute-sanitizer is closed on the GPU pool; SAN=1 runs it where allowed)
 [ -n "$SAN" ] && bash tools/sanitize.sh ${SANCASES:-3d v2 pipe modes}
+[ -n "$SHELLS" ] && timeout 900 python tools/time_shells.py > gpurun_out/time_shells_${TAG}.json 2> gpurun_out/time_shells.err
 # CPU only: the oracle against itself from an fp32-rounded start at C3 (DESIGN 7)
 [ -n "$CHAOS" ] && timeout 2400 python tools/chaos_c3.py gpurun_out/chaos_c3_${TAG}.json > gpurun_out/chaos.log 2>&1
 true
