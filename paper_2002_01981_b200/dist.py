@@ -313,7 +313,7 @@ def _halo_sendrecv(dist, rank, world, send_lo, send_hi, recv_lo, recv_hi):
         ops += [("send", send_hi, rank + 1), ("recv", recv_hi, rank + 1)]
     if not ops:
         return
-    if dist.get_backend() == "gloo":
+    if dist.get_backend() == "gloo" and any(t.device.type == "cuda" for _, t, _ in ops):
         torch.cuda.current_stream().synchronize()
     bufs = [(k, _coll_tensor(dist, t), t, peer) for k, t, peer in ops]
     reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend if k == "send" else dist.irecv, b, peer)
@@ -347,7 +347,7 @@ class _SlabGeometry:
             nrecs.append(ctx.slab_records(_grid(nx, ny, nz, z0=z0, nz_total=nz_total)))
         self.nrec = nrecs[self.rank]
         self.nrec_max = max(nrecs)
-        self.dev = torch.device(f"cuda:{ctx.device}")
+        self.dev = getattr(ctx, "torch_device", None) or torch.device(f"cuda:{ctx.device}")
         self.counts = torch.tensor(nrecs, dtype=torch.int32, device=self.dev)
         self.rec = torch.zeros((P, self.nrec, 10), dtype=torch.float64, device=self.dev)
         self.rec_pad = torch.zeros((P, self.nrec_max, 10), dtype=torch.float64, device=self.dev)

@@ -163,3 +163,89 @@ def test_slab_chunk_depends_on_the_volume_only():
         assert slab_chunk(nx, ny, nz) == tz
     with pytest.raises(PifcmError):
         slab_chunk(0, 5, 5)
+
+
+class _HostCtx:
+    """The host-only part of a Context (pifcm_slab_chunk / pifcm_slab_records
+    need no GPU) with CPU tensors, for the slab bookkeeping on CPU ranks."""
+    torch_device = __import__("torch").device("cpu")
+
+    def __init__(self):
+        from paper_2002_01981_b200 import _abi
+        self.lib = _abi.load()
+
+    def slab_chunk(self, nx, ny, nz_total):
+        from paper_2002_01981_b200.api import slab_chunk
+        return slab_chunk(nx, ny, nz_total, self.lib)
+
+    def slab_records(self, grid):
+        import ctypes as ct
+        n = ct.c_int32()
+        assert self.lib.pifcm_slab_records(ct.byref(grid), ct.byref(n)) == 0
+        return n.value
+
+
+def _halo_worker(rank, world, port, H, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2002_01981_b200.dist import _SlabGeometry
+    nx, ny, nz_total, P = 5, 4, 40, 2
+    g = _SlabGeometry(_HostCtx(), nx, ny, nz_total, P, dist, H)
+    pl = nx * ny
+    # a state whose every voxel holds (state, global plane, voxel) in its row
+    U = torch.full((P, (g.nz + 2 * H) * pl, 4), -1.0)
+    for p in range(P):
+        for k in range(g.nz):
+            U[p, (H + k) * pl:(H + k + 1) * pl, 0] = p
+            U[p, (H + k) * pl:(H + k + 1) * pl, 1] = g.z0 + k
+
+    def pack(op, buf):  # the first / last H local planes (pifcm_slab_halo_v ops 0, 1)
+        src = H if op == 0 else g.nz
+        buf.copy_(U[:, src * pl:(src + H) * pl])
+
+    def unpack(op, buf):  # the lower / upper H halo planes (ops 2, 3), zeros outside the volume
+        dst = 0 if op == 2 else g.nz + H
+        U[:, dst * pl:(dst + H) * pl] = 0.0 if buf is None else buf
+
+    g.exchange(pack, unpack)
+    q.put((rank, g.z0, g.nz, U.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("H", [1, 2, 3])
+def test_slab_halo_exchange_two_ranks(H):
+    """The z-slab halo bookkeeping of the drivers (_SlabGeometry.exchange over
+    gloo, world 2, CPU): every rank's H lower / upper halo planes hold the
+    neighbour's global planes z0 - H .. z0 - 1 and z0 + nz .. z0 + nz + H - 1,
+    zeros outside the volume (v = H shells, Eq. 9-10)."""
+    import torch.multiprocessing as mp
+    port = _free_port()
+    cm = mp.get_context("spawn")
+    q = cm.Queue()
+    procs = [cm.Process(target=_halo_worker, args=(r, 2, port, H, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pl = 5 * 4
+    for rank, z0, nz, U in res:
+        for k in range(H):  # lower halo plane k = global plane z0 - H + k
+            gz = z0 - H + k
+            plane = U[:, k * pl:(k + 1) * pl]
+            if gz < 0:
+                assert (plane == 0).all()
+            else:
+                assert (plane[:, :, 1] == gz).all() and (plane[0, :, 0] == 0).all() and (plane[1, :, 0] == 1).all()
+        for k in range(H):  # upper halo plane k = global plane z0 + nz + k
+            gz = z0 + nz + k
+            plane = U[:, (H + nz + k) * pl:(H + nz + k + 1) * pl]
+            if gz >= 40:
+                assert (plane == 0).all()
+            else:
+                assert (plane[:, :, 1] == gz).all()
