@@ -250,6 +250,12 @@ int pifcm_iterate(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *
  * bit-identical to those (used by multi-rank pipelines that run the final
  * IFCM replicated on every rank). */
 #define PIFCM_ITER_CANONICAL 1
+/* With PIFCM_ITER_CANONICAL, a 2D image (nz = 1, v = 1), P = 1 and iters > 1
+ * run every iteration in one cooperative launch (a grid barrier and the
+ * canonical finalisation between the steps; results bit-identical to one
+ * launch per step) when its CTAs can all be resident; PIFCM_ITER_PER_STEP
+ * forces one launch per iteration. */
+#define PIFCM_ITER_PER_STEP 2
 int pifcm_iterate_ex(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cfg *cfg,
                      const float *x, const float *U_in, float *U_out, float *centers,
                      const double *lam_xi, int32_t P, int32_t iters, double *stats,

@@ -18,7 +18,8 @@ Q_LITERAL, Q_SQEUCLID = 0, 1
 FIT_CHAINED = 0
 FIT_ANCHORED = 1
 FIT_LEADER = 2
-ITER_CANONICAL = 1  # pifcm_iterate_ex flag
+ITER_CANONICAL = 1  # pifcm_iterate_ex flags
+ITER_PER_STEP = 2
 U8 = 0
 U16 = 1
 F32 = 2

@@ -242,10 +242,11 @@ class Context:
     def iterate(self, x: torch.Tensor, U_in: torch.Tensor, U_out: torch.Tensor,
                 centers: torch.Tensor, lam_xi: torch.Tensor, cfg: IfcmConfig, iters: int = 1,
                 stats: torch.Tensor | None = None, nx: int | None = None, stream=None,
-                canonical: bool = False):
+                canonical: bool = False, per_step: bool = False):
         """pifcm_iterate(_ex): x [nz,ny,pitch] f32; U_in/U_out [P,nz*ny*nx,4] f32;
         centers [P,4] f32; lam_xi [P,2] f64; stats [P,4] f64 or None.
-        canonical: the z-chunk decomposition of pifcm_segment's final IFCM."""
+        canonical: the z-chunk decomposition of pifcm_segment's final IFCM.
+        per_step: one launch per iteration (no cooperative 2D loop)."""
         nz, ny, pitch = x.shape
         P = U_in.shape[0]
         if nx is None:
@@ -257,7 +258,8 @@ class Context:
         ws = torch.empty(max(n.value, 1), dtype=torch.uint8, device=x.device)
         rc = self.lib.pifcm_iterate_ex(self._h, ct.byref(g), ct.byref(cfg.c()), _ptr(x), _ptr(U_in),
                                        _ptr(U_out), _ptr(centers), _ptr(lam_xi), P, iters, _ptr(stats),
-                                       _ptr(ws), n.value, _abi.ITER_CANONICAL if canonical else 0,
+                                       _ptr(ws), n.value,
+                                       (_abi.ITER_CANONICAL if canonical else 0) | (_abi.ITER_PER_STEP if per_step else 0),
                                        _stream(stream))
         self._ck(rc)
         return U_out

@@ -144,7 +144,7 @@ FcmHistArgs fcm_hist_args(void *ws, int nvals) {
 // Workspace layout (all offsets 256-byte aligned).
 struct Layout {
     size_t x, vol, lab, hist, mm, c0, slots, hdr, dhdr, pos, vel, pbf, pbx, fit, evalpos, cur, nxt,
-        gbc, cent, part, stats, lamxi, cnt, hf, shc, vcnt, fhws, cprev, fstats, total;
+        gbc, cent, part, stats, lamxi, cnt, gbar, hf, shc, vcnt, fhws, cprev, fstats, total;
     int nslots, P, Pl, p0, nblk, mode, eb;  // eb: states per evaluation launch (CHAINED)
     long long nvox;
 };
@@ -195,6 +195,7 @@ Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg 
     L.stats = take(sizeof(double) * 4 * (Pl > 1 ? Pl : 1));
     L.lamxi = take(sizeof(double) * 2 * (Pl > 1 ? Pl : 1));
     L.cnt = take(sizeof(unsigned) * (Pl > 1 ? Pl : 1));
+    L.gbar = take(sizeof(unsigned) * 2);  // grid barrier of the 2D final-IFCM loop
     L.hf = L.mode == PIFCM_FIT_CHAINED ? take(0) : take(sizeof(float4) * 2 * (size_t)L.nvox);
     L.shc = take(sizeof(float) * 4);
     // the FCM start on the value histogram (any quantised dtype)
@@ -270,12 +271,11 @@ int timed_step(pifcm_ctx *ctx, const StepArgs &a, int C, bool stencil, int P, lo
     return PIFCM_OK;
 }
 
-// One step launch + finalize for P states.
-int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x,
-             const float4 *Uin, float4 *Uout, const int *in_idx, const int *out_idx,
-             float *centers, const double *lamxi, bool stencil, int first, int P,
-             double *partials, double *fitness, double *stats, float eps, int *status,
-             const int *stop, cudaStream_t st, int n_in_states, unsigned *counters, bool canonical = false) {
+// The arguments of a step launch for P states.
+StepArgs step_args(const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x, const float4 *Uin,
+                   float4 *Uout, const int *in_idx, const int *out_idx, float *centers, const double *lamxi,
+                   int first, double *partials, double *fitness, double *stats, float eps, int *status,
+                   const int *stop, int n_in_states, unsigned *counters, bool canonical) {
     StepArgs a{};
     a.x = x;
     a.nx = g->nx; a.ny = g->ny; a.nz = g->nz; a.pitch = g->pitch;
@@ -295,12 +295,62 @@ int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, con
     a.stats_out = stats;
     a.eps = eps;
     a.status = status;
+    return a;
+}
+
+// One step launch + finalize for P states.
+int run_step(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x,
+             const float4 *Uin, float4 *Uout, const int *in_idx, const int *out_idx,
+             float *centers, const double *lamxi, bool stencil, int first, int P,
+             double *partials, double *fitness, double *stats, float eps, int *status,
+             const int *stop, cudaStream_t st, int n_in_states, unsigned *counters, bool canonical = false) {
+    const StepArgs a = step_args(g, cfg, x, Uin, Uout, in_idx, out_idx, centers, lamxi, first, partials, fitness,
+                                 stats, eps, status, stop, n_in_states, counters, canonical);
     int r = timed_step(ctx, a, cfg->C, stencil, P, a.nvox, st);
     if (r) return r;
     // Eq. 3 / Eq. 1 finalisation is fused: the last CTA of each state sums the
     // partial records (finalize_if_last in step.cu) -- in the canonical
     // decomposition exactly as k_slab_finalize sums the records of a slab split
     return PIFCM_OK;
+}
+
+// The iterations of one 2D state (nz = 1, v = 1) in one cooperative launch
+// (k_step_2d_loop: a grid barrier and the canonical finalisation between the
+// steps, the same records and sums as one launch per step, so the results are
+// bit-identical).  *used = false when it did not run (not 2D, or its CTAs
+// cannot all be resident): the caller then launches per step.  The iterations
+// run are stats[2] (read by the caller, who also passes them to
+// loop_timing_count when timing is on).
+int run_2d_loop(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x, float4 *UA,
+                float4 *UB, float *centers, const double *lamxi, int iters, double *partials, double *stats,
+                int *status, unsigned *counters, unsigned *gbar, cudaStream_t st, bool *used) {
+    *used = false;
+    if (g->nz != 1 || g->nz_total > 1 || cfg->v != 1 || iters < 2 || !gbar || !stats) return PIFCM_OK;
+    const StepArgs a = step_args(g, cfg, x, UA, UB, nullptr, nullptr, centers, lamxi, 0, partials, nullptr, stats,
+                                 cfg->eps, status, nullptr, 1, counters, true);
+    const bool timed = ctx->timing;
+    if (timed) {
+        while (ctx->tev.size() < ctx->tused + 2) {
+            cudaEvent_t e;
+            CK(ctx, cudaEventCreate(&e));
+            ctx->tev.push_back(e);
+        }
+        CK(ctx, cudaEventRecord(ctx->tev[ctx->tused], st));
+    }
+    LAUNCH(ctx, 1, launch_2d_loop(a, cfg->C, UA, UB, iters, gbar, st, used));
+    if (timed) {
+        CK(ctx, cudaEventRecord(ctx->tev[ctx->tused + 1], st));
+        if (ctx->tcls.size() < ctx->tused / 2 + 1) ctx->tcls.resize(ctx->tused / 2 + 1);
+        ctx->tcls[ctx->tused / 2] = 1;  // single-state class; launches / bytes added by loop_timing_count
+        ctx->tused += 2;
+    }
+    return PIFCM_OK;
+}
+// Count the iterations of a run_2d_loop launch as single-state launches.
+void loop_timing_count(pifcm_ctx *ctx, int done, long long vox) {
+    if (!ctx->timing) return;
+    ctx->t_bytes[1] += 36.0 * (double)vox * done;
+    ctx->t_launches[1] += done;
 }
 
 // lambda = xi = 0 exactly -> the pointwise FCM kernel (Eq. 4 reduces to the plain distance).
@@ -428,7 +478,7 @@ int pifcm_iterate_workspace_size(const pifcm_grid *grid, const pifcm_ifcm_cfg *c
     const int nblk = step_nblk_max(grid->nx, grid->ny, grid->nz);
     size_t b = align_up(sizeof(double) * kNR * (size_t)nblk * P, 256) +  // partials
                align_up(sizeof(double) * 4 * P, 256) + 256 +             // stats scratch + status
-               align_up(sizeof(unsigned) * P, 256);                      // finalisation counters
+               align_up(sizeof(unsigned) * P, 256) + 256;                // finalisation counters, grid barrier
     if (iters > 1) b += align_up(sizeof(float4) * (size_t)nvox * P, 256);
     *bytes = b;
     return PIFCM_OK;
@@ -446,7 +496,8 @@ int pifcm_iterate_ex(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cf
                      const float *U_in, float *U_out, float *centers, const double *lam_xi, int32_t P,
                      int32_t iters, double *stats, void *ws, size_t ws_bytes, int32_t flags,
                      pifcm_stream stream) {
-    if (flags & ~PIFCM_ITER_CANONICAL) return ctx ? fail(ctx, PIFCM_EINVAL, "unknown flags %d", flags) : PIFCM_EINVAL;
+    if (flags & ~(PIFCM_ITER_CANONICAL | PIFCM_ITER_PER_STEP))
+        return ctx ? fail(ctx, PIFCM_EINVAL, "unknown flags %d", flags) : PIFCM_EINVAL;
     const bool canonical = (flags & PIFCM_ITER_CANONICAL) != 0;
     if (!ctx) return PIFCM_EINVAL;
     int r;
@@ -471,6 +522,7 @@ int pifcm_iterate_ex(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cf
     double *st_scr = at<double>(ws, o); o = align_up(o + sizeof(double) * 4 * P, 256);
     int *status = at<int>(ws, o); o += 256;
     unsigned *counters = at<unsigned>(ws, o); o = align_up(o + sizeof(unsigned) * P, 256);
+    unsigned *gbar = at<unsigned>(ws, o); o += 256;
     float4 *scratch = iters > 1 ? at<float4>(ws, o) : nullptr;
     CK(ctx, cudaMemsetAsync(counters, 0, sizeof(unsigned) * P, st));
     double *S = stats ? stats : st_scr;
@@ -490,6 +542,25 @@ int pifcm_iterate_ex(pifcm_ctx *ctx, const pifcm_grid *grid, const pifcm_ifcm_cf
     const bool zero = host_zero_lamxi(lam_xi, P, st, &ok);
     if (!ok) return fail(ctx, PIFCM_ECUDA, "reading lam_xi failed");
     const float eps = cfg->eps;
+    if (canonical && !zero && P == 1 && iters > 1 && !(flags & PIFCM_ITER_PER_STEP)) {
+        // a 2D image: every iteration in one cooperative launch (bit-identical
+        // to one launch per step); buffers ordered so that, as below, step t
+        // writes U_out iff iters - t is even (launch_fixup_copy's convention)
+        float4 *Uo = reinterpret_cast<float4 *>(U_out);
+        float4 *UA = (iters & 1) ? scratch : Uo, *UB = (iters & 1) ? Uo : scratch;
+        bool used = false;
+        if (grid->nz == 1 && cfg->v == 1) {
+            CK(ctx, cudaMemcpyAsync(UA, U_in, sizeof(float4) * (size_t)nvox, cudaMemcpyDeviceToDevice, st));
+            if ((r = run_2d_loop(ctx, grid, cfg, x, UA, UB, centers, lam_xi, iters, partials, S, status, counters,
+                                 gbar, st, &used)))
+                return r;
+        }
+        if (used) {
+            loop_timing_count(ctx, iters, nvox);
+            if (eps > 0.f) LAUNCH(ctx, 1, launch_fixup_copy(scratch, Uo, nvox, P, S, iters, st));
+            return PIFCM_OK;
+        }
+    }
     const float4 *src = reinterpret_cast<const float4 *>(U_in);
     for (int t = 1; t <= iters; ++t) {
         float4 *dst = (((iters - t) & 1) == 0) ? reinterpret_cast<float4 *>(U_out) : scratch;
@@ -851,8 +922,24 @@ int pifcm_argmax(pifcm_ctx *ctx, const pifcm_grid *grid, int32_t C, const float 
 static int run_until(pifcm_ctx *ctx, const pifcm_grid *g, const pifcm_ifcm_cfg *cfg, const float *x,
                      float4 *slots, long long nvox, int a, int b, float *centers, const double *lamxi,
                      bool stencil, bool fcm_first, double *partials, double *stats, int *status, unsigned *counters,
-                     cudaStream_t st, int *res, int *iters) {
+                     cudaStream_t st, int *res, int *iters, unsigned *gbar = nullptr) {
     CK(ctx, cudaMemsetAsync(stats, 0, sizeof(double) * 4, st));
+    if (stencil && !fcm_first) {  // a 2D image: every iteration in one cooperative launch
+        bool used = false;
+        int r = run_2d_loop(ctx, g, cfg, x, slots + (long long)a * nvox, slots + (long long)b * nvox, centers, lamxi,
+                            cfg->max_iter, partials, stats, status, counters, gbar, st, &used);
+        if (r) return r;
+        if (used) {
+            double h[4];
+            CK(ctx, cudaMemcpyAsync(h, stats, sizeof h, cudaMemcpyDeviceToHost, st));
+            CK(ctx, cudaStreamSynchronize(st));
+            const int done = (int)h[2];
+            loop_timing_count(ctx, done, nvox);
+            *iters = done;
+            *res = (done % 2 == 1) ? b : a;
+            return PIFCM_OK;
+        }
+    }
     int src = a, dst = b, t = 0;
     // the host checks the device's convergence flag every 16 iterations: once
     // converged the remaining launches return at once (a few us each), which
@@ -1032,7 +1119,7 @@ int pifcm_segment(pifcm_ctx *ctx, const void *vol, int32_t dtype, int32_t nx, in
     const bool zero = (pres.lambda == 0.0 && pres.xi == 0.0);
     int fin_slot = gs, fin_iters = 0;
     if ((r = run_until(ctx, &g, cfg, x, slots, L.nvox, gs, other, cent, lamxi, !zero, false, partials, stats, status,
-                       at<unsigned>(ws, L.cnt), st, &fin_slot, &fin_iters)))
+                       at<unsigned>(ws, L.cnt), st, &fin_slot, &fin_iters, at<unsigned>(ws, L.gbar))))
         return r;
     CK(ctx, cudaEventRecord(ev[4], st));
     nvtx.phase("pifcm: defuzzify");

@@ -173,7 +173,11 @@ struct FcmHistArgs {
 // ---------------------------------------------------------------- launchers
 // All return cudaGetLastError() of the launch.
 cudaError_t launch_step(const StepArgs &a, int C, bool stencil, int P, cudaStream_t st);
-cudaError_t launch_step_shells(const StepArgs &a, int C, int P, cudaStream_t st);  // step_shells.cu (v = 2, 3)
+cudaError_t launch_step_shells(const StepArgs &a, int C, int P, cudaStream_t st);
+// the iterations of one 2D state in one cooperative launch; *used = false when
+// its CTAs cannot all be resident (step.cu)
+cudaError_t launch_2d_loop(const StepArgs &a, int C, float4 *UA, float4 *UB, int iters, unsigned *gbar,
+                           cudaStream_t st, bool *used);  // step_shells.cu (v = 2, 3)
 int step_nblk(int nx, int ny, int nz, bool stencil, int P);
 int slab_tz(int nx, int ny, int nz_total);
 int step_nblk_max(int nx, int ny, int nz);

@@ -584,21 +584,18 @@ __global__ void __launch_bounds__(kStepThreads, kStepMinBlocks)
 #define PIFCM_2D_MINBLOCKS 5
 #endif
 // A CTA walks a column of kTYB2D tiles in y, the next tile's TMA load in
-// flight while the current one is computed (two smem buffers).
+// flight while the current one is computed (two smem buffers).  One call =
+// this CTA's tiles of one Jacobi step of state p, ending with its block
+// record; `call` = how many earlier calls this CTA made (k_step_2d_loop's
+// iteration): the two TMA buffers' mbarrier parities continue across calls.
 template <int C, bool M2, bool DU>
-__global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
-    k_step_2d(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, const StepArgs a) {
+__device__ __forceinline__ void step2d_tiles(const CUtensorMap *pmU, const CUtensorMap *pmX, const StepArgs &a,
+                                             const int p, unsigned char *sbuf, uint64_t *bar, const int call) {
     constexpr int NP = (C + 1) / 2;
-    // TMA destinations: 128-byte aligned stages (as the 3D ring)
-    __shared__ __align__(128) unsigned char sbuf[2 * (kUStagePad + kXStagePad)];
-    __shared__ __align__(8) uint64_t bar[2];
     // (stage pointers are formed from the __shared__ array at each use, so the
     // compiler keeps them in the shared window: LDS, not generic loads)
     auto sUb = [&](int b) { return reinterpret_cast<float4 *>(sbuf + b * kUStagePad); };
     auto sXb = [&](int b) { return reinterpret_cast<float *>(sbuf + 2 * kUStagePad + b * kXStagePad); };
-    const int p = blockIdx.z;
-    if (a.stop && *a.stop) return;
-    if (a.stats && a.stats[4 * p + 3] != 0.0) return;
     const int txi = blockIdx.x % a.tiles_x;
     const int ty0 = (blockIdx.x / a.tiles_x) * kTYB2D;
     const int ntile = min(kTYB2D, a.tiles_y - ty0);
@@ -606,17 +603,11 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
     const int slot = a.in_idx ? a.in_idx[p] : p;
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
     auto issue = [&](int k) {
         const int b = k & 1, y0k = (ty0 + k) * kTY;
         mbar_expect_tx(&bar[b], kUStageBytes + kXStageBytes);
-        tma_load_4d(sUb(b), &tmU, &bar[b], 4 * (x0 - 1), y0k - 1, 0, slot);
-        tma_load_3d(sXb(b), &tmX, &bar[b], x0 - kXOff, y0k - 1, 0);
+        tma_load_4d(sUb(b), pmU, &bar[b], 4 * (x0 - 1), y0k - 1, 0, slot);
+        tma_load_3d(sXb(b), pmX, &bar[b], x0 - kXOff, y0k - 1, 0);
     };
     if (tid == 0) {
         issue(0);
@@ -624,8 +615,9 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
     }
     float4 *Uout = a.U_out + (long long)(a.out_idx ? a.out_idx[p] : p) * a.nvox;
     float2 c2[2];
-    c2[0] = make_float2(a.centers[4 * p + 0], a.centers[4 * p + 1]);
-    c2[1] = make_float2(a.centers[4 * p + 2], a.centers[4 * p + 3]);
+    // (L2 loads: in k_step_2d_loop another CTA finalised them this launch)
+    c2[0] = make_float2(__ldcg(a.centers + 4 * p + 0), __ldcg(a.centers + 4 * p + 1));
+    c2[1] = make_float2(__ldcg(a.centers + 4 * p + 2), __ldcg(a.centers + 4 * p + 3));
     const float lam = (float)a.lam_xi[2 * p], xi = (float)a.lam_xi[2 * p + 1];
     const float2 nlam2 = make_float2(-lam, -lam), nxi2 = make_float2(-xi, -xi);
     const float w2 = a.q_mode == 0 ? 4.0f : 2.0f, w3 = a.q_mode == 0 ? 9.0f : 3.0f;  // Eq. 7 q2 (R1)
@@ -652,7 +644,8 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
             invQ[r] = Qs > 0.f ? 1.0f / Qs : 0.f;
             if (gx < a.nx && gy < a.ny) vmask |= 1u << r;
         }
-        mbar_wait(&bar[b], (k >> 1) & 1);
+        // buffer b is used (ntile + 1 - b) / 2 times per call
+        mbar_wait(&bar[b], (unsigned)(call * ((ntile + 1 - b) / 2) + (k >> 1)) & 1u);
 
         float xr[kRY];
 #pragma unroll
@@ -769,7 +762,82 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
     float num[kMaxC] = {num2[0].x, num2[0].y, num2[1].x, num2[1].y};
     float den[kMaxC] = {den2[0].x, den2[0].y, den2[1].x, den2[1].y};
     block_partials<kWarpsY>(num, den, Jacc, duacc, a.partials + ((long long)p * a.nblk + blockIdx.x) * kNR);
+}
+
+template <int C, bool M2, bool DU>
+__global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
+    k_step_2d(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmX, const StepArgs a) {
+    // TMA destinations: 128-byte aligned stages (as the 3D ring)
+    __shared__ __align__(128) unsigned char sbuf[2 * (kUStagePad + kXStagePad)];
+    __shared__ __align__(8) uint64_t bar[2];
+    const int p = blockIdx.z;
+    if (a.stop && *a.stop) return;
+    if (a.stats && a.stats[4 * p + 3] != 0.0) return;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    step2d_tiles<C, M2, DU>(&tmU, &tmX, a, p, sbuf, bar, 0);
     finalize_if_last<kStepThreads>(a, p, a.nblk);
+}
+
+// Grid-wide barrier of a cooperative launch (every CTA resident): arrival
+// counter gbar[0], generation gbar[1] (both 0 before the launch).
+__device__ __forceinline__ void grid_barrier(unsigned *gbar, unsigned nblocks, unsigned &gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned target = gen + 1u;
+        if (atomicAdd(&gbar[0], 1u) == nblocks - 1u) {
+            gbar[0] = 0u;
+            __threadfence();
+            atomicExch(&gbar[1], target);
+        } else {
+            unsigned g;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gbar + 1) : "memory");
+            } while (g < target);
+        }
+        __threadfence();
+    }
+    ++gen;
+    __syncthreads();
+}
+
+// The final IFCM of one 2D state (nz = 1, P = 1) in one cooperative launch:
+// `iters` Jacobi steps ping-ponging between UA (input of step 0) and UB, each
+// followed by a grid barrier, the canonical finalisation by CTA 0 (the same
+// fixed-order sum, thread count and Eq. 3 / Eq. 1 as the last-CTA finaliser
+// of k_step_2d, so the results equal one launch per step bit for bit), a
+// second barrier, and the convergence test (stats[3], max|du| < eps).  Saves
+// the launch, ramp-up and tail of every step of a latency-bound small launch.
+template <int C, bool M2>
+__global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
+    k_step_2d_loop(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmX, const StepArgs a, float4 *UA, float4 *UB, int iters,
+                   unsigned *gbar) {
+    __shared__ __align__(128) unsigned char sbuf[2 * (kUStagePad + kXStagePad)];
+    __shared__ __align__(8) uint64_t bar[2];
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned gen = 0u;
+    for (int t = 0; t < iters; ++t) {
+        StepArgs at = a;
+        at.U_out = (t & 1) ? UA : UB;
+        // the previous step's states (generic stores) are read by TMA (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        step2d_tiles<C, M2, true>((t & 1) ? &tmB : &tmA, &tmX, at, 0, sbuf, bar, t);
+        grid_barrier(gbar, gridDim.x, gen);
+        if (blockIdx.x == 0) finalize_state<kStepThreads>(at, 0, a.nblk, reinterpret_cast<double(*)[kNR]>(sbuf));
+        grid_barrier(gbar, gridDim.x, gen);
+        if (__ldcg(a.stats_out + 3) != 0.0) break;  // converged (eps): the last step's output is final
+    }
 }
 
 // ----------------------------------------------------------------------------
@@ -979,6 +1047,55 @@ static cudaError_t launch_t(const StepArgs &a, bool stencil, int P, cudaStream_t
     dim3 grid(a.nblk, P);
     k_step_pointwise<C, M2><<<grid, kPwThreads, 0, st>>>(a);
     return cudaGetLastError();
+}
+
+template <int C, bool M2>
+static cudaError_t launch_2d_loop_t(const StepArgs &a, float4 *UA, float4 *UB, int iters, unsigned *gbar,
+                                    cudaStream_t st, bool *used) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_2d_loop<C, M2>, kStepThreads, 0) !=
+            cudaSuccess)
+        return cudaErrorInvalidValue;
+    const int grid = a.tiles_x * ((a.tiles_y + kTYB2D - 1) / kTYB2D);
+    if (grid > per_sm * nsm) return cudaSuccess;  // not co-resident: the caller launches per step
+    StepArgs aa = a, ab = a;
+    aa.U_in = UA;
+    ab.U_in = UB;
+    CUtensorMap mA, mB, mX, mX2;
+    if (!make_maps(aa, &mA, &mX) || !make_maps(ab, &mB, &mX2)) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(gbar, 0, 2 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    void *args[] = {&mA, &mB, &mX, &aa, &UA, &UB, &iters, &gbar};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(k_step_2d_loop<C, M2>), dim3(grid),
+                                    dim3(kStepThreads), args, 0, st);
+    if (e == cudaSuccess) *used = true;
+    return e;
+}
+
+// The iterations of one 2D state in one cooperative launch (k_step_2d_loop);
+// *used = false (and nothing launched) when the CTAs cannot all be resident.
+cudaError_t launch_2d_loop(const StepArgs &a0, int C, float4 *UA, float4 *UB, int iters, unsigned *gbar,
+                           cudaStream_t st, bool *used) {
+    *used = false;
+    StepArgs a = a0;
+    if (a.nz != 1 || a.v != 1 || a.hf) return cudaErrorInvalidValue;
+    a.tiles_x = (a.nx + kTX - 1) / kTX;
+    a.tiles_y = (a.ny + kTY - 1) / kTY;
+    a.z_lo = 0; a.nz_t = 1; a.goff = 0; a.nz_g = 1;
+    a.nblk = step_nblk(a.nx, a.ny, 1, true, 1);
+    a.in_idx = nullptr; a.out_idx = nullptr; a.stats = nullptr; a.stop = nullptr;
+    const bool m2 = a.m == 2.0f;
+    switch (C) {
+        case 2: return m2 ? launch_2d_loop_t<2, true>(a, UA, UB, iters, gbar, st, used)
+                          : launch_2d_loop_t<2, false>(a, UA, UB, iters, gbar, st, used);
+        case 3: return m2 ? launch_2d_loop_t<3, true>(a, UA, UB, iters, gbar, st, used)
+                          : launch_2d_loop_t<3, false>(a, UA, UB, iters, gbar, st, used);
+        case 4: return m2 ? launch_2d_loop_t<4, true>(a, UA, UB, iters, gbar, st, used)
+                          : launch_2d_loop_t<4, false>(a, UA, UB, iters, gbar, st, used);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t launch_step(const StepArgs &a0, int C, bool stencil, int P, cudaStream_t st) {

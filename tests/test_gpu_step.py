@@ -339,3 +339,31 @@ def test_small2d_multi_iteration(ctx, orc, shape, C, m, q_mode):
     for i, s in enumerate(states):
         _, _, it, _ = orc.ifcm_run(x, s[1], s[2], lams[i][0], lams[i][1], eps=1e-3, max_iter=100, m=m, q_mode=q_mode)
         assert abs(int(stats[i, 2].item()) - it) <= 1, (i, stats[i, 2].item(), it)
+
+
+@pytest.mark.parametrize("shape,iters,eps", [((96, 97), 20, 0.0), ((140, 41), 30, 1e-4), ((854, 854), 12, 0.0)])
+def test_2d_cooperative_loop_equals_per_step(ctx, shape, iters, eps):
+    """The final IFCM of a 2D image in one cooperative launch
+    (k_step_2d_loop: grid barriers, canonical finalisation by CTA 0) against
+    one launch per iteration: memberships, centres and stats bit-identical,
+    including an eps stop before the last iteration."""
+    from paper_2002_01981_b200 import IfcmConfig, to_aos, to_pitched_x
+    ny, nx = shape
+    x, U, c = random_state(nx, ny, 1, 4, seed=5, crisp_frac=0.1)
+    dev = torch.device("cuda:0")
+    xt = to_pitched_x(x, dev)
+    cfg = IfcmConfig(C=4, eps=eps)
+    lx = torch.tensor([[0.7, 0.9]], dtype=torch.float64, device=dev)
+    out = []
+    for per_step in (True, False):
+        Ui = to_aos(U, dev).view(1, -1, 4)
+        Uo = torch.empty_like(Ui)
+        cen = torch.zeros((1, 4), device=dev)
+        cen[0, :4] = torch.as_tensor(c)
+        st = torch.zeros((1, 4), dtype=torch.float64, device=dev)
+        ctx.iterate(xt, Ui, Uo, cen, lx, cfg, iters=iters, stats=st, nx=nx, canonical=True, per_step=per_step)
+        out.append((Uo.clone(), cen.clone(), st.clone()))
+    (U1, c1, s1), (U2, c2, s2) = out
+    assert torch.equal(U1, U2) and torch.equal(c1, c2) and torch.equal(s1, s2), (s1, s2)
+    if eps > 0:
+        assert 1 <= s1[0, 2].item() <= iters
