@@ -195,7 +195,7 @@ Layout layout(const pifcm_grid *g, const pifcm_ifcm_cfg *c, const pifcm_pso_cfg 
     L.stats = take(sizeof(double) * 4 * (Pl > 1 ? Pl : 1));
     L.lamxi = take(sizeof(double) * 2 * (Pl > 1 ? Pl : 1));
     L.cnt = take(sizeof(unsigned) * (Pl > 1 ? Pl : 1));
-    L.gbar = take(sizeof(unsigned) * 2);  // grid barrier of the 2D final-IFCM loop
+    L.gbar = take(sizeof(unsigned) * 3);  // grid barrier + release word of the 2D final-IFCM loop
     L.hf = L.mode == PIFCM_FIT_CHAINED ? take(0) : take(sizeof(float4) * 2 * (size_t)L.nvox);
     L.shc = take(sizeof(float) * 4);
     // the FCM start on the value histogram (any quantised dtype)

@@ -784,7 +784,8 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
 }
 
 // Grid-wide barrier of a cooperative launch (every CTA resident): arrival
-// counter gbar[0], generation gbar[1] (both 0 before the launch).
+// counter gbar[0], generation gbar[1] (both 0 before the launch; gbar[2] is
+// k_step_2d_loop's finalisation release word).
 __device__ __forceinline__ void grid_barrier(unsigned *gbar, unsigned nblocks, unsigned &gen) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -834,8 +835,22 @@ __global__ void __launch_bounds__(kStepThreads, PIFCM_2D_MINBLOCKS)
         asm volatile("fence.proxy.async.global;" ::: "memory");
         step2d_tiles<C, M2, true>((t & 1) ? &tmB : &tmA, &tmX, at, 0, sbuf, bar, t);
         grid_barrier(gbar, gridDim.x, gen);
-        if (blockIdx.x == 0) finalize_state<kStepThreads>(at, 0, a.nblk, reinterpret_cast<double(*)[kNR]>(sbuf));
-        grid_barrier(gbar, gridDim.x, gen);
+        // CTA 0 finalises; the others wait for its release word gbar[2]
+        // (a broadcast, not a second all-CTA barrier)
+        if (blockIdx.x == 0) {
+            finalize_state<kStepThreads>(at, 0, a.nblk, reinterpret_cast<double(*)[kNR]>(sbuf));
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicExch(&gbar[2], (unsigned)(t + 1));
+            }
+        } else if (threadIdx.x == 0) {
+            unsigned g;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gbar + 2) : "memory");
+            } while (g < (unsigned)(t + 1));
+            __threadfence();
+        }
+        __syncthreads();
         if (__ldcg(a.stats_out + 3) != 0.0) break;  // converged (eps): the last step's output is final
     }
 }
@@ -1065,7 +1080,7 @@ static cudaError_t launch_2d_loop_t(const StepArgs &a, float4 *UA, float4 *UB, i
     ab.U_in = UB;
     CUtensorMap mA, mB, mX, mX2;
     if (!make_maps(aa, &mA, &mX) || !make_maps(ab, &mB, &mX2)) return cudaErrorInvalidValue;
-    cudaError_t e = cudaMemsetAsync(gbar, 0, 2 * sizeof(unsigned), st);
+    cudaError_t e = cudaMemsetAsync(gbar, 0, 3 * sizeof(unsigned), st);
     if (e != cudaSuccess) return e;
     void *args[] = {&mA, &mB, &mX, &aa, &UA, &UB, &iters, &gbar};
     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(k_step_2d_loop<C, M2>), dim3(grid),
