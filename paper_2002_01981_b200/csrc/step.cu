@@ -1085,8 +1085,14 @@ static cudaError_t launch_2d_loop_t(const StepArgs &a, float4 *UA, float4 *UB, i
     void *args[] = {&mA, &mB, &mX, &aa, &UA, &UB, &iters, &gbar};
     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(k_step_2d_loop<C, M2>), dim3(grid),
                                     dim3(kStepThreads), args, 0, st);
-    if (e == cudaSuccess) *used = true;
-    return e;
+    if (e == cudaSuccess) {
+        *used = true;
+        return cudaSuccess;
+    }
+    // a refused cooperative launch (configuration, not a device fault): clear
+    // the error and let the caller launch one step at a time
+    (void)cudaGetLastError();
+    return cudaSuccess;
 }
 
 // The iterations of one 2D state in one cooperative launch (k_step_2d_loop);
