@@ -61,7 +61,11 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """nvidia-smi clocks and throttle reasons during the timed region: started
+    before the warm-up (nvidia-smi needs ~0.1 s to its first sample), every
+    sample time-stamped, only those inside [mark(), stop()] kept -- a timed
+    region shorter than the sampling period keeps the sample nearest to it
+    ("samples": 0)."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -70,12 +74,13 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.t0 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -84,11 +89,17 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self):
+        """The timed region starts now."""
+        self.t0 = time.time()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.time()
+        time.sleep(0.12)  # one more sample after the region, for the nearest-sample fallback
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -96,7 +107,14 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = self.t0 if self.t0 is not None else 0.0
+        inside = [ln for t, ln in self.lines if t0 <= t <= t1]
+        nearest = False
+        if not inside and self.lines:
+            mid = 0.5 * (t0 + t1)
+            inside = [min(self.lines, key=lambda tl: abs(tl[0] - mid))[1]]
+            nearest = True
+        for ln in inside:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -112,7 +130,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": 0 if nearest else len(sm)}
 
 
 def _volume(name="C3"):
@@ -339,7 +357,10 @@ def run_ours(args, rank, world, local_rank):
     def units(r):
         return r["units"] if "units" in r else Pw * r["generations"] + r["final_iters"]
 
-    # ---- warm-up
+    # ---- warm-up (the clock sampler starts here so it samples by the timed region)
+    clocks = ClockSampler(dev_index) if rank == 0 else None
+    if clocks:
+        clocks.start()
     rep = None
     for _ in range(args.warmup):
         rep = step()
@@ -353,10 +374,9 @@ def run_ours(args, rank, world, local_rank):
     # ---- timed region: device-resident input
     ctx.timing_enable(True)
     l0 = ctx.launch_count()
-    clocks = ClockSampler(dev_index) if rank == 0 else None
-    if clocks:
-        clocks.start()
     barrier()
+    if clocks:
+        clocks.mark()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
